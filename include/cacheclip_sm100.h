@@ -1,0 +1,217 @@
+/*
+ * cacheclip_sm100.h — C-ABI of libcacheclip_sm100.so, the B200 (sm_100a)
+ * kernels behind CacheClip's prefill hot path (arxiv 2510.10129).
+ *
+ * The reference (``cacheclip``, pure Python/numpy) has no FFI; its drop-in
+ * boundary is the Python function API (pkg/src/cacheclip/__init__.py:9-133).
+ * Each entry point below replaces the numpy body of one reference function;
+ * the Python package ``paper_2510_10129_b200`` keeps the reference names and
+ * signatures and calls these through ctypes.
+ *
+ * Conventions (all entry points):
+ *   - plain device pointers, element counts / strides as int64, a cudaStream_t
+ *     (passed as void*); no torch types, no allocation inside (caller-owned
+ *     workspaces), no host synchronisation, stream-ordered and reentrant;
+ *   - return 0 on success, otherwise a CC_ERR_* code; the message is
+ *     available from cc_last_error() (thread-local). Arguments are validated
+ *     before any launch, mirroring the reference's validate-before-mutate rule
+ *     (model.py:688-701, kv_store.py:206-225).
+ */
+#ifndef CACHECLIP_SM100_H_
+#define CACHECLIP_SM100_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CC_ABI_VERSION 1
+
+/* status codes -> Python exceptions (paper_2510_10129_b200/_lib.py) */
+#define CC_OK 0
+#define CC_ERR_VALUE 1       /* ValueError (bad selection, ids, ...)          */
+#define CC_ERR_DIMENSION 2   /* DimensionError (tensor_core.py:18)            */
+#define CC_ERR_CONSISTENCY 3 /* CacheConsistencyError (kv_store.py:52)        */
+#define CC_ERR_CUDA 4        /* RuntimeError: CUDA launch / driver failure    */
+#define CC_ERR_UNSUPPORTED 5 /* DimensionError: shape outside kernel support  */
+
+/* element types */
+#define CC_F32 0
+#define CC_BF16 1
+/* activation-operand layout for the 3xTF32 GEMM: row r of a [rows, K] matrix
+ * is stored as 3K floats [hi | hi | lo] with hi = tf32(x), lo = x - hi. */
+#define CC_F32_SPLIT3 2
+
+/* GEMM kinds */
+#define CC_GEMM_BF16 0   /* A, B bf16, fp32 accumulate in TMEM (tcgen05 kind::f16) */
+#define CC_GEMM_TF32X3 1 /* A = [hi|hi|lo], B = [hi|lo|hi] along K (kind::tf32)   */
+
+/* GEMM epilogues */
+#define CC_EPI_STORE 0    /* C = acc + bias                                      */
+#define CC_EPI_RESIDUAL 1 /* H(f32) += acc + bias                                */
+#define CC_EPI_GLU 2      /* C = act(gate + bg) * (up + bu), gate/up interleaved */
+#define CC_EPI_ACT 3      /* C = act(acc + bias)                                 */
+#define CC_EPI_QKV_ROPE 4 /* bias, RoPE q/k per row, q out, K/V scattered        */
+
+#define CC_ACT_SILU 0
+#define CC_ACT_GELU_TANH 1
+
+/* Library identity / device check. */
+int cc_abi_version(void);
+const char* cc_last_error(void);
+/* Returns CC_OK when device `dev` is sm_100 (B200) and the kernels load. */
+int cc_device_check(int dev);
+
+/* ------------------------------------------------------------------------
+ * (1) KV assembly — replaces the per-layer concatenate + rope_apply in
+ *     merge_caches (kv_store.py:237-248) and ChunkCache.attention_banks
+ *     (kv_store.py:106-116, single segment, local positions).
+ *
+ * Destination row r (0 <= r < n_dst_rows) is copied from exactly one segment;
+ * its key is rotated to position r (+ pos_offset), values pass through.
+ * Angles: theta = pos * inv_freq[i] in float64 (inv_freq from the host,
+ * computed as base ** (-2i/d) exactly like tensor_core.py:48-50), cos/sin
+ * rounded to float32, products separately rounded (bitwise rope_apply).
+ * Source/destination layout per tensor: [n_layers][rows][kv_heads][head_dim].
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  const void* k;     /* source keys (position-free), [n_layers][src_rows][H][D] */
+  const void* v;     /* source values                                            */
+  int64_t src_rows;  /* rows per layer in the source tensors                    */
+  int64_t src_row0;  /* first source row copied                                 */
+  int64_t dst_row0;  /* first destination row                                   */
+  int64_t n_rows;    /* rows in this segment                                    */
+} cc_kv_segment;
+
+int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows,
+                   int32_t n_layers, int32_t kv_heads, int32_t head_dim, int32_t dtype,
+                   const double* inv_freq_host, int64_t pos_offset,
+                   void* dst_k, void* dst_v, int64_t dst_rows_cap, void* stream);
+
+/* Per-row float32 cos/sin tables [n][head_dim/2] for arbitrary positions
+ * (float64 angle formation, tensor_core.py:41-51). */
+int cc_rope_table(const int64_t* positions, int64_t n, const double* inv_freq_host,
+                  int32_t head_dim, float* cos_out, float* sin_out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (2) Embedding gather + RMSNorm — _embed (model.py:484-492) and rms_norm
+ *     (tensor_core.py:99-106) feeding attention_qkv / _mlp / _final_logits.
+ * h_out (f32 residual stream, may be NULL): h = embed[ids[r]]
+ * x_out: rmsnorm(h) * gain in x_mode (CC_BF16 / CC_F32 / CC_F32_SPLIT3).
+ * ---------------------------------------------------------------------- */
+int cc_embed_rmsnorm(const int64_t* ids, int64_t rows, const void* embed, int32_t embed_dtype,
+                     int64_t vocab, int32_t d, float* h_out, const float* gain, float eps,
+                     void* x_out, int32_t x_mode, void* stream);
+int cc_rmsnorm(const float* h, int64_t rows, int32_t d, int64_t ld_h, const float* gain,
+               float eps, void* x_out, int32_t x_mode, void* stream);
+/* Weight preparation: fp32 [rows, cols] -> CC_BF16 or split layout
+ * (split_mode 0 = activation [hi|hi|lo], 1 = weight [hi|lo|hi]). */
+int cc_convert_matrix(const float* src, int64_t rows, int64_t cols, void* dst, int32_t dst_mode,
+                      int32_t split_weight, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (3) tcgen05 GEMM with fused epilogues — every x @ W in attention_qkv,
+ *     _attn_project_out and _mlp (model.py:340-432). C[M,N] = A[M,K]·B[N,K]^T,
+ *     both operands K-major (weights stored transposed, [out, in]).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t kind;      /* CC_GEMM_BF16 | CC_GEMM_TF32X3                            */
+  int32_t epilogue;  /* CC_EPI_*                                                 */
+  int64_t M, N, K;   /* logical sizes; operand row width is K (bf16) or 3K      */
+  const void* A; int64_t lda;  /* elements                                       */
+  const void* B; int64_t ldb;
+  const float* bias;           /* [N] (GLU: interleaved like B) or NULL          */
+  void* C; int64_t ldc; int32_t c_mode;  /* output (RESIDUAL: f32 H, in place)   */
+  int32_t act;                 /* CC_ACT_* for GLU / ACT                          */
+  int32_t glu_block;           /* GLU: gate/up interleave block (columns)         */
+  int64_t n_out;               /* GLU: valid output columns (d_ff)                */
+  /* QKV + RoPE epilogue */
+  int32_t n_q_heads, n_kv_heads, head_dim;
+  const float* rope_cos; const float* rope_sin;  /* [M][head_dim/2]              */
+  void* q_out; int64_t ldq; int32_t q_mode;
+  void* k_cache; void* v_cache; int32_t cache_dtype;   /* row = dst_rows[m]      */
+  const int64_t* dst_rows;     /* [M] cache row per GEMM row (NULL: identity)    */
+  void* k_raw;                 /* optional position-free K (chunk precompute)    */
+  const int64_t* raw_rows;     /* [M] row in k_raw (NULL: identity)              */
+} cc_gemm_args;
+
+int cc_gemm(const cc_gemm_args* args, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (4) Sparse-row attention — causal_attention(q, bank_k, bank_v,
+ *     row_limits=idx+1) in selective_forward (model.py:715-720) and the
+ *     mask_offset rule of layer_forward (model.py:467-476). Row i of q
+ *     (packed [m][Hq][D], rotated) attends cache rows [0, positions[i]] of
+ *     the bf16 bank [rows][Hkv][D]; GQA head h reads KV head h / (Hq/Hkv).
+ *     factor = scale/(sqrt(D)*temperature) per row (row_factor, or uniform).
+ * ---------------------------------------------------------------------- */
+int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions, int64_t m,
+                            const void* k_cache, const void* v_cache, int64_t n_keys,
+                            int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                            float factor, const float* row_factor,
+                            void* out, int64_t ldo, void* stream);
+
+/* Float32 banked causal attention (the fp32-faithful aux model path,
+ * peek_forward / prefill of the scoring model): for sequence s, new row i
+ * (global packed row row0[s] + i, i < n_new[s]) attends the sequence's bank
+ * rows [0, n_bank[s]) and new rows [0, i]. out_mode CC_F32 / CC_F32_SPLIT3
+ * writes the context; weights_out (optional, replaces the context) receives
+ * the softmax weights of bank columns [w_col0, n_bank[s]) as
+ * [s][head][i][col - w_col0] with row pitch w_ld (the last-layer scoring map,
+ * selector.py:157-165). */
+typedef struct {
+  const float* k;   /* bank keys (rotated) for this layer, [n_bank][Hkv][D] */
+  const float* v;
+  int64_t n_bank;
+  int64_t row0;     /* first packed new row */
+  int64_t n_new;
+} cc_bank_seq;
+
+int cc_banked_attention_f32(const cc_bank_seq* seqs_dev, int32_t n_seqs, int32_t max_new,
+                            int64_t max_bank, const float* q, const float* k_new,
+                            const float* v_new, int32_t n_q_heads, int32_t n_kv_heads,
+                            int32_t head_dim, float factor, void* out, int32_t out_mode,
+                            float* weights_out, int64_t w_col0, int64_t w_ld, void* stream);
+
+/* ------------------------------------------------------------------------
+ * (5) Importance reduction + grouped top-k — aux_score_tokens' head/query
+ *     mean (selector.py:163-165), selection_budget/top_candidates
+ *     (selector.py:113-129) and the per-chunk window rule (selector.py:182-214).
+ * ---------------------------------------------------------------------- */
+/* weights [n_seqs][H][Q][w_ld] -> scores[col_offset[s] + j], j < chunk_len[s]:
+ * in-order sum over heads / H, then in-order sum over queries / Q. */
+int cc_reduce_scores(const float* weights, int32_t n_seqs, int32_t n_heads, int32_t n_query,
+                     int64_t w_ld, const int64_t* chunk_lens_dev, const int64_t* col_offset_dev,
+                     int64_t max_chunk, float* scores, void* stream);
+
+/* Stable top-`budget` of scores (higher first, lower index on ties), then the
+ * window rule per chunk. Outputs: out_indices[0..*out_count) ascending
+ * (+ index_offset); win_selected / win_kept per window (windows enumerated
+ * chunk by chunk, ceil(len/window_len) each). Single CTA; workspace >=
+ * cc_select_workspace_bytes(n, n_chunks). */
+int64_t cc_select_workspace_bytes(int64_t n, int32_t n_chunks);
+int cc_select_topk_windows(const float* scores, int64_t n, const int64_t* chunk_lens_dev,
+                           int32_t n_chunks, int64_t n_windows, int64_t budget,
+                           int32_t window_len, int32_t threshold, int32_t expand,
+                           int64_t index_offset, int64_t* out_indices, int64_t* out_count,
+                           int32_t* win_selected, int32_t* win_kept, void* workspace,
+                           void* stream);
+
+/* ------------------------------------------------------------------------
+ * (6) First token — _final_logits (model.py:495-503) + argmax
+ *     (cli.py:233): RMSNorm of the last row, lm_head GEMV, argmax.
+ * ---------------------------------------------------------------------- */
+int64_t cc_lm_head_workspace_bytes(int64_t vocab);
+int cc_lm_head_argmax(const float* h_row, const float* gain, float eps, int32_t d,
+                      const void* lm_head, int32_t dtype, int64_t vocab, float* logits,
+                      int64_t* argmax_out, void* workspace, void* stream);
+
+/* Row gather for the residual stream (compaction helpers). */
+int cc_gather_i64(const int64_t* src, const int64_t* idx, int64_t n, int64_t* dst, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CACHECLIP_SM100_H_ */

@@ -1,0 +1,123 @@
+"""ctypes binding of libcacheclip_sm100.so (the C-ABI in include/cacheclip_sm100.h).
+
+There is deliberately no fallback: if the shared library is missing or the
+device is not sm_100, every hot-path call raises. Status codes map to the
+reference's exception classes (tensor_core.py:18, kv_store.py:36-52).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import CacheConsistencyError, DimensionError
+
+LIB_NAME = "libcacheclip_sm100.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+CC_OK, CC_ERR_VALUE, CC_ERR_DIMENSION, CC_ERR_CONSISTENCY, CC_ERR_CUDA, CC_ERR_UNSUPPORTED = range(6)
+CC_F32, CC_BF16, CC_F32_SPLIT3 = 0, 1, 2
+CC_GEMM_BF16, CC_GEMM_TF32X3 = 0, 1
+CC_EPI_STORE, CC_EPI_RESIDUAL, CC_EPI_GLU, CC_EPI_ACT, CC_EPI_QKV_ROPE = range(5)
+CC_ACT_SILU, CC_ACT_GELU_TANH = 0, 1
+
+i32, i64, f32, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p
+
+
+class KvSegment(ctypes.Structure):
+    _fields_ = [("k", vp), ("v", vp), ("src_rows", i64), ("src_row0", i64),
+                ("dst_row0", i64), ("n_rows", i64)]
+
+
+class BankSeq(ctypes.Structure):
+    _fields_ = [("k", vp), ("v", vp), ("n_bank", i64), ("row0", i64), ("n_new", i64)]
+
+
+class GemmArgs(ctypes.Structure):
+    _fields_ = [
+        ("kind", i32), ("epilogue", i32),
+        ("M", i64), ("N", i64), ("K", i64),
+        ("A", vp), ("lda", i64),
+        ("B", vp), ("ldb", i64),
+        ("bias", vp),
+        ("C", vp), ("ldc", i64), ("c_mode", i32),
+        ("act", i32), ("glu_block", i32), ("n_out", i64),
+        ("n_q_heads", i32), ("n_kv_heads", i32), ("head_dim", i32),
+        ("rope_cos", vp), ("rope_sin", vp),
+        ("q_out", vp), ("ldq", i64), ("q_mode", i32),
+        ("k_cache", vp), ("v_cache", vp), ("cache_dtype", i32),
+        ("dst_rows", vp),
+        ("k_raw", vp),
+        ("raw_rows", vp),
+    ]
+
+
+_SIGS = {
+    "cc_abi_version": ([], i32),
+    "cc_last_error": ([], ctypes.c_char_p),
+    "cc_device_check": ([i32], i32),
+    "cc_assemble_kv": ([vp, i32, i64, i32, i32, i32, i32, vp, i64, vp, vp, i64, vp], i32),
+    "cc_rope_table": ([vp, i64, vp, i32, vp, vp, vp], i32),
+    "cc_embed_rmsnorm": ([vp, i64, vp, i32, i64, i32, vp, vp, f32, vp, i32, vp], i32),
+    "cc_rmsnorm": ([vp, i64, i32, i64, vp, f32, vp, i32, vp], i32),
+    "cc_convert_matrix": ([vp, i64, i64, vp, i32, i32, vp], i32),
+    "cc_gemm": ([ctypes.POINTER(GemmArgs), vp], i32),
+    "cc_sparse_row_attention": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),
+    "cc_banked_attention_f32": ([vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, f32, vp, i32, vp, i64, i64, vp], i32),
+    "cc_reduce_scores": ([vp, i32, i32, i32, i64, vp, vp, i64, vp, vp], i32),
+    "cc_select_workspace_bytes": ([i64, i32], i64),
+    "cc_select_topk_windows": ([vp, i64, vp, i32, i64, i64, i32, i32, i32, i64, vp, vp, vp, vp, vp, vp], i32),
+    "cc_lm_head_workspace_bytes": ([i64], i64),
+    "cc_lm_head_argmax": ([vp, vp, f32, i32, vp, i32, i64, vp, vp, vp, vp], i32),
+    "cc_gather_i64": ([vp, vp, i64, vp, vp], i32),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+_lib = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load (once) and type the C-ABI library; raises if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"{LIB_NAME} not built ({path}); run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "— there is no CPU fallback for the CacheClip hot path")
+    lib = ctypes.CDLL(path)
+    for name, (args, res) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc == CC_OK:
+        return
+    msg = load().cc_last_error().decode("utf-8", "replace")
+    if rc == CC_ERR_VALUE:
+        raise ValueError(msg)
+    if rc in (CC_ERR_DIMENSION, CC_ERR_UNSUPPORTED):
+        raise DimensionError(msg)
+    if rc == CC_ERR_CONSISTENCY:
+        raise CacheConsistencyError(msg)
+    raise RuntimeError(f"libcacheclip_sm100: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args))
+
+
+_device_ok: set[int] = set()
+
+
+def require_device(dev: int) -> None:
+    """Fail loudly unless `dev` is a B200 (sm_100) the kernels can run on."""
+    if dev in _device_ok:
+        return
+    call("cc_device_check", dev)
+    _device_ok.add(dev)

@@ -1,0 +1,441 @@
+// Persistent warp-specialised tcgen05 GEMM for sm_100a with fused epilogues.
+//
+//   C[M,N] = A[M,K] · B[N,K]^T      (A activations, B weights [out, in], both K-major)
+//
+// Roles per CTA (192 threads, one CTA per SM):
+//   warp 0      TMA producer: A/B tiles -> 128B-swizzled smem ring (mbarrier full/empty)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, fp32 in TMEM)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
+// Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the
+// MMAs of tile i+1. kind::f16 (bf16) for the primary model; kind::tf32 over
+// [hi|hi|lo]·[hi|lo|hi] operands (3xTF32, fp32-faithful) for the scoring model.
+//
+// Replaces the numpy `x @ W` of attention_qkv / _attn_project_out / _mlp
+// (model.py:340-432) and fuses bias, RoPE + K/V scatter (model.py:709-714),
+// residual add and the gated activation (model.py:418-426) into the epilogue.
+#include "cc_common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace cc {
+
+constexpr int kBM = 128;
+constexpr int kGemmThreads = 192;
+
+template <int BN, bool kTF32>
+struct GemmCfg {
+  static constexpr int ELEM = kTF32 ? 4 : 2;
+  static constexpr int BK = 128 / ELEM;  // one 128-byte swizzle row per tile row
+  static constexpr int UK = kTF32 ? 8 : 16;
+  static constexpr int KSTEPS = BK / UK;
+  static constexpr int A_BYTES = kBM * 128;
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : 6;
+  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr uint32_t IDESC = umma_idesc(kBM, BN, kTF32);
+};
+
+struct EpiParams {
+  int epilogue;
+  int64_t M, N;
+  const float* bias;
+  void* C;
+  int64_t ldc;
+  int c_mode;
+  int act;
+  int64_t n_out;
+  int n_q_heads, n_kv_heads, head_dim;
+  const float* rope_cos;
+  const float* rope_sin;
+  void* q_out;
+  int64_t ldq;
+  int q_mode;
+  void* k_cache;
+  void* v_cache;
+  int cache_dtype;
+  const int64_t* dst_rows;
+  void* k_raw;
+  const int64_t* raw_rows;
+};
+
+__device__ __forceinline__ float act_apply(int act, float x) {
+  return act == CC_ACT_SILU ? silu_f(x) : gelu_tanh_f(x);
+}
+
+// Store 32 consecutive values of one row (cols [col0, col0+32)) in `mode`.
+// `width` = logical row width (split layout uses a 3*width pitch).
+__device__ __forceinline__ void store_row32(void* base, int mode, int64_t row, int64_t ld, int64_t col0,
+                                            int64_t width, const float* v) {
+  const bool full = (col0 + 32 <= width);
+  if (mode == CC_BF16) {
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(base) + row * ld + col0;
+    if (full && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[q * 8 + 2 * i], v[q * 8 + 2 * i + 1]);
+        reinterpret_cast<uint4*>(p)[q] = u;
+      }
+    } else {
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < width) p[j] = __float2bfloat16_rn(v[j]);
+    }
+  } else if (mode == CC_F32) {
+    float* p = reinterpret_cast<float*>(base) + row * ld + col0;
+    if (full && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j < width) p[j] = v[j];
+    }
+  } else {  // CC_F32_SPLIT3 : [hi | hi | lo]
+    float* p = reinterpret_cast<float*>(base) + row * ld * 3 + col0;
+    for (int j = 0; j < 32; ++j) {
+      if (col0 + j < width) {
+        float hi, lo, lh, ll;
+        split_tf32(v[j], hi, lo);
+        split_tf32(lo, lh, ll);
+        p[j] = hi;
+        p[width + j] = hi;
+        p[2 * width + j] = lh;
+      }
+    }
+  }
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tbase, int c0, int64_t grow,
+                                               int64_t n0, bool row_ok) {
+  float v[32];
+  if (ep.epilogue == CC_EPI_GLU) {
+    float u[32];
+    tmem_ld32(tbase + c0, v);
+    tmem_ld32(tbase + c0 + BN / 2, u);
+    if (!row_ok) return;
+    const int64_t ocol0 = n0 / 2 + c0;  // output column
+    const int64_t gcol = n0 + c0;       // interleaved gate column
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float g = v[j], up = u[j];
+      if (ep.bias) {
+        g += ep.bias[gcol + j];
+        up += ep.bias[gcol + BN / 2 + j];
+      }
+      v[j] = __fmul_rn(act_apply(ep.act, g), up);
+    }
+    store_row32(ep.C, ep.c_mode, grow, ep.ldc, ocol0, ep.n_out, v);
+    return;
+  }
+  tmem_ld32(tbase + c0, v);
+  if (!row_ok) return;
+  const int64_t col0 = n0 + c0;
+  if (col0 >= ep.N) return;
+  if (ep.bias) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < ep.N) v[j] += ep.bias[col0 + j];
+  }
+  switch (ep.epilogue) {
+    case CC_EPI_STORE:
+      store_row32(ep.C, ep.c_mode, grow, ep.ldc, col0, ep.N, v);
+      break;
+    case CC_EPI_ACT:
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = act_apply(ep.act, v[j]);
+      store_row32(ep.C, ep.c_mode, grow, ep.ldc, col0, ep.N, v);
+      break;
+    case CC_EPI_RESIDUAL: {
+      float* h = reinterpret_cast<float*>(ep.C) + grow * ep.ldc + col0;
+      if (col0 + 32 <= ep.N && ((reinterpret_cast<uintptr_t>(h) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 o = reinterpret_cast<float4*>(h)[q];
+          o.x = __fadd_rn(o.x, v[4 * q]);
+          o.y = __fadd_rn(o.y, v[4 * q + 1]);
+          o.z = __fadd_rn(o.z, v[4 * q + 2]);
+          o.w = __fadd_rn(o.w, v[4 * q + 3]);
+          reinterpret_cast<float4*>(h)[q] = o;
+        }
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (col0 + j < ep.N) h[j] = __fadd_rn(h[j], v[j]);
+      }
+      break;
+    }
+    case CC_EPI_QKV_ROPE: {
+      const int dh = ep.head_dim;
+      const int64_t qw = (int64_t)ep.n_q_heads * dh, kw = (int64_t)ep.n_kv_heads * dh;
+      if (col0 < qw + kw) {  // q or k: rotate adjacent pairs
+        const int half = dh >> 1;
+        const int p0 = (int)(col0 % dh) >> 1;
+        const float* cs = ep.rope_cos + grow * half + p0;
+        const float* sn = ep.rope_sin + grow * half + p0;
+        float r[32];
+#pragma unroll
+        for (int p = 0; p < 16; ++p) rope_pair(v[2 * p], v[2 * p + 1], cs[p], sn[p], r[2 * p], r[2 * p + 1]);
+        if (col0 < qw) {
+          store_row32(ep.q_out, ep.q_mode, grow, ep.ldq, col0, qw, r);
+        } else {
+          const int64_t drow = ep.dst_rows ? ep.dst_rows[grow] : grow;
+          store_row32(ep.k_cache, ep.cache_dtype, drow, kw, col0 - qw, kw, r);
+          if (ep.k_raw) {
+            const int64_t rrow = ep.raw_rows ? ep.raw_rows[grow] : grow;
+            store_row32(ep.k_raw, ep.cache_dtype, rrow, kw, col0 - qw, kw, v);
+          }
+        }
+      } else {
+        const int64_t drow = ep.dst_rows ? ep.dst_rows[grow] : grow;
+        store_row32(ep.v_cache, ep.cache_dtype, drow, kw, col0 - qw - kw, kw, v);
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+template <int BN, bool kTF32>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
+                int num_m, int num_n, int num_kb) {
+  using Cfg = GemmCfg<BN, kTF32>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + Cfg::STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = num_m * num_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int mb = t % num_m, nb = t / num_m;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          tma_load_2d(smem_a + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * Cfg::BK, mb * kBM);
+          tma_load_2d(smem_b + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * Cfg::BK, nb * BN);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a0 = smem_u32(smem_a + stage * Cfg::A_BYTES);
+          const uint32_t b0 = smem_u32(smem_b + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < Cfg::KSTEPS; ++k) {
+            tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
+                          (kb | k) != 0 ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+          if (kb == num_kb - 1) tc_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else {
+    // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    const int quarter = warp & 3;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const int mb = t % num_m, nb = t / num_m;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(quarter * 32) << 16);
+      const int64_t grow = (int64_t)mb * kBM + quarter * 32 + lane;
+      const bool row_ok = grow < ep.M;
+      const int64_t n0 = (int64_t)nb * BN;
+      const int cols = (ep.epilogue == CC_EPI_GLU) ? BN / 2 : BN;
+      for (int c0 = 0; c0 < cols; c0 += 32) epilogue_chunk<BN>(ep, tbase, c0, grow, n0, row_ok);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const void* ptr, bool f32, int64_t inner, int64_t rows, int64_t ld,
+                    int box_inner, int box_rows) {
+  auto enc = get_encode();
+  if (!enc) return fail(CC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int esz = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return CC_OK;
+}
+
+template <int BN, bool kTF32>
+static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaStream_t st) {
+  using Cfg = GemmCfg<BN, kTF32>;
+  CUtensorMap ta, tb;
+  int rc = make_map(&ta, a->A, kTF32, kop, a->M, a->lda, Cfg::BK, kBM);
+  if (rc) return rc;
+  rc = make_map(&tb, a->B, kTF32, kop, a->N, a->ldb, Cfg::BK, BN);
+  if (rc) return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_kernel<BN, kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    attr_set = true;
+  }
+  const int num_m = (int)((a->M + kBM - 1) / kBM);
+  const int num_n = (int)((a->N + BN - 1) / BN);
+  const int num_kb = (int)((kop + Cfg::BK - 1) / Cfg::BK);
+  const int tiles = num_m * num_n;
+  const int grid = tiles < num_sms() ? tiles : num_sms();
+  gemm_kernel<BN, kTF32><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb);
+  CC_LAUNCH_CHECK("gemm");
+  return CC_OK;
+}
+
+}  // namespace cc
+
+using namespace cc;
+
+extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
+  CC_CHECK_ARG(a, CC_ERR_VALUE, "null gemm args");
+  CC_CHECK_ARG(a->M >= 0 && a->N > 0 && a->K > 0, CC_ERR_DIMENSION, "bad GEMM shape M=%lld N=%lld K=%lld",
+               (long long)a->M, (long long)a->N, (long long)a->K);
+  if (a->M == 0) return CC_OK;
+  const bool tf32 = a->kind == CC_GEMM_TF32X3;
+  CC_CHECK_ARG(tf32 || a->kind == CC_GEMM_BF16, CC_ERR_UNSUPPORTED, "gemm kind %d", a->kind);
+  const int64_t kop = tf32 ? 3 * a->K : a->K;
+  const int esz = tf32 ? 4 : 2;
+  CC_CHECK_ARG(a->lda >= kop && a->ldb >= kop, CC_ERR_DIMENSION, "leading dimension smaller than K");
+  CC_CHECK_ARG((a->lda * esz) % 16 == 0 && (a->ldb * esz) % 16 == 0, CC_ERR_UNSUPPORTED,
+               "operand rows must be 16-byte aligned");
+  CC_CHECK_ARG(((uintptr_t)a->A % 16) == 0 && ((uintptr_t)a->B % 16) == 0, CC_ERR_UNSUPPORTED,
+               "operands must be 16-byte aligned");
+  CC_CHECK_ARG(a->N % 16 == 0, CC_ERR_UNSUPPORTED, "N=%lld must be a multiple of 16", (long long)a->N);
+  EpiParams ep{};
+  ep.epilogue = a->epilogue;
+  ep.M = a->M;
+  ep.N = a->N;
+  ep.bias = a->bias;
+  ep.C = a->C;
+  ep.ldc = a->ldc;
+  ep.c_mode = a->c_mode;
+  ep.act = a->act;
+  ep.n_out = a->n_out;
+  ep.n_q_heads = a->n_q_heads;
+  ep.n_kv_heads = a->n_kv_heads;
+  ep.head_dim = a->head_dim;
+  ep.rope_cos = a->rope_cos;
+  ep.rope_sin = a->rope_sin;
+  ep.q_out = a->q_out;
+  ep.ldq = a->ldq;
+  ep.q_mode = a->q_mode;
+  ep.k_cache = a->k_cache;
+  ep.v_cache = a->v_cache;
+  ep.cache_dtype = a->cache_dtype;
+  ep.dst_rows = a->dst_rows;
+  ep.k_raw = a->k_raw;
+  ep.raw_rows = a->raw_rows;
+  bool wide;
+  if (a->epilogue == CC_EPI_GLU) {
+    CC_CHECK_ARG(a->glu_block == 128 && a->N % 256 == 0, CC_ERR_UNSUPPORTED,
+                 "GLU needs gate/up interleaved in blocks of 128 (N=%lld)", (long long)a->N);
+    wide = true;
+  } else if (a->epilogue == CC_EPI_QKV_ROPE) {
+    CC_CHECK_ARG(a->head_dim % 32 == 0 && a->rope_cos && a->rope_sin && a->k_cache && a->v_cache && a->q_out,
+                 CC_ERR_UNSUPPORTED, "QKV epilogue needs head_dim %% 32 == 0 and all outputs");
+    CC_CHECK_ARG(a->N == (int64_t)(a->n_q_heads + 2 * a->n_kv_heads) * a->head_dim ||
+                     a->N == (int64_t)(a->n_q_heads + a->n_kv_heads) * a->head_dim,
+                 CC_ERR_DIMENSION, "QKV width mismatch");
+    wide = a->N >= 2048;
+  } else {
+    const int64_t t256 = ((a->M + 127) / 128) * ((a->N + 255) / 256);
+    wide = t256 >= 2 * num_sms() || a->N % 128 != 0;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (tf32) return wide ? launch<256, true>(a, ep, kop, st) : launch<128, true>(a, ep, kop, st);
+  return wide ? launch<256, false>(a, ep, kop, st) : launch<128, false>(a, ep, kop, st);
+}

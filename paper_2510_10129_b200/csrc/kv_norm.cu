@@ -1,0 +1,369 @@
+// KV assembly (merge_caches), RoPE tables, embedding + RMSNorm, operand
+// conversion. HBM-bound kernels: 128-bit coalesced accesses, grids sized to
+// keep every SM busy, angles formed once per (row, pair) and reused across
+// all layers and heads.
+#include "cc_common.cuh"
+
+#include <algorithm>
+#include <mutex>
+#include <string>
+
+namespace cc {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+
+int num_sms() {
+  static int n = -1;
+  if (n < 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = kNumSMs;
+  }
+  return n;
+}
+
+constexpr int kMaxPairs = 128;  // head_dim <= 256
+struct InvFreq {
+  double v[kMaxPairs];
+};
+
+// ---------------------------------------------------------------------------
+// KV assembly: one thread owns one 16-byte vector (a run of adjacent pairs) of
+// one (row, kv head) and walks every layer, so the float64 angles are formed
+// once and reused n_layers times. Keys rotated, values copied.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<float> {
+  static constexpr int N = 4;
+};
+template <>
+struct Vec16<__nv_bfloat16> {
+  static constexpr int N = 8;
+};
+
+template <typename T>
+__device__ __forceinline__ void load_vec(const T* p, float* out);
+template <>
+__device__ __forceinline__ void load_vec<float>(const float* p, float* out) {
+  float4 v = __ldg(reinterpret_cast<const float4*>(p));
+  out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void load_vec<__nv_bfloat16>(const __nv_bfloat16* p, float* out) {
+  uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    out[2 * i] = f.x;
+    out[2 * i + 1] = f.y;
+  }
+}
+template <typename T>
+__device__ __forceinline__ void store_vec(T* p, const float* in);
+template <>
+__device__ __forceinline__ void store_vec<float>(float* p, const float* in) {
+  *reinterpret_cast<float4*>(p) = make_float4(in[0], in[1], in[2], in[3]);
+}
+template <>
+__device__ __forceinline__ void store_vec<__nv_bfloat16>(__nv_bfloat16* p, const float* in) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(in[2 * i], in[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = v;
+}
+template <typename T>
+__device__ __forceinline__ void copy_vec(const T* src, T* dst) {
+  *reinterpret_cast<uint4*>(dst) = __ldg(reinterpret_cast<const uint4*>(src));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) assemble_kernel(const cc_kv_segment* __restrict__ segs, int n_segs,
+                                                       int64_t n_dst_rows, int n_layers, int kv_heads,
+                                                       int head_dim, InvFreq inv, int64_t pos_offset,
+                                                       T* __restrict__ dst_k, T* __restrict__ dst_v,
+                                                       int64_t dst_rows_cap) {
+  constexpr int V = Vec16<T>::N;
+  const int vecs_per_row = kv_heads * head_dim / V;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / vecs_per_row;
+  if (row >= n_dst_rows) return;
+  const int vi = (int)(gid - row * vecs_per_row);
+  const int col = vi * V;               // element offset inside the row
+  const int pair0 = (col % head_dim) / 2;
+
+  // segment lookup: last segment with dst_row0 <= row (segments sorted)
+  int lo = 0, hi = n_segs - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].dst_row0 <= row) lo = mid; else hi = mid - 1;
+  }
+  const cc_kv_segment sg = segs[lo];
+  const int64_t src_row = sg.src_row0 + (row - sg.dst_row0);
+  const int row_elems = kv_heads * head_dim;
+  const T* ks = reinterpret_cast<const T*>(sg.k) + src_row * row_elems + col;
+  const T* vs = reinterpret_cast<const T*>(sg.v) + src_row * row_elems + col;
+  const int64_t src_layer = sg.src_rows * row_elems;
+  T* kd = dst_k + row * row_elems + col;
+  T* vd = dst_v + row * row_elems + col;
+  const int64_t dst_layer = dst_rows_cap * row_elems;
+
+  const double pos = (double)(row + pos_offset);
+  float c[V / 2], s[V / 2];
+#pragma unroll
+  for (int p = 0; p < V / 2; ++p) {
+    double sd, cd;
+    sincos(pos * inv.v[pair0 + p], &sd, &cd);
+    c[p] = (float)cd;
+    s[p] = (float)sd;
+  }
+  for (int l = 0; l < n_layers; ++l) {
+    float x[V], y[V];
+    load_vec<T>(ks + l * src_layer, x);
+    if (dst_v) copy_vec<T>(vs + l * src_layer, vd + l * dst_layer);
+#pragma unroll
+    for (int p = 0; p < V / 2; ++p) rope_pair(x[2 * p], x[2 * p + 1], c[p], s[p], y[2 * p], y[2 * p + 1]);
+    store_vec<T>(kd + l * dst_layer, y);
+  }
+}
+
+static bool fill_inv(InvFreq& inv, const double* host, int head_dim) {
+  if (head_dim <= 0 || head_dim % 2 || head_dim / 2 > kMaxPairs || !host) return false;
+  for (int i = 0; i < head_dim / 2; ++i) inv.v[i] = host[i];
+  return true;
+}
+
+__global__ void rope_table_kernel(const int64_t* __restrict__ pos, int64_t n, InvFreq inv, int half,
+                                  float* __restrict__ cos_out, float* __restrict__ sin_out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * half) return;
+  int64_t r = i / half;
+  int p = (int)(i - r * half);
+  double sd, cd;
+  sincos((double)pos[r] * inv.v[p], &sd, &cd);
+  cos_out[i] = (float)cd;
+  sin_out[i] = (float)sd;
+}
+
+// ---------------------------------------------------------------------------
+// Embedding gather + RMSNorm (one CTA per row). numpy order: ms = sum(x^2)/d
+// in float32, y = x / sqrt(ms + eps) * gain with IEEE division and sqrt.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  float t = (lane < nw) ? red[lane] : 0.f;
+  if (warp == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  return red[32];
+}
+
+__device__ __forceinline__ void write_x(void* x_out, int mode, int64_t row, int d, int j, float y) {
+  if (mode == CC_BF16) {
+    reinterpret_cast<__nv_bfloat16*>(x_out)[row * d + j] = __float2bfloat16_rn(y);
+  } else if (mode == CC_F32) {
+    reinterpret_cast<float*>(x_out)[row * d + j] = y;
+  } else {
+    float hi, lo, lh, ll;
+    split_tf32(y, hi, lo);
+    split_tf32(lo, lh, ll);
+    float* o = reinterpret_cast<float*>(x_out) + row * (int64_t)d * 3;
+    o[j] = hi;
+    o[d + j] = hi;
+    o[2 * d + j] = lh;
+  }
+}
+
+constexpr int kNormThreads = 256;
+constexpr int kNormMaxPer = 32;  // d <= 8192
+
+__global__ void __launch_bounds__(kNormThreads) embed_rmsnorm_kernel(
+    const int64_t* __restrict__ ids, const void* __restrict__ embed, int embed_dtype, int d,
+    float* __restrict__ h_out, const float* __restrict__ gain, float eps, void* __restrict__ x_out, int x_mode,
+    const float* __restrict__ h_in, int64_t ld_h) {
+  __shared__ float red[33];
+  const int64_t row = blockIdx.x;
+  float vals[kNormMaxPer];
+  float ss = 0.f;
+  int cnt = 0;
+  for (int j = threadIdx.x; j < d; j += kNormThreads, ++cnt) {
+    float v;
+    if (h_in) {
+      v = h_in[row * ld_h + j];
+    } else {
+      const int64_t t = ids[row];
+      v = embed_dtype == CC_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(embed)[t * d + j])
+                                 : reinterpret_cast<const float*>(embed)[t * d + j];
+      if (h_out) h_out[row * d + j] = v;
+    }
+    vals[cnt] = v;
+    ss = fmaf(v, v, ss);
+  }
+  const float tot = block_sum(ss, red);
+  const float ms = __fdiv_rn(tot, (float)d);
+  const float r = __fsqrt_rn(__fadd_rn(ms, eps));
+  cnt = 0;
+  for (int j = threadIdx.x; j < d; j += kNormThreads, ++cnt) {
+    float y = __fmul_rn(__fdiv_rn(vals[cnt], r), gain[j]);
+    write_x(x_out, x_mode, row, d, j, y);
+  }
+}
+
+__global__ void convert_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, void* __restrict__ dst,
+                               int mode, int split_weight) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * cols) return;
+  int64_t r = i / cols, c = i - r * cols;
+  float x = src[i];
+  if (mode == CC_BF16) {
+    reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(x);
+  } else if (mode == CC_F32) {
+    reinterpret_cast<float*>(dst)[i] = x;
+  } else {
+    float hi, lo, lh, ll;
+    split_tf32(x, hi, lo);
+    split_tf32(lo, lh, ll);
+    float* o = reinterpret_cast<float*>(dst) + r * cols * 3;
+    o[c] = hi;
+    o[cols + c] = split_weight ? lh : hi;
+    o[2 * cols + c] = split_weight ? hi : lh;
+  }
+}
+
+__global__ void gather_i64_kernel(const int64_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                                  int64_t* __restrict__ dst) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+}  // namespace cc
+
+using namespace cc;
+
+extern "C" {
+
+int cc_abi_version(void) { return CC_ABI_VERSION; }
+const char* cc_last_error(void) { return g_err; }
+
+int cc_device_check(int dev) {
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, dev);
+  if (e != cudaSuccess) return fail(CC_ERR_CUDA, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(CC_ERR_UNSUPPORTED, "device %d is sm_%d%d; libcacheclip_sm100 is built for sm_100a only", dev,
+                prop.major, prop.minor);
+  return CC_OK;
+}
+
+int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows, int32_t n_layers,
+                   int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
+                   int64_t pos_offset, void* dst_k, void* dst_v, int64_t dst_rows_cap, void* stream) {
+  CC_CHECK_ARG(segs_dev && n_segs > 0, CC_ERR_CONSISTENCY, "nothing to merge");
+  CC_CHECK_ARG(n_layers > 0 && kv_heads > 0, CC_ERR_DIMENSION, "bad geometry");
+  CC_CHECK_ARG(n_dst_rows <= dst_rows_cap, CC_ERR_DIMENSION, "destination capacity %lld < rows %lld",
+               (long long)dst_rows_cap, (long long)n_dst_rows);
+  InvFreq inv;
+  CC_CHECK_ARG(fill_inv(inv, inv_freq_host, head_dim), CC_ERR_DIMENSION, "rotary head_dim %d unsupported",
+               head_dim);
+  if (n_dst_rows == 0) return CC_OK;
+  const int V = dtype == CC_BF16 ? 8 : 4;
+  CC_CHECK_ARG(head_dim % V == 0, CC_ERR_UNSUPPORTED, "head_dim %d not a multiple of %d", head_dim, V);
+  CC_CHECK_ARG(dst_k && (reinterpret_cast<uintptr_t>(dst_k) | reinterpret_cast<uintptr_t>(dst_v)) % 16 == 0,
+               CC_ERR_UNSUPPORTED, "destination not 16-byte aligned");
+  const int64_t threads = n_dst_rows * (int64_t)(kv_heads * head_dim / V);
+  const int bs = 256;
+  const int64_t grid = (threads + bs - 1) / bs;
+  if (dtype == CC_BF16) {
+    assemble_kernel<__nv_bfloat16><<<grid, bs, 0, as_stream(stream)>>>(
+        segs_dev, n_segs, n_dst_rows, n_layers, kv_heads, head_dim, inv, pos_offset,
+        reinterpret_cast<__nv_bfloat16*>(dst_k), reinterpret_cast<__nv_bfloat16*>(dst_v), dst_rows_cap);
+  } else if (dtype == CC_F32) {
+    assemble_kernel<float><<<grid, bs, 0, as_stream(stream)>>>(segs_dev, n_segs, n_dst_rows, n_layers, kv_heads,
+                                                              head_dim, inv, pos_offset,
+                                                              reinterpret_cast<float*>(dst_k),
+                                                              reinterpret_cast<float*>(dst_v), dst_rows_cap);
+  } else {
+    return fail(CC_ERR_UNSUPPORTED, "cache dtype %d unsupported", dtype);
+  }
+  CC_LAUNCH_CHECK("assemble_kv");
+  return CC_OK;
+}
+
+int cc_rope_table(const int64_t* positions, int64_t n, const double* inv_freq_host, int32_t head_dim,
+                  float* cos_out, float* sin_out, void* stream) {
+  InvFreq inv;
+  CC_CHECK_ARG(fill_inv(inv, inv_freq_host, head_dim), CC_ERR_DIMENSION, "rotary head_dim %d unsupported",
+               head_dim);
+  if (n <= 0) return CC_OK;
+  const int half = head_dim / 2;
+  const int64_t total = n * half;
+  rope_table_kernel<<<(total + 255) / 256, 256, 0, as_stream(stream)>>>(positions, n, inv, half, cos_out, sin_out);
+  CC_LAUNCH_CHECK("rope_table");
+  return CC_OK;
+}
+
+int cc_embed_rmsnorm(const int64_t* ids, int64_t rows, const void* embed, int32_t embed_dtype, int64_t vocab,
+                     int32_t d, float* h_out, const float* gain, float eps, void* x_out, int32_t x_mode,
+                     void* stream) {
+  (void)vocab;
+  CC_CHECK_ARG(d > 0 && d <= kNormThreads * kNormMaxPer, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
+  if (rows <= 0) return CC_OK;
+  embed_rmsnorm_kernel<<<rows, kNormThreads, 0, as_stream(stream)>>>(ids, embed, embed_dtype, d, h_out, gain, eps,
+                                                                       x_out, x_mode, nullptr, 0);
+  CC_LAUNCH_CHECK("embed_rmsnorm");
+  return CC_OK;
+}
+
+int cc_rmsnorm(const float* h, int64_t rows, int32_t d, int64_t ld_h, const float* gain, float eps, void* x_out,
+               int32_t x_mode, void* stream) {
+  CC_CHECK_ARG(d > 0 && d <= kNormThreads * kNormMaxPer, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
+  if (rows <= 0) return CC_OK;
+  embed_rmsnorm_kernel<<<rows, kNormThreads, 0, as_stream(stream)>>>(nullptr, nullptr, 0, d, nullptr, gain, eps,
+                                                                       x_out, x_mode, h, ld_h);
+  CC_LAUNCH_CHECK("rmsnorm");
+  return CC_OK;
+}
+
+int cc_convert_matrix(const float* src, int64_t rows, int64_t cols, void* dst, int32_t dst_mode,
+                      int32_t split_weight, void* stream) {
+  const int64_t n = rows * cols;
+  if (n <= 0) return CC_OK;
+  convert_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(src, rows, cols, dst, dst_mode, split_weight);
+  CC_LAUNCH_CHECK("convert_matrix");
+  return CC_OK;
+}
+
+int cc_gather_i64(const int64_t* src, const int64_t* idx, int64_t n, int64_t* dst, void* stream) {
+  if (n <= 0) return CC_OK;
+  gather_i64_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(src, idx, n, dst);
+  CC_LAUNCH_CHECK("gather_i64");
+  return CC_OK;
+}
+
+}  // extern "C"

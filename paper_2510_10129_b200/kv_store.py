@@ -1,0 +1,273 @@
+"""Device-resident chunk and merged KV caches and the sink-deduplicating merge.
+
+Same contract as pkg/src/cacheclip/kv_store.py: chunk caches hold keys
+position-free; the merge keeps chunk 0's prefix (the shared attention sink),
+concatenates every chunk's body and rotates each surviving key once, straight
+into its global position; values pass through (kv_store.py:193-258).
+
+HBM layout: one tensor per cache, [n_layers][rows][kv_heads][head_dim]
+(bf16 for a bf16 model, fp32 for an fp32 model). A merged cache is allocated
+with spare row capacity so the query rows of extend_cache append in place.
+``.keys`` / ``.values`` return the reference's per-layer list view.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import RopeParams
+from .errors import CacheConsistencyError
+from .flops import PipelineTrace
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def host_to_device(data: np.ndarray, device) -> torch.Tensor:
+    """Small host table -> device via pinned staging (stream-ordered copy)."""
+    t = torch.from_numpy(np.ascontiguousarray(data))
+    if t.numel() == 0:
+        return torch.empty(0, dtype=t.dtype, device=device)
+    return t.pin_memory().to(device, non_blocking=True)
+
+
+def _as_layers(x, device=None) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        if x.dim() != 4:
+            raise CacheConsistencyError("cache tensor must be [layers, rows, heads, head_dim]")
+        return x
+    if isinstance(x, (list, tuple)) and x:
+        parts = [p if isinstance(p, torch.Tensor) else torch.from_numpy(np.asarray(p)) for p in x]
+        shape = tuple(parts[0].shape)
+        for p in parts:
+            if tuple(p.shape) != shape:
+                raise CacheConsistencyError(f"layer shape {tuple(p.shape)} != {shape}")
+        return torch.stack(parts).to(device if device is not None else parts[0].device)
+    raise CacheConsistencyError("cache needs matching per-layer key/value lists")
+
+
+class ChunkCache:
+    """One chunk processed against the shared prefix, keys position-free."""
+
+    KEYS_ROTATED = False
+
+    def __init__(self, keys, values, token_ids, prefix_len: int, tokenizer_id: str,
+                 model_fingerprint: str) -> None:
+        k = _as_layers(keys)
+        v = _as_layers(values, k.device)
+        if k.shape != v.shape:
+            raise CacheConsistencyError(f"layer shape {tuple(v.shape)} != {tuple(k.shape)}")
+        if k.dtype not in (torch.float32, torch.bfloat16) or v.dtype != k.dtype:
+            raise CacheConsistencyError(f"cache tensors must be float32 or bfloat16, got {k.dtype}")
+        self.k, self.v = k.contiguous(), v.contiguous()
+        self.token_ids = list(int(t) for t in token_ids)
+        self.prefix_len = int(prefix_len)
+        self.tokenizer_id = tokenizer_id
+        self.model_fingerprint = model_fingerprint
+        self._k_local = None
+        if self.k.shape[1] != len(self.token_ids):
+            raise CacheConsistencyError(f"{self.k.shape[1]} cache rows but {len(self.token_ids)} token ids")
+        if not 0 <= self.prefix_len <= self.n_rows:
+            raise CacheConsistencyError(f"prefix_len {self.prefix_len} outside 0..{self.n_rows}")
+
+    @property
+    def keys(self) -> list[torch.Tensor]:
+        return list(self.k.unbind(0))
+
+    @property
+    def values(self) -> list[torch.Tensor]:
+        return list(self.v.unbind(0))
+
+    @property
+    def n_layers(self) -> int:
+        return self.k.shape[0]
+
+    @property
+    def n_rows(self) -> int:
+        return self.k.shape[1]
+
+    @property
+    def chunk_ids(self) -> list[int]:
+        return self.token_ids[self.prefix_len:]
+
+    @property
+    def chunk_len(self) -> int:
+        return self.n_rows - self.prefix_len
+
+    def local_rotated_keys(self, rope: RopeParams) -> torch.Tensor:
+        """Keys rotated at local positions 0..n-1 (attention_banks,
+        kv_store.py:106-116), formed once and memoised: a chunk cache is
+        immutable, so the per-call re-rotation of the reference is redundant."""
+        if self._k_local is None:
+            out = torch.empty_like(self.k)
+            segs = host_to_device(_segments([(self, 0, 0, self.n_rows)]), self.k.device)
+            inv = rope.inv_freq
+            _lib.call("cc_assemble_kv", segs.data_ptr(), 1, self.n_rows, self.n_layers, self.k.shape[2],
+                      self.k.shape[3], _dtype_code(self.k.dtype), inv.ctypes.data, 0,
+                      out.data_ptr(), None, self.n_rows, _stream())
+            self._k_local = out
+        return self._k_local
+
+    def attention_banks(self, rope: RopeParams, trace: PipelineTrace | None = None, stage: str = "decode"):
+        k = self.local_rotated_keys(rope)
+        return list(zip(k.unbind(0), self.v.unbind(0)))
+
+
+def _dtype_code(dt: torch.dtype) -> int:
+    return _lib.CC_BF16 if dt == torch.bfloat16 else _lib.CC_F32
+
+
+def _segments(spec) -> np.ndarray:
+    """[(chunk, src_row0, dst_row0, n_rows)] -> packed cc_kv_segment bytes."""
+    arr = (_lib.KvSegment * len(spec))()
+    for i, (c, s0, d0, n) in enumerate(spec):
+        arr[i] = _lib.KvSegment(c.k.data_ptr(), c.v.data_ptr(), c.n_rows, s0, d0, n)
+    return np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+
+
+@dataclass(frozen=True)
+class MergeLayout:
+    sink_len: int
+    chunk_lens: tuple[int, ...]
+
+    @property
+    def total(self) -> int:
+        return self.sink_len + sum(self.chunk_lens)
+
+    def chunk_start(self, chunk: int) -> int:
+        return self.sink_len + sum(self.chunk_lens[:chunk])
+
+
+class MergedCache:
+    """Concatenated chunk rows at contiguous positions, keys rotated.
+
+    ``source`` is (chunk, row) per merged row, (-1, i) for appended rows;
+    ``recomputed_rows`` is the selective-recompute provenance (kv_store.py:133-183).
+    """
+
+    KEYS_ROTATED = True
+
+    def __init__(self, k_store: torch.Tensor, v_store: torch.Tensor, n_rows: int, token_ids, layout: MergeLayout,
+                 source, tokenizer_id: str, model_fingerprint: str, recomputed_rows=()) -> None:
+        self.k_store, self.v_store = k_store, v_store
+        self._n_rows = int(n_rows)
+        self.token_ids = list(token_ids)
+        self.layout = layout
+        self.source = list(source)
+        self.tokenizer_id = tokenizer_id
+        self.model_fingerprint = model_fingerprint
+        self.recomputed_rows = tuple(recomputed_rows)
+        if self._n_rows != len(self.token_ids) or self._n_rows != len(self.source):
+            raise CacheConsistencyError("rows, token ids, and source map disagree")
+
+    @property
+    def n_rows(self) -> int:
+        return self._n_rows
+
+    @property
+    def capacity(self) -> int:
+        return self.k_store.shape[1]
+
+    @property
+    def keys(self) -> list[torch.Tensor]:
+        return list(self.k_store[:, : self._n_rows].unbind(0))
+
+    @property
+    def values(self) -> list[torch.Tensor]:
+        return list(self.v_store[:, : self._n_rows].unbind(0))
+
+    @property
+    def positions(self) -> np.ndarray:
+        return np.arange(self._n_rows, dtype=np.int64)
+
+    def attention_banks(self, rope=None, trace=None, stage="decode"):
+        return list(zip(self.keys, self.values))
+
+    def ensure_capacity(self, rows: int) -> None:
+        """Grow the row capacity (copy) so `rows` rows fit in place."""
+        if rows <= self.capacity:
+            return
+        L, _, H, D = self.k_store.shape
+        cap = max(rows, int(self.capacity * 1.25) + 64)
+        for name in ("k_store", "v_store"):
+            old = getattr(self, name)
+            new = torch.empty(L, cap, H, D, dtype=old.dtype, device=old.device)
+            new[:, : self._n_rows].copy_(old[:, : self._n_rows])
+            setattr(self, name, new)
+
+    def _append_rows(self, token_ids) -> None:
+        base = self._n_rows
+        self.token_ids.extend(int(t) for t in token_ids)
+        self.source.extend((-1, base + i) for i in range(len(token_ids)))
+        self._n_rows += len(token_ids)
+
+    def copy(self) -> "MergedCache":
+        return MergedCache(self.k_store.clone(), self.v_store.clone(), self._n_rows, self.token_ids,
+                           self.layout, self.source, self.tokenizer_id, self.model_fingerprint,
+                           self.recomputed_rows)
+
+
+def compute_positions(chunk_lens: Sequence[int], prefix_len: int) -> np.ndarray:
+    if prefix_len < 0 or any(c < 0 for c in chunk_lens):
+        raise ValueError("lengths must be non-negative")
+    return np.arange(prefix_len + sum(chunk_lens), dtype=np.int64)
+
+
+def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: PipelineTrace | None = None,
+                 *, capacity: int | None = None) -> MergedCache:
+    """Concatenate chunk caches keeping only the first copy of the prefix and
+    rotate keys to global positions in one HBM pass (kv_store.py:193-258).
+    ``capacity`` reserves rows for in-place appends (query rows)."""
+    if not chunks:
+        raise CacheConsistencyError("nothing to merge")
+    first = chunks[0]
+    sink = first.prefix_len
+    prefix_ids = first.token_ids[:sink]
+    geom = tuple(first.k.shape[2:])
+    for i, c in enumerate(chunks):
+        if c.prefix_len != sink:
+            raise CacheConsistencyError(f"chunk {i} prefix_len {c.prefix_len} != {sink}")
+        if c.token_ids[:sink] != prefix_ids:
+            raise CacheConsistencyError(f"chunk {i} has different prefix tokens")
+        if c.model_fingerprint != first.model_fingerprint:
+            raise CacheConsistencyError(f"chunk {i} built with a different model")
+        if c.tokenizer_id != first.tokenizer_id:
+            raise CacheConsistencyError(f"chunk {i} built with a different tokenizer")
+        if c.n_layers != first.n_layers or tuple(c.k.shape[2:]) != geom or c.k.dtype != first.k.dtype \
+                or c.k.device != first.k.device:
+            raise CacheConsistencyError(f"chunk {i} has mismatched tensor geometry")
+    lens = tuple(c.chunk_len for c in chunks)
+    total = sink + sum(lens)
+    cap = max(total, capacity or 0)
+    token_ids = list(prefix_ids)
+    source: list[tuple[int, int]] = [(0, r) for r in range(sink)]
+    spec = []
+    dst = 0
+    for ci, c in enumerate(chunks):
+        token_ids.extend(c.chunk_ids)
+        source.extend((ci, sink + j) for j in range(c.chunk_len))
+        s0 = 0 if ci == 0 else sink
+        n = c.n_rows - s0
+        if n:
+            spec.append((c, s0, dst, n))
+        dst += n
+    L, H, D = first.n_layers, geom[0], geom[1]
+    k_store = torch.empty(L, cap, H, D, dtype=first.k.dtype, device=first.k.device)
+    v_store = torch.empty_like(k_store)
+    if total:
+        segs = host_to_device(_segments(spec), first.k.device)
+        inv = rope.inv_freq
+        _lib.call("cc_assemble_kv", segs.data_ptr(), len(spec), total, L, H, D, _dtype_code(first.k.dtype),
+                  inv.ctypes.data, 0, k_store.data_ptr(), v_store.data_ptr(), cap, _stream())
+    if trace is not None:
+        for _ in range(L):
+            trace.rope("merge_overhead", total * H, D)
+    return MergedCache(k_store, v_store, total, token_ids, MergeLayout(sink, lens), source,
+                       first.tokenizer_id, first.model_fingerprint)

@@ -1,0 +1,271 @@
+"""Token-importance scoring and recompute-set selection on the device
+(pkg/src/cacheclip/selector.py).
+
+aux_score_tokens runs the scoring model (fp32, 3xTF32 GEMMs) for every chunk
+in ONE batched pass: each chunk is a sequence whose bank is its cached rows at
+local positions and whose new rows are the query (model.py:568-607); the last
+layer stops at the attention weights over chunk columns, reduced in the
+reference's order into per-token scores (selector.py:157-179).
+
+select_tokens runs budget -> exact stable top-k -> per-chunk window rule in a
+single-CTA kernel; one host read brings back the selection.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import asdict, dataclass
+from fractions import Fraction
+from typing import Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from .flops import PipelineTrace, trace_layer
+from .kv_store import ChunkCache, host_to_device
+from .runtime import ScoreSpec, bank_tables, forward_banked
+from .tokenizers import TokenSpan, align_spans
+from .weights import Model
+
+
+@dataclass(frozen=True)
+class SelectionConfig:
+    recomp_ratio: float
+    window_len: int = 8
+    window_threshold: int = 5
+    expand_full_window: bool = False
+
+    def __post_init__(self) -> None:
+        if not 0.0 <= self.recomp_ratio <= 1.0:
+            raise ValueError(f"recomp_ratio must be in [0, 1], got {self.recomp_ratio}")
+        if self.window_len < 1:
+            raise ValueError(f"window_len must be >= 1, got {self.window_len}")
+        if not 0 <= self.window_threshold <= self.window_len:
+            raise ValueError(f"window_threshold must be in 0..window_len, got {self.window_threshold}")
+
+
+class ImportanceScores:
+    """Concatenated per-token scores (device fp32) with their chunk lengths."""
+
+    def __init__(self, scores, chunk_lens) -> None:
+        if isinstance(scores, torch.Tensor):
+            self.device_scores = scores.float().contiguous()
+        else:
+            arr = np.asarray(scores, dtype=np.float32)
+            if arr.ndim != 1:
+                raise ValueError("scores must be 1-D")
+            self.device_scores = torch.from_numpy(arr.copy())
+        self.chunk_lens = tuple(int(c) for c in chunk_lens)
+        if self.device_scores.dim() != 1 or self.device_scores.numel() != sum(self.chunk_lens):
+            raise ValueError(f"{self.device_scores.numel()} scores for chunk lengths {self.chunk_lens}")
+
+    @property
+    def scores(self) -> np.ndarray:
+        return self.device_scores.detach().cpu().numpy()
+
+
+@dataclass(frozen=True)
+class WindowRecord:
+    window_id: int
+    chunk: int
+    start: int
+    end: int
+    selected: int
+    kept: bool
+    partial: bool
+
+
+@dataclass(frozen=True)
+class AuxSelection:
+    indices: tuple[int, ...]
+    windows: tuple[WindowRecord, ...]
+    n_tokens: int
+    requested_ratio: float
+
+    @property
+    def effective_ratio(self) -> float:
+        return len(self.indices) / self.n_tokens if self.n_tokens else 0.0
+
+
+@dataclass(frozen=True)
+class SelectionPlan:
+    indices: tuple[int, ...]
+    windows: tuple[WindowRecord, ...]
+    requested_ratio: float
+    effective_ratio: float
+
+    def to_json_dict(self) -> dict:
+        return {"indices": list(self.indices), "windows": [asdict(w) for w in self.windows],
+                "requested_ratio": self.requested_ratio, "effective_ratio": self.effective_ratio}
+
+    @classmethod
+    def from_json_dict(cls, data: dict) -> "SelectionPlan":
+        return cls(tuple(int(i) for i in data["indices"]), tuple(WindowRecord(**w) for w in data["windows"]),
+                   float(data["requested_ratio"]), float(data["effective_ratio"]))
+
+
+def selection_budget(ratio: float, n_tokens: int) -> int:
+    """ceil(ratio * n) on the ratio's decimal rendering (selector.py:113-123)."""
+    if n_tokens < 0:
+        raise ValueError("token count must be non-negative")
+    return max(0, min(n_tokens, math.ceil(Fraction(str(float(ratio))) * n_tokens)))
+
+
+# ---------------------------------------------------------------------------
+def _device_of(t: torch.Tensor) -> torch.device:
+    return t.device if t.is_cuda else torch.device("cuda")
+
+
+def _run_select(scores: torch.Tensor, chunk_lens: Sequence[int], budget: int, window_len: int, threshold: int,
+                expand: bool, index_offset: int = 0):
+    """Launch the top-k/window kernel; returns device (indices, count, win_sel, win_kept)."""
+    dev = _device_of(scores)
+    s = scores.to(dev, dtype=torch.float32).contiguous()
+    n = s.numel()
+    lens = np.asarray(chunk_lens, dtype=np.int64)
+    n_win = int(sum(-(-int(c) // window_len) for c in lens))
+    lib = _lib.load()
+    ws_bytes = int(lib.cc_select_workspace_bytes(n, len(lens)))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    out_idx = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+    out_cnt = torch.empty(1, dtype=torch.int64, device=dev)
+    win_sel = torch.empty(max(n_win, 1), dtype=torch.int32, device=dev)
+    win_kept = torch.empty(max(n_win, 1), dtype=torch.int32, device=dev)
+    lens_dev = host_to_device(lens, dev)
+    _lib.call("cc_select_topk_windows", s.data_ptr(), n, lens_dev.data_ptr(), len(lens), n_win, budget,
+              window_len, threshold, int(expand), index_offset, out_idx.data_ptr(), out_cnt.data_ptr(),
+              win_sel.data_ptr(), win_kept.data_ptr(), ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    return out_idx, out_cnt, win_sel[:n_win], win_kept[:n_win]
+
+
+def top_candidates(scores, budget: int) -> np.ndarray:
+    """Indices of the `budget` highest scores, lower index first on ties,
+    returned ascending (selector.py:126-129) — the window kernel with 1-token
+    windows and threshold 1 keeps exactly the candidates."""
+    t = scores if isinstance(scores, torch.Tensor) else torch.from_numpy(np.asarray(scores, np.float32).copy())
+    n = t.numel()
+    budget = max(0, min(int(budget), n))
+    if n == 0:
+        return np.zeros(0, dtype=np.int64)
+    idx, cnt, _, _ = _run_select(t, [n], budget, 1, 1, False)
+    k = int(cnt.item())
+    return idx[:k].cpu().numpy()
+
+
+def select_tokens(scores: ImportanceScores, config: SelectionConfig) -> AuxSelection:
+    """Budgeted top-k filtered by the window rule, aux-token space (selector.py:182-214)."""
+    sel, _ = select_tokens_device(scores, config)
+    return sel
+
+
+def select_tokens_device(scores: ImportanceScores, config: SelectionConfig, index_offset: int = 0):
+    """select_tokens plus the device copy of the (offset) indices for the
+    recompute launch. The only host sync of the pipeline: count, indices and
+    window flags come back in one D2H copy."""
+    n = int(scores.device_scores.numel())
+    budget = selection_budget(config.recomp_ratio, n)
+    idx, cnt, wsel, wkept = _run_select(scores.device_scores, scores.chunk_lens, budget, config.window_len,
+                                        config.window_threshold, config.expand_full_window, index_offset)
+    n_win = wsel.numel()
+    # one D2H read: count | window counts | kept flags | indices
+    flags = torch.cat([cnt, wsel.long(), wkept.long(), idx]).cpu().numpy()
+    k = int(flags[0])
+    wsel_h, wkept_h = flags[1:1 + n_win], flags[1 + n_win:1 + 2 * n_win]
+    idx_h = flags[1 + 2 * n_win:1 + 2 * n_win + k].astype(np.int64)
+    windows = []
+    wid, base = 0, 0
+    for ci, clen in enumerate(scores.chunk_lens):
+        for ws in range(0, clen, config.window_len):
+            we = min(ws + config.window_len, clen)
+            windows.append(WindowRecord(wid, ci, base + ws, base + we, int(wsel_h[wid]), bool(wkept_h[wid]),
+                                        (we - ws) < config.window_len))
+            wid += 1
+        base += clen
+    aux_idx = tuple(int(i) - index_offset for i in idx_h)
+    sel = AuxSelection(aux_idx, tuple(windows), n, config.recomp_ratio)
+    return sel, (idx[:k], idx_h)
+
+
+def map_selection(aux_selection: AuxSelection, aux_spans: Sequence[TokenSpan], primary_spans: Sequence[TokenSpan],
+                  *, index_offset: int = 0) -> SelectionPlan:
+    """Project aux-space selection onto primary tokens (selector.py:217-245)."""
+    if len(aux_spans) != aux_selection.n_tokens:
+        raise ValueError(f"{len(aux_spans)} aux spans for a selection over {aux_selection.n_tokens} tokens")
+    if _same_spans(aux_spans, primary_spans):
+        primary = list(aux_selection.indices)
+    else:
+        primary = align_spans(aux_spans, primary_spans).project(aux_selection.indices)
+    return SelectionPlan(tuple(p + index_offset for p in primary), aux_selection.windows,
+                         aux_selection.requested_ratio,
+                         len(primary) / len(primary_spans) if primary_spans else 0.0)
+
+
+def _same_spans(a, b) -> bool:
+    if a is b:
+        return True
+    if len(a) != len(b):
+        return False
+    return all(x.start == y.start and x.end == y.end for x, y in zip(a, b))
+
+
+# ---------------------------------------------------------------------------
+def aux_score_tokens(aux_model: Model, aux_chunk_caches: Sequence[ChunkCache], query_ids: Sequence[int], *,
+                     trace: PipelineTrace | None = None, workers: int = 1) -> ImportanceScores:
+    """Score chunk tokens by last-layer query attention (selector.py:132-179).
+
+    All chunks run as one batch of sequences; ``workers`` is accepted for
+    signature parity (the result is invariant to it, as in the reference)."""
+    if not aux_chunk_caches:
+        raise ValueError("no chunk caches to score")
+    if not query_ids:
+        raise ValueError("query must be non-empty")
+    for i, cache in enumerate(aux_chunk_caches):
+        if cache.model_fingerprint != aux_model.fingerprint:
+            raise ValueError(f"aux chunk {i} was built by a different model")
+    c = aux_model.config
+    if c.dtype != "fp32":
+        raise ValueError("the scoring model must run in fp32 mode (exact selection)")
+    q = np.asarray(list(query_ids), dtype=np.int64)
+    if q.min() < 0 or q.max() >= c.vocab_size:
+        raise ValueError(f"token id outside vocab of size {c.vocab_size}")
+    dev = aux_model.device
+    S, Q = len(aux_chunk_caches), q.size
+    n_rows = np.array([ch.n_rows for ch in aux_chunk_caches], dtype=np.int64)
+    prefix = aux_chunk_caches[0].prefix_len
+    chunk_lens = n_rows - np.array([ch.prefix_len for ch in aux_chunk_caches], dtype=np.int64)
+    if any(ch.prefix_len != prefix for ch in aux_chunk_caches):
+        # columns start at each chunk's own prefix_len; the kernel uses one col0
+        raise ValueError("aux chunks must share one prefix length")
+    ids = np.tile(q, S)
+    pos = (n_rows[:, None] + np.arange(Q, dtype=np.int64)[None, :]).reshape(-1)
+    col_off = np.concatenate([[0], np.cumsum(chunk_lens)[:-1]]).astype(np.int64)
+    host = np.concatenate([ids, pos, chunk_lens, col_off])
+    buf = host_to_device(host, dev)
+    R = S * Q
+    ids_d, pos_d = buf[:R], buf[R:2 * R]
+    lens_d, off_d = buf[2 * R:2 * R + S], buf[2 * R + S:]
+    seqs = [(ch.local_rotated_keys(c.rope), ch.v, ch.n_rows, si * Q, Q) for si, ch in enumerate(aux_chunk_caches)]
+    tables = bank_tables(c.n_layers, seqs, dev)
+    scores = torch.empty(int(chunk_lens.sum()), dtype=torch.float32, device=dev)
+    spec = ScoreSpec(prefix, lens_d, off_d, int(chunk_lens.max()), scores)
+    forward_banked(aux_model, ids_d, pos_d, tables, S, Q, int(n_rows.max()), score=spec)
+    if trace is not None:
+        for ch in aux_chunk_caches:
+            for _ in range(c.n_layers):
+                trace.rope("selection", ch.n_rows * c.kv_heads, c.d_head)
+            for _ in range(c.n_layers):
+                trace_layer(trace, c, "selection", Q, Q * ch.n_rows + Q * (Q + 1) // 2)
+            trace.matmul("selection", 1, c.d_model, c.vocab_size)
+    return ImportanceScores(scores, tuple(int(x) for x in chunk_lens))
+
+
+def random_select(n_tokens: int, ratio: float, seed: int, *, index_offset: int = 0) -> SelectionPlan:
+    """Seeded uniform sample without replacement; ablation control (selector.py:294-312)."""
+    if n_tokens < 0:
+        raise ValueError("token count must be non-negative")
+    budget = selection_budget(ratio, n_tokens)
+    rng = np.random.default_rng(seed)
+    chosen = np.sort(rng.choice(n_tokens, size=budget, replace=False))
+    return SelectionPlan(tuple(int(i) + index_offset for i in chosen), (), float(ratio),
+                         budget / n_tokens if n_tokens else 0.0)

@@ -1,0 +1,294 @@
+"""Kernel-level checks of libcacheclip_sm100.so on a B200, each against a
+plain torch / numpy reference of the same op (float64 where it matters)."""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cacheclip_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    from paper_2510_10129_b200 import _lib as L
+    L.load()
+    L.require_device(0)
+    return L
+
+
+def _gemm(kind, epi, A, B, **kw):
+    from paper_2510_10129_b200 import runtime
+    M, N = A.shape[0], B.shape[0]
+    K = B.shape[1] // (3 if kind == 1 else 1)
+    runtime.gemm(kind, epi, M, N, K, A, B, **kw)
+    torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 128, 64), (200, 256, 320), (1000, 4608, 512), (300, 1152, 896),
+                                   (4096, 4096, 1024)])
+def test_gemm_bf16_store(M, N, K):
+    from paper_2510_10129_b200 import _lib as L
+    g = torch.Generator(device=DEV).manual_seed(M + N + K)
+    A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    B = torch.randn(N, K, device=DEV, generator=g).to(torch.bfloat16)
+    bias = torch.randn(N, device=DEV, generator=g)
+    C = torch.empty(M, N, device=DEV, dtype=torch.float32)
+    _gemm(L.CC_GEMM_BF16, L.CC_EPI_STORE, A, B, bias=bias, C=C, ldc=N, c_mode=L.CC_F32)
+    ref = A.double() @ B.double().t() + bias.double()
+    err = (C.double() - ref).abs().max().item()
+    assert err < 1e-3 * math.sqrt(K), err
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 128, 128), (2048, 1152, 896), (33, 4864 * 2 // 2, 896)])
+def test_gemm_tf32x3_is_fp32_faithful(M, N, K):
+    from paper_2510_10129_b200 import _lib as L
+    g = torch.Generator(device=DEV).manual_seed(7 + M)
+    a = torch.randn(M, K, device=DEV, generator=g)
+    b = torch.randn(N, K, device=DEV, generator=g)
+    A = torch.empty(M, 3 * K, device=DEV)
+    B = torch.empty(N, 3 * K, device=DEV)
+    s = torch.cuda.current_stream().cuda_stream
+    L.call("cc_convert_matrix", a.data_ptr(), M, K, A.data_ptr(), L.CC_F32_SPLIT3, 0, s)
+    L.call("cc_convert_matrix", b.data_ptr(), N, K, B.data_ptr(), L.CC_F32_SPLIT3, 1, s)
+    C = torch.empty(M, N, device=DEV)
+    _gemm(L.CC_GEMM_TF32X3, L.CC_EPI_STORE, A, B, C=C, ldc=N, c_mode=L.CC_F32)
+    ref = a.double() @ b.double().t()
+    # fp32 sgemm-level error: |err| <~ K * 2^-24 * |a||b| scale; demand < 4e-6 relative to sqrt(K)
+    err = ((C.double() - ref).abs() / math.sqrt(K)).max().item()
+    assert err < 4e-6, err
+    fp32 = (a @ b.t()).double()
+    err32 = ((fp32 - ref).abs() / math.sqrt(K)).max().item()
+    assert err < 4 * max(err32, 1e-7), (err, err32)
+
+
+def test_gemm_residual_and_glu():
+    from paper_2510_10129_b200 import _lib as L
+    from paper_2510_10129_b200.weights import _interleave_glu, _interleave_bias
+    g = torch.Generator(device=DEV).manual_seed(3)
+    M, K, FF = 300, 256, 384
+    x = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    wg = torch.randn(FF, K, device=DEV, generator=g) * 0.05
+    wu = torch.randn(FF, K, device=DEV, generator=g) * 0.05
+    bg = torch.randn(FF, device=DEV, generator=g) * 0.1
+    bu = torch.randn(FF, device=DEV, generator=g) * 0.1
+    W = _interleave_glu(wg, wu).to(torch.bfloat16)
+    b = _interleave_bias(bg, bu)
+    out = torch.empty(M, FF, device=DEV, dtype=torch.float32)
+    _gemm(L.CC_GEMM_BF16, L.CC_EPI_GLU, x, W, bias=b, C=out, ldc=FF, c_mode=L.CC_F32, act=L.CC_ACT_SILU, n_out=FF)
+    xd = x.double()
+    gate = xd @ wg.to(torch.bfloat16).double().t() + bg.double()
+    up = xd @ wu.to(torch.bfloat16).double().t() + bu.double()
+    ref = gate / (1 + torch.exp(-gate)) * up
+    assert (out.double() - ref).abs().max().item() < 2e-3
+    # residual: h += x @ W^T
+    Wr = (torch.randn(K, K, device=DEV, generator=g) * 0.05).to(torch.bfloat16)
+    h = torch.randn(M, K, device=DEV, generator=g)
+    h0 = h.clone()
+    _gemm(L.CC_GEMM_BF16, L.CC_EPI_RESIDUAL, x, Wr, C=h, ldc=K, c_mode=L.CC_F32)
+    ref = h0.double() + xd @ Wr.double().t()
+    assert (h.double() - ref).abs().max().item() < 2e-3
+
+
+def test_gemm_qkv_rope_scatter():
+    from paper_2510_10129_b200 import _lib as L
+    from paper_2510_10129_b200.config import RopeParams
+    from paper_2510_10129_b200.runtime import gemm
+    g = torch.Generator(device=DEV).manual_seed(5)
+    M, d, Hq, Hkv, dh = 77, 256, 4, 2, 64
+    N = (Hq + 2 * Hkv) * dh
+    x = torch.randn(M, d, device=DEV, generator=g).to(torch.bfloat16)
+    W = (torch.randn(N, d, device=DEV, generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(N, device=DEV, generator=g) * 0.1
+    rows = np.sort(np.random.default_rng(0).choice(1000, M, replace=False)).astype(np.int64)
+    pos = torch.from_numpy(rows).to(DEV)
+    rope = RopeParams(dh, 1e6)
+    cos, sin = rope.angles(rows)
+    cos_t, sin_t = torch.from_numpy(cos).to(DEV), torch.from_numpy(sin).to(DEV)
+    q = torch.empty(M, Hq * dh, device=DEV, dtype=torch.bfloat16)
+    kc = torch.zeros(1000, Hkv, dh, device=DEV, dtype=torch.bfloat16)
+    vc = torch.zeros_like(kc)
+    kraw = torch.zeros(M, Hkv, dh, device=DEV, dtype=torch.bfloat16)
+    gemm(L.CC_GEMM_BF16, L.CC_EPI_QKV_ROPE, M, N, d, x, W, bias=bias, rope=(cos_t, sin_t), q_out=q, ldq=Hq * dh,
+         k_cache=kc, v_cache=vc, dst_rows=pos, k_raw=kraw, heads=(Hq, Hkv, dh))
+    torch.cuda.synchronize()
+    y = (x.float() @ W.float().t() + bias).cpu().numpy()
+    qr = y[:, : Hq * dh].reshape(M, Hq, dh)
+    kr = y[:, Hq * dh:(Hq + Hkv) * dh].reshape(M, Hkv, dh)
+    vr = y[:, (Hq + Hkv) * dh:].reshape(M, Hkv, dh)
+    q_ref = orc.rope_rotate(qr, rows, dh, 1e6)
+    k_ref = orc.rope_rotate(kr, rows, dh, 1e6)
+    tol = 3e-2
+    np.testing.assert_allclose(q.float().cpu().numpy().reshape(M, Hq, dh), q_ref, atol=tol, rtol=1e-2)
+    np.testing.assert_allclose(kc[pos].float().cpu().numpy(), k_ref, atol=tol, rtol=1e-2)
+    np.testing.assert_allclose(vc[pos].float().cpu().numpy(), vr, atol=tol, rtol=1e-2)
+    np.testing.assert_allclose(kraw.float().cpu().numpy(), kr, atol=tol, rtol=1e-2)
+    untouched = np.setdiff1d(np.arange(1000), rows)
+    assert kc[torch.from_numpy(untouched).to(DEV)].abs().max().item() == 0.0
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_assemble_bitwise_rope(dtype):
+    """merge_caches rotation vs the oracle: bitwise in fp32 (tensor_core.py:83-84
+    separately rounded products, float64 angles), bitwise after bf16 rounding."""
+    from paper_2510_10129_b200 import ChunkCache, RopeParams, merge_caches
+    rng = np.random.default_rng(11)
+    L_, H, D, P = 3, 2, 128, 7
+    prefix = list(range(P))
+    base = 1e6
+    chunks, o_chunks = [], []
+    shared_k = rng.standard_normal((L_, P, H, D)).astype(np.float32)
+    shared_v = rng.standard_normal((L_, P, H, D)).astype(np.float32)
+    for i, n in enumerate((33, 1, 250, 64)):
+        k = rng.standard_normal((L_, P + n, H, D)).astype(np.float32) * 3
+        v = rng.standard_normal((L_, P + n, H, D)).astype(np.float32)
+        k[:, :P], v[:, :P] = shared_k, shared_v
+        if dtype == torch.bfloat16:
+            k, v = orc.round_to_bf16(k), orc.round_to_bf16(v)
+        ids = prefix + list(range(100 + 1000 * i, 100 + 1000 * i + n))
+        chunks.append(ChunkCache(torch.from_numpy(k).to(DEV, dtype), torch.from_numpy(v).to(DEV, dtype), ids, P,
+                                 "t", "m"))
+        o_chunks.append(orc.Chunk([k[l] for l in range(L_)], [v[l] for l in range(L_)], ids, P))
+    merged = merge_caches(chunks, RopeParams(D, base), capacity=500)
+    ref = orc.merge(o_chunks, D, base)
+    assert merged.token_ids == ref.token_ids and merged.source == ref.source
+    assert merged.layout.sink_len == P and merged.layout.chunk_lens == ref.chunk_lens
+    for l in range(L_):
+        got_k = merged.keys[l].float().cpu().numpy()
+        want_k = ref.keys[l] if dtype == torch.float32 else orc.round_to_bf16(ref.keys[l])
+        np.testing.assert_array_equal(got_k, want_k)
+        np.testing.assert_array_equal(merged.values[l].float().cpu().numpy(), ref.values[l])
+
+
+def _attn_ref(q, k, v, limits, factor):
+    """fp64 masked attention; q [m, Hq, D], k/v [n, Hkv, D]."""
+    m, Hq, D = q.shape
+    G = Hq // k.shape[1]
+    kk = k.double().repeat_interleave(G, dim=1)
+    vv = v.double().repeat_interleave(G, dim=1)
+    s = torch.einsum("mhd,nhd->hmn", q.double(), kk) * factor
+    n = k.shape[0]
+    mask = torch.arange(n, device=q.device)[None, :] >= limits[:, None]
+    s = s.masked_fill(mask[None], float("-inf"))
+    w = torch.softmax(s, dim=-1)
+    return torch.einsum("hmn,nhd->mhd", w, vv)
+
+
+@pytest.mark.parametrize("D,Hq,Hkv,m,n", [(128, 28, 4, 300, 2000), (64, 4, 2, 100, 1040), (128, 8, 8, 5, 70)])
+def test_sparse_row_attention(D, Hq, Hkv, m, n):
+    from paper_2510_10129_b200 import _lib as L
+    g = torch.Generator(device=DEV).manual_seed(D + m)
+    q = torch.randn(m, Hq, D, device=DEV, generator=g).to(torch.bfloat16)
+    k = torch.randn(n, Hkv, D, device=DEV, generator=g).to(torch.bfloat16)
+    v = torch.randn(n, Hkv, D, device=DEV, generator=g).to(torch.bfloat16)
+    pos = torch.sort(torch.randperm(n, generator=torch.Generator().manual_seed(1))[:m]).values.to(DEV)
+    out = torch.empty(m, Hq * D, device=DEV, dtype=torch.bfloat16)
+    factor = 1.0 / math.sqrt(D)
+    L.call("cc_sparse_row_attention", q.data_ptr(), Hq * D, pos.data_ptr(), m, k.data_ptr(), v.data_ptr(), n, Hq,
+           Hkv, D, factor, None, out.data_ptr(), Hq * D, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = _attn_ref(q, k, v, pos + 1, factor)
+    err = (out.double().view(m, Hq, D) - ref).abs().max().item()
+    assert err < 2e-2, err
+
+
+def test_banked_attention_f32_matches_reference_math():
+    from paper_2510_10129_b200 import _lib as L
+    from paper_2510_10129_b200.runtime import bank_tables
+    rng = np.random.default_rng(2)
+    Hq, Hkv, D, Q = 4, 2, 64, 8
+    banks = [rng.standard_normal((1, nb, Hkv, D)).astype(np.float32) for nb in (40, 3, 100)]
+    vbanks = [rng.standard_normal((1, nb, Hkv, D)).astype(np.float32) for nb in (40, 3, 100)]
+    S = len(banks)
+    q = rng.standard_normal((S * Q, Hq * D)).astype(np.float32)
+    kn = rng.standard_normal((S * Q, Hkv * D)).astype(np.float32)
+    vn = rng.standard_normal((S * Q, Hkv * D)).astype(np.float32)
+    tk = [torch.from_numpy(b).to(DEV) for b in banks]
+    tv = [torch.from_numpy(b).to(DEV) for b in vbanks]
+    tables = bank_tables(1, [(tk[s], tv[s], banks[s].shape[1], s * Q, Q) for s in range(S)], DEV)
+    qd, kd, vd = (torch.from_numpy(a).to(DEV) for a in (q, kn, vn))
+    out = torch.empty(S * Q, Hq * D, device=DEV)
+    factor = float(np.float32(1 / math.sqrt(D)))
+    maxb = max(b.shape[1] for b in banks)
+    L.call("cc_banked_attention_f32", tables[0].data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
+           vd.data_ptr(), Hq, Hkv, D, factor, out.data_ptr(), L.CC_F32, None, 0, 0,
+           torch.cuda.current_stream().cuda_stream)
+    w = torch.zeros(S, Hq, Q, maxb, device=DEV)
+    L.call("cc_banked_attention_f32", tables[0].data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
+           vd.data_ptr(), Hq, Hkv, D, factor, out.data_ptr(), L.CC_F32, w.data_ptr(), 0, maxb,
+           torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    wg = w.cpu().numpy()
+    for s in range(S):
+        nb = banks[s].shape[1]
+        bank_k = np.concatenate([banks[s][0], kn[s * Q:(s + 1) * Q].reshape(Q, Hkv, D)])
+        bank_v = np.concatenate([vbanks[s][0], vn[s * Q:(s + 1) * Q].reshape(Q, Hkv, D)])
+        qq = q[s * Q:(s + 1) * Q].reshape(Q, Hq, D).transpose(1, 0, 2)
+        ctx, wr = orc.attend(qq, bank_k.transpose(1, 0, 2), bank_v.transpose(1, 0, 2), nb + np.arange(Q) + 1)
+        np.testing.assert_allclose(got[s * Q:(s + 1) * Q].reshape(Q, Hq, D), ctx.transpose(1, 0, 2),
+                                   rtol=2e-5, atol=2e-6)
+        np.testing.assert_allclose(wg[s, :, :, :nb], wr[:, :, :nb], rtol=2e-5, atol=1e-7)
+
+
+def _sel_gpu(scores, lens, ratio, wl=8, thr=5, expand=False):
+    from paper_2510_10129_b200 import ImportanceScores, SelectionConfig, select_tokens
+    s = ImportanceScores(torch.from_numpy(np.asarray(scores, np.float32)).to(DEV), lens)
+    return select_tokens(s, SelectionConfig(ratio, wl, thr, expand))
+
+
+def test_select_kernel_matches_oracle_random_and_ties():
+    rng = np.random.default_rng(9)
+    for trial in range(30):
+        n_chunks = int(rng.integers(1, 9))
+        lens = [int(x) for x in rng.integers(1, 300, n_chunks)]
+        n = sum(lens)
+        if trial % 3 == 0:
+            s = rng.integers(0, 4, n).astype(np.float32)  # massive ties
+        elif trial % 3 == 1:
+            s = rng.random(n, dtype=np.float32)
+        else:
+            s = (rng.random(n) * 1e-3).astype(np.float32)
+            s[rng.integers(0, n, n // 4)] = 0.0
+        ratio = float(rng.choice([0.0, 0.05, 0.1, 0.2, 0.25, 0.4, 0.5, 1.0]))
+        thr = int(rng.integers(0, 9))
+        expand = bool(rng.integers(0, 2))
+        idx, wins = orc.select(s, lens, ratio, 8, thr, expand)
+        got = _sel_gpu(s, lens, ratio, 8, thr, expand)
+        assert got.indices == idx, (trial, ratio, thr)
+        assert [(w.window_id, w.chunk, w.start, w.end, w.selected, w.kept, w.partial) for w in got.windows] == \
+               [(w.window_id, w.chunk, w.start, w.end, w.selected, w.kept, w.partial) for w in wins]
+
+
+def test_select_kats():
+    got = _sel_gpu([10, 9, 8, 7, 6, 5, 0, 0, 4, 3, 0, 0, 0, 0, 0, 0], [16], 0.5)
+    assert got.indices == (0, 1, 2, 3, 4, 5)
+    from paper_2510_10129_b200 import top_candidates
+    np.testing.assert_array_equal(top_candidates(np.array([1, 3, 3, .5], np.float32), 2), [1, 2])
+    np.testing.assert_array_equal(top_candidates(np.ones(5, np.float32), 3), [0, 1, 2])
+    big = np.random.default_rng(0).random(200_000, dtype=np.float32)
+    np.testing.assert_array_equal(top_candidates(big, 40_000), orc.top_k_stable(big, 40_000))
+
+
+def test_lm_head_argmax():
+    from paper_2510_10129_b200 import _lib as L
+    g = torch.Generator(device=DEV).manual_seed(4)
+    d, V = 3584, 152064
+    h = torch.randn(d, device=DEV, generator=g)
+    gain = torch.rand(d, device=DEV, generator=g) + 0.5
+    W = (torch.randn(V, d, device=DEV, generator=g) * d ** -0.5).to(torch.bfloat16)
+    logits = torch.empty(V, device=DEV)
+    am = torch.empty(1, dtype=torch.int64, device=DEV)
+    ws = torch.empty(64, dtype=torch.uint8, device=DEV)
+    L.call("cc_lm_head_argmax", h.data_ptr(), gain.data_ptr(), 1e-6, d, W.data_ptr(), L.CC_BF16, V,
+           logits.data_ptr(), am.data_ptr(), ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    x = h.double() / torch.sqrt((h.double() ** 2).mean() + 1e-6) * gain.double()
+    ref = W.double() @ x
+    assert (logits.double() - ref).abs().max().item() < 1e-3
+    assert int(am.item()) == int(torch.argmax(logits).item())

@@ -1,0 +1,173 @@
+"""End-to-end parity of the device hot path against the CPU oracle and the
+reference's own golden outputs (tests/golden/*.npz).
+
+Tolerances (stated here, measured on B200):
+  * token selection (indices, window records), merged layout: EXACT;
+  * importance scores: rtol 1e-5 (fp32-faithful 3xTF32 scoring model);
+  * merged keys/values from identical chunk caches: BITWISE (fp32 rotation
+    with separately rounded products, then bf16 rounding);
+  * recomputed K/V and first-token logits of the bf16 primary: within
+    BF16_KV_RTOL relative L2 / BF16_LOGIT_TOL x std(logits), and never more
+    than 2x the error of the device's own dense bf16 full prefill on the same
+    inputs (SURVEY §8(c) calibration rule).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cacheclip_oracle as orc
+from oracle.synth import B1, C1, C1_EXACT
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+DEV = "cuda"
+BF16_KV_RTOL = 2e-2
+BF16_LOGIT_TOL = 5e-2
+
+
+def _cfg(oc: orc.OracleConfig, dtype: str):
+    from paper_2510_10129_b200 import ModelConfig
+    return ModelConfig(n_layers=oc.n_layers, n_heads=oc.n_heads, d_model=oc.d_model, d_head=oc.d_head,
+                       d_ff=oc.d_ff, vocab_size=oc.vocab_size, rope_base=oc.rope_base, norm_eps=oc.norm_eps,
+                       activation=oc.activation, mlp_gated=oc.mlp_gated, attn_bias=oc.attn_bias,
+                       mlp_bias=oc.mlp_bias, tokenizer_id="chars", n_kv_heads=oc.kv_heads, dtype=dtype)
+
+
+def _bf16_params(p):
+    out = {}
+    for k, v in p.items():
+        out[k] = orc.round_to_bf16(v) if v.ndim == 2 else v
+    return out
+
+
+class Case:
+    def __init__(self, w):
+        import paper_2510_10129_b200 as cc
+        self.w = w
+        self.g = dict(np.load(os.path.join(GOLDEN, f"{w.name}.npz")))
+        self.p_params = orc.seeded_params(w.primary, w.primary_seed, w.bias_std)
+        self.a_params = orc.seeded_params(w.aux, w.aux_seed, w.bias_std)
+        self.primary = cc.from_params(_cfg(w.primary, "bf16"), self.p_params)
+        self.aux = cc.from_params(_cfg(w.aux, "fp32"), self.a_params)
+        self.o_primary = orc.OracleModel(w.primary, _bf16_params(self.p_params))   # same bf16 weights
+        self.o_aux = orc.OracleModel(w.aux, self.a_params)
+        self.prefix, self.chunk_ids, self.query = w.token_ids(0)
+        self.config = cc.SelectionConfig(w.ratio, w.window_len, w.window_threshold)
+
+
+@pytest.fixture(scope="module", params=[C1, C1_EXACT, B1], ids=lambda w: w.name)
+def case(request):
+    return Case(request.param)
+
+
+def _upload_chunk(o: orc.Chunk, dtype, fp):
+    import paper_2510_10129_b200 as cc
+    k = np.stack(o.keys)
+    v = np.stack(o.values)
+    return cc.ChunkCache(torch.from_numpy(k).to(DEV, dtype), torch.from_numpy(v).to(DEV, dtype), o.token_ids,
+                         o.prefix_len, "chars", fp)
+
+
+def test_chain_selection_matches_reference(case):
+    """Device chunk precompute + scoring + selection reproduce the REFERENCE's
+    selected indices and window records exactly (golden fixture)."""
+    import paper_2510_10129_b200 as cc
+    aux_chunks = [cc.prefill_chunk(case.aux, case.prefix, c) for c in case.chunk_ids]
+    scores = cc.aux_score_tokens(case.aux, aux_chunks, case.query)
+    np.testing.assert_allclose(scores.scores, case.g["scores"], rtol=1e-5, atol=1e-9)
+    sel = cc.select_tokens(scores, case.config)
+    sink = case.w.prefix_len
+    assert tuple(i + sink for i in sel.indices) == tuple(int(i) for i in case.g["indices"])
+    win = np.array([[x.window_id, x.chunk, x.start, x.end, x.selected, int(x.kept), int(x.partial)]
+                    for x in sel.windows], dtype=np.int64).reshape(-1, 7)
+    np.testing.assert_array_equal(win, case.g["windows"])
+
+
+def test_stage_parity_from_identical_caches(case):
+    """Feed the oracle's own chunk caches to the device path: merge bitwise,
+    scores rtol 1e-5, selection exact, recompute + logits within bf16 tolerance."""
+    import paper_2510_10129_b200 as cc
+    w = case.w
+    o_chunks = [orc.prefill_chunk(case.o_primary, case.prefix, c) for c in case.chunk_ids]
+    # the device primary stores bf16 caches: round the oracle caches identically
+    for ch in o_chunks:
+        ch.keys = [orc.round_to_bf16(k) for k in ch.keys]
+        ch.values = [orc.round_to_bf16(v) for v in ch.values]
+    o_aux_chunks = [orc.prefill_chunk(case.o_aux, case.prefix, c) for c in case.chunk_ids]
+    d_chunks = [_upload_chunk(c, torch.bfloat16, case.primary.fingerprint) for c in o_chunks]
+    d_aux = [_upload_chunk(c, torch.float32, case.aux.fingerprint) for c in o_aux_chunks]
+
+    # merge: bitwise after bf16 rounding
+    merged = cc.merge_caches(d_chunks, case.primary.config.rope, capacity=10_000)
+    o_merged = orc.merge(o_chunks, w.primary.d_head, w.primary.rope_base)
+    for l in range(w.primary.n_layers):
+        np.testing.assert_array_equal(merged.keys[l].float().cpu().numpy(), orc.round_to_bf16(o_merged.keys[l]))
+        np.testing.assert_array_equal(merged.values[l].float().cpu().numpy(), o_merged.values[l])
+    assert merged.token_ids == o_merged.token_ids and merged.source == o_merged.source
+
+    # scoring + selection
+    o_scores = orc.aux_scores(case.o_aux, o_aux_chunks, case.query)
+    scores = cc.aux_score_tokens(case.aux, d_aux, case.query)
+    np.testing.assert_allclose(scores.scores, o_scores, rtol=1e-5, atol=1e-9)
+    o_idx, o_win = orc.select(o_scores, [c.chunk_len for c in o_aux_chunks], w.ratio, w.window_len,
+                              w.window_threshold)
+    sel = cc.select_tokens(scores, case.config)
+    assert sel.indices == o_idx
+
+    # full pipeline from identical caches
+    tok = cc.GreedyTokenizer(cc.char_vocab(max(w.primary.vocab_size, w.aux.vocab_size)), "chars")
+    out = cc.cacheclip_prefill(case.primary, case.aux, d_chunks, d_aux, tok.decode(case.query), case.config,
+                               primary_tokenizer=tok, aux_tokenizer=tok)
+    o_out = orc.cacheclip(case.o_primary, case.o_aux, o_chunks, o_aux_chunks, case.query, w.ratio,
+                          window_len=w.window_len, threshold=w.window_threshold)
+    assert out.plan.indices == o_out.indices
+    assert out.cache.recomputed_rows == o_out.cache.recomputed_rows
+    assert out.cache.token_ids == o_out.cache.token_ids
+    sel_rows = np.asarray(o_out.indices, dtype=np.int64)
+    q_rows = np.arange(o_out.cache.n_rows - len(case.query), o_out.cache.n_rows)
+    rows = np.concatenate([sel_rows, q_rows])
+    for l in range(w.primary.n_layers):
+        for got_t, want in ((out.cache.keys[l], o_out.cache.keys[l]), (out.cache.values[l], o_out.cache.values[l])):
+            got = got_t.float().cpu().numpy()[rows]
+            ref = want[rows]
+            rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-12)
+            assert rel < BF16_KV_RTOL, (l, rel)
+    dl = np.abs(out.logits - o_out.logits).max()
+    assert dl < BF16_LOGIT_TOL * o_out.logits.std(), dl
+    # calibration: the device's dense bf16 full prefill on the same context
+    full = cc.full_attention_prefill(case.primary, orc.context_ids(o_chunks, case.query))
+    o_full = orc.full_prefill(case.o_primary, orc.context_ids(o_chunks, case.query))
+    dense_err = np.abs(full.logits - o_full.logits).max()
+    print(f"{w.name}: |dlogits| clip={dl:.3e} dense={dense_err:.3e} std={o_out.logits.std():.3f} "
+          f"m={len(out.plan.indices)}")
+    assert dl <= 2 * dense_err + 1e-3 * o_out.logits.std()
+
+
+def test_full_prefill_and_ratio_identities(case):
+    import paper_2510_10129_b200 as cc
+    w = case.w
+    chunks = [cc.prefill_chunk(case.primary, case.prefix, c) for c in case.chunk_ids]
+    aux_chunks = [cc.prefill_chunk(case.aux, case.prefix, c) for c in case.chunk_ids]
+    ids = cc.reuse_context_ids(chunks, case.query)
+    full = cc.full_attention_prefill(case.primary, ids)
+    std = case.g["full_logits"].std()
+    assert np.abs(full.logits - case.g["full_logits"]).max() < BF16_LOGIT_TOL * std
+    # ratio 0 == direct reuse, bitwise on device (test_pipeline.py:124-133)
+    clip0 = cc.cacheclip_prefill(case.primary, case.aux, chunks, aux_chunks, case.query,
+                                 cc.SelectionConfig(0.0))
+    direct = cc.direct_reuse_prefill(case.primary, chunks, case.query)
+    assert clip0.plan.indices == ()
+    np.testing.assert_array_equal(clip0.logits, direct.logits)
+    # ratio 1 == full prefill within the bf16 tolerance (test_pipeline.py:144-150)
+    clip1 = cc.cacheclip_prefill(case.primary, case.aux, chunks, aux_chunks, case.query,
+                                 cc.SelectionConfig(1.0))
+    assert clip1.plan.indices == tuple(range(w.prefix_len, clip1.cache.layout.total))
+    assert np.abs(clip1.logits - full.logits).max() < BF16_LOGIT_TOL * std
+    # the CacheClip strategy vs the reference's own first-token logits
+    clip = cc.cacheclip_prefill(case.primary, case.aux, chunks, aux_chunks, case.query, case.config)
+    assert clip.plan.indices == tuple(int(i) for i in case.g["indices"])
+    assert np.abs(clip.logits - case.g["clip_logits"]).max() < BF16_LOGIT_TOL * std
+    assert clip.first_token == int(np.argmax(clip.logits))

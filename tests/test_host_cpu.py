@@ -1,0 +1,129 @@
+"""CPU-side checks: the C-ABI library loads and exports every symbol the
+header declares, and the host logic (budget, tokenizers, alignment, MAC
+accounting, weight layouts) matches the reference's contracts."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "cacheclip_sm100.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|const char\*)\s+(cc_\w+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2510_10129_b200 import _lib
+    lib = _lib.load()
+    names = _declared()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(lib, n), n
+    assert set(names) == set(_lib.EXPORTED_SYMBOLS)
+    assert lib.cc_abi_version() == 1
+
+
+def test_struct_layouts_match_header():
+    from paper_2510_10129_b200 import _lib
+    assert ctypes.sizeof(_lib.KvSegment) == 48
+    assert ctypes.sizeof(_lib.BankSeq) == 40
+
+
+def test_budget_kats():
+    from paper_2510_10129_b200 import selection_budget
+    assert selection_budget(0.2, 125) == 25
+    assert selection_budget(0.2, 16) == 4
+    assert selection_budget(0.3, 10) == 3
+    assert selection_budget(1.0, 7) == 7
+    assert selection_budget(0.0, 7) == 0
+    assert selection_budget(0.5, 0) == 0
+    assert selection_budget(0.2, 32768) == 6554
+    with pytest.raises(ValueError):
+        selection_budget(0.5, -1)
+
+
+def test_selection_config_validation():
+    from paper_2510_10129_b200 import SelectionConfig
+    with pytest.raises(ValueError):
+        SelectionConfig(recomp_ratio=1.5)
+    with pytest.raises(ValueError):
+        SelectionConfig(recomp_ratio=0.5, window_len=0)
+    with pytest.raises(ValueError):
+        SelectionConfig(recomp_ratio=0.5, window_threshold=9)
+
+
+def test_tokenizer_roundtrip_and_alignment():
+    from paper_2510_10129_b200 import GreedyTokenizer, TokenSpan, align_spans, char_vocab
+    from paper_2510_10129_b200.errors import SpanCoverageError, UnknownCharacterError
+    tok = GreedyTokenizer(["a", "b", "ab", "abc", " "], "t")
+    spans = tok.encode_with_offsets("abcab a")
+    assert [s.token_id for s in spans] == [3, 2, 4, 0]
+    assert tok.decode(tok.encode("abcab a")) == "abcab a"
+    with pytest.raises(UnknownCharacterError):
+        tok.encode("z")
+    src = [TokenSpan(0, 0, 2), TokenSpan(1, 2, 3)]
+    dst = [TokenSpan(0, 0, 1), TokenSpan(1, 1, 3)]
+    assert align_spans(src, dst).images == ((0, 1), (1,))
+    with pytest.raises(SpanCoverageError):
+        align_spans(src, [TokenSpan(0, 0, 1)])
+    v = char_vocab(152064)
+    assert len(set(v)) == 152064
+    ct = GreedyTokenizer(v, "chars")
+    ids = list(np.random.default_rng(0).integers(0, 152064, 2000))
+    assert ct.encode(ct.decode(ids)) == [int(i) for i in ids]
+
+
+def test_mac_closed_forms_equal_reference_convention():
+    """With n_kv_heads == n_heads the closed forms reproduce the reference's
+    full_prefill_macs / extend_macs (flops.py:123-173) term by term."""
+    from paper_2510_10129_b200 import ModelConfig, extend_macs, full_prefill_macs
+    c = ModelConfig(n_layers=3, n_heads=4, d_model=48, d_head=12, d_ff=96, vocab_size=160, mlp_gated=True)
+    L, dm, h, dh = 37, 48, 4, 12
+    tri = L * (L + 1) // 2
+    ref = 3 * (3 * L * dm * h * dh + L * h * dh * dm + 2 * L * h * 4 * (dh // 2) + 2 * h * tri * dh
+               + 3 * L * dm * 96) + dm * 160
+    assert full_prefill_macs(c, L) == ref
+    n, p = 5, 20
+    pairs = n * p + n * (n + 1) // 2
+    ref_e = 3 * (3 * n * dm * h * dh + n * h * dh * dm + 2 * n * h * 4 * (dh // 2) + 2 * h * pairs * dh
+                 + 3 * n * dm * 96) + dm * 160
+    assert extend_macs(c, n, p) == ref_e
+
+
+def test_glu_interleave_layout():
+    import torch
+    from paper_2510_10129_b200.weights import _interleave_bias, _interleave_glu
+    g = torch.arange(300 * 2, dtype=torch.float32).view(300, 2)
+    u = -g
+    w = _interleave_glu(g, u)
+    assert w.shape == (2 * 384, 2)
+    assert torch.equal(w[0:128], g[0:128]) and torch.equal(w[128:256], u[0:128])
+    assert torch.equal(w[512:512 + 44], g[256:300]) and torch.equal(w[640:640 + 44], u[256:300])
+    assert torch.count_nonzero(w[512 + 44:640]) == 0
+    b = _interleave_bias(torch.arange(300.), -torch.arange(300.))
+    assert b.shape == (768,) and b[128] == 0 and b[129] == -1
+
+
+def test_reference_init_matches_oracle_recipe():
+    from oracle import cacheclip_oracle as orc
+    from oracle.synth import C1_PRIMARY
+    from paper_2510_10129_b200 import ModelConfig, reference_init_params
+    c = ModelConfig(n_layers=4, n_heads=4, n_kv_heads=2, d_model=256, d_head=64, d_ff=1024, vocab_size=512,
+                    rope_base=1e4, activation="silu", mlp_gated=True)
+    a = reference_init_params(c, 0)
+    b = orc.seeded_params(C1_PRIMARY, 0)
+    assert a.keys() == b.keys()
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_rope_inv_freq_matches_reference_formula():
+    from paper_2510_10129_b200 import RopeParams
+    r = RopeParams(128, 1e6)
+    np.testing.assert_array_equal(r.inv_freq, 1e6 ** (-np.arange(0, 128, 2, dtype=np.float64) / 128))
