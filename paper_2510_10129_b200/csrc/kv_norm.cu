@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const cc_kv_segment* __re
                                                        int64_t n_dst_rows, int n_layers, int kv_heads,
                                                        int head_dim, InvFreq inv, int64_t pos_offset,
                                                        T* __restrict__ dst_k, T* __restrict__ dst_v,
-                                                       int64_t dst_rows_cap) {
+                                                       int64_t dst_rows_cap, int copy_v) {
   constexpr int V = Vec16<T>::N;
   const int vecs_per_row = kv_heads * head_dim / V;
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const cc_kv_segment* __re
   const T* vs = reinterpret_cast<const T*>(sg.v) + src_row * row_elems + col;
   const int64_t src_layer = sg.src_rows * row_elems;
   T* kd = dst_k + row * row_elems + col;
-  T* vd = dst_v + row * row_elems + col;
+  T* vd = copy_v ? dst_v + row * row_elems + col : nullptr;
   const int64_t dst_layer = dst_rows_cap * row_elems;
 
   const double pos = (double)(row + pos_offset);
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const cc_kv_segment* __re
   for (int l = 0; l < n_layers; ++l) {
     float x[V], y[V];
     load_vec<T>(ks + l * src_layer, x);
-    if (dst_v) copy_vec<T>(vs + l * src_layer, vd + l * dst_layer);
+    if (copy_v) copy_vec<T>(vs + l * src_layer, vd + l * dst_layer);
 #pragma unroll
     for (int p = 0; p < V / 2; ++p) rope_pair(x[2 * p], x[2 * p + 1], c[p], s[p], y[2 * p], y[2 * p + 1]);
     store_vec<T>(kd + l * dst_layer, y);
@@ -302,12 +302,12 @@ int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_
   if (dtype == CC_BF16) {
     assemble_kernel<__nv_bfloat16><<<grid, bs, 0, as_stream(stream)>>>(
         segs_dev, n_segs, n_dst_rows, n_layers, kv_heads, head_dim, inv, pos_offset,
-        reinterpret_cast<__nv_bfloat16*>(dst_k), reinterpret_cast<__nv_bfloat16*>(dst_v), dst_rows_cap);
+        reinterpret_cast<__nv_bfloat16*>(dst_k), reinterpret_cast<__nv_bfloat16*>(dst_v), dst_rows_cap, dst_v != nullptr);
   } else if (dtype == CC_F32) {
     assemble_kernel<float><<<grid, bs, 0, as_stream(stream)>>>(segs_dev, n_segs, n_dst_rows, n_layers, kv_heads,
                                                               head_dim, inv, pos_offset,
                                                               reinterpret_cast<float*>(dst_k),
-                                                              reinterpret_cast<float*>(dst_v), dst_rows_cap);
+                                                              reinterpret_cast<float*>(dst_v), dst_rows_cap, dst_v != nullptr);
   } else {
     return fail(CC_ERR_UNSUPPORTED, "cache dtype %d unsupported", dtype);
   }
