@@ -108,8 +108,46 @@ def check(rc: int) -> None:
     raise RuntimeError(f"libcacheclip_sm100: {msg}")
 
 
-def call(name: str, *args) -> None:
-    check(getattr(load(), name)(*args))
+class KernelTimer:
+    """Optional per-launch CUDA-event timing (bench roofline). Each record is
+    (entry point, start event, end event, meta dict) on the launching stream."""
+
+    def __init__(self) -> None:
+        self.records: list = []
+
+    def summary(self) -> dict:
+        import torch
+        torch.cuda.synchronize()
+        out: dict = {}
+        for name, e0, e1, meta in self.records:
+            d = out.setdefault(name, {"launches": 0, "ms": 0.0, "flops": 0.0, "bytes": 0.0})
+            d["launches"] += 1
+            d["ms"] += e0.elapsed_time(e1)
+            d["flops"] += meta.get("flops", 0.0)
+            d["bytes"] += meta.get("bytes", 0.0)
+        return out
+
+
+_timer: KernelTimer | None = None
+
+
+def set_timer(timer: KernelTimer | None) -> None:
+    global _timer
+    _timer = timer
+
+
+def call(name: str, *args, meta: dict | None = None) -> None:
+    fn = getattr(load(), name)
+    t = _timer
+    if t is None:
+        check(fn(*args))
+        return
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    check(fn(*args))
+    e1.record()
+    t.records.append((name, e0, e1, meta or {}))
 
 
 _device_ok: set[int] = set()

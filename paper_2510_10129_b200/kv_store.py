@@ -265,7 +265,8 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
         segs = host_to_device(_segments(spec), first.k.device)
         inv = rope.inv_freq
         _lib.call("cc_assemble_kv", segs.data_ptr(), len(spec), total, L, H, D, _dtype_code(first.k.dtype),
-                  inv.ctypes.data, 0, k_store.data_ptr(), v_store.data_ptr(), cap, _stream())
+                  inv.ctypes.data, 0, k_store.data_ptr(), v_store.data_ptr(), cap, _stream(),
+                  meta={"bytes": 2.0 * 2 * total * L * H * D * first.k.element_size()})
     if trace is not None:
         for _ in range(L):
             trace.rope("merge_overhead", total * H, D)

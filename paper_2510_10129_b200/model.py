@@ -84,7 +84,7 @@ def _dense(model: Model, ids: torch.Tensor, want_logits: bool):
     if c.dtype == "bf16":
         bank = torch.empty(n, c.kv_heads, c.d_head, dtype=torch.bfloat16, device=dev)
         res = forward_rows(model, ids, pos, lambda l: (bank, V[l], None, K[l], None, bank, V[l]), n,
-                           want_logits=want_logits)
+                           want_logits=want_logits, pairs=visible_pairs(n))
         return K, V, res.logits, res.argmax
     tables = bank_tables(c.n_layers, [(None, None, 0, 0, n)], dev)
     h = forward_banked(model, ids, pos, tables, 1, n, 0, v_dst=lambda l: V[l], k_raw_dst=lambda l: K[l])
@@ -184,8 +184,9 @@ def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | No
     ids, pos = dev_buf[:R], dev_buf[R:]
     rf = _row_factor(model, knobs, nq, m, dev)
     ks, vs = cache.k_store, cache.v_store
+    pairs = (int(np.sum(sel_idx + 1)) if m else 0) + (visible_pairs(nq, base) if nq else 0)
     res = forward_rows(model, ids, pos, lambda l: (ks[l], vs[l], pos, None, None, ks[l], vs[l]), base + nq,
-                       row_factor=rf, want_logits=want_logits and nq > 0)
+                       row_factor=rf, want_logits=want_logits and nq > 0, pairs=pairs)
     if trace is not None:
         for _ in range(c.n_layers):
             if m:

@@ -61,7 +61,7 @@ def gemm(kind: int, epilogue: int, M: int, N: int, K: int, A: torch.Tensor, B: t
     a.q_out, a.ldq, a.q_mode = _p(q_out), ldq, q_mode
     a.k_cache, a.v_cache, a.cache_dtype = _p(k_cache), _p(v_cache), cache_dtype
     a.dst_rows, a.k_raw, a.raw_rows = _p(dst_rows), _p(k_raw), _p(raw_rows)
-    _lib.check(_lib.load().cc_gemm(ctypes.byref(a), _s()))
+    _lib.call("cc_gemm", ctypes.byref(a), _s(), meta={"flops": 2.0 * M * N * K, "kind": kind})
 
 
 def rope_table(model: Model, positions: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
@@ -104,7 +104,8 @@ class RowsResult:
 
 def forward_rows(model: Model, ids: torch.Tensor, positions: torch.Tensor,
                  kv: Callable[[int], tuple], n_keys: int, *, row_factor: torch.Tensor | None = None,
-                 want_logits: bool = True, logits_out: torch.Tensor | None = None) -> RowsResult:
+                 want_logits: bool = True, logits_out: torch.Tensor | None = None,
+                 pairs: int = 0) -> RowsResult:
     """bf16 engine. kv(layer) -> (k_scatter, v_scatter, dst_rows, k_raw, raw_rows,
     attn_k, attn_v): where the QKV epilogue writes and what attention reads."""
     c = model.config
@@ -135,7 +136,7 @@ def forward_rows(model: Model, ids: torch.Tensor, positions: torch.Tensor,
              dst_rows=dst, k_raw=kraw, raw_rows=rrows, heads=(c.n_heads, c.kv_heads, c.d_head))
         _lib.call("cc_sparse_row_attention", q.data_ptr(), qw, positions.data_ptr(), R, ak.data_ptr(),
                   av.data_ptr(), n_keys, c.n_heads, c.kv_heads, c.d_head, factor, _p(row_factor),
-                  ctx.data_ptr(), qw, _s())
+                  ctx.data_ptr(), qw, _s(), meta={"flops": 4.0 * c.n_heads * c.d_head * pairs})
         gemm(BF, _lib.CC_EPI_RESIDUAL, R, d, qw, ctx, lw.w_o, bias=lw.b_o, C=h, ldc=d, c_mode=_lib.CC_F32)
         _mlp(model, lw, h, x, act, BF, _lib.CC_BF16)
     logits = argmax = None
