@@ -226,6 +226,7 @@ def run_ours(args, rank: int, world: int):
     evs = []
     barrier()
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push("timed")
     with ClockSampler(local) as clocks:
         _lib.set_timer(timer)
         for _ in range(args.steps):
@@ -237,6 +238,7 @@ def run_ours(args, rank: int, world: int):
             evs.append((e0, e1))
         _lib.set_timer(None)
         torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ttft = float(np.mean(step_ms))
