@@ -151,6 +151,13 @@ int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions
                             int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
                             float factor, const float* row_factor,
                             void* out, int64_t ldo, void* stream);
+/* Same contract on legacy mma.sync tensor cores: the baseline the tcgen05
+ * kernel above is measured against (kept for A/B tests and the bench). */
+int cc_sparse_row_attention_mma(const void* q, int64_t ldq, const int64_t* positions, int64_t m,
+                                const void* k_cache, const void* v_cache, int64_t n_keys,
+                                int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
+                                float factor, const float* row_factor,
+                                void* out, int64_t ldo, void* stream);
 
 /* Float32 banked causal attention (the fp32-faithful aux model path,
  * peek_forward / prefill of the scoring model): for sequence s, new row i

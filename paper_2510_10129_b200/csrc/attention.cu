@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kBankThreads) banked_attention_f32_kernel(
 
 using namespace cc;
 
-extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions, int64_t m,
+extern "C" int cc_sparse_row_attention_mma(const void* q, int64_t ldq, const int64_t* positions, int64_t m,
                                        const void* k_cache, const void* v_cache, int64_t n_keys, int32_t n_q_heads,
                                        int32_t n_kv_heads, int32_t head_dim, float factor, const float* row_factor,
                                        void* out, int64_t ldo, void* stream) {

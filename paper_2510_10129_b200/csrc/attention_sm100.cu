@@ -1,0 +1,411 @@
+// Sparse-row flash attention on tcgen05 (sm_100a).
+//
+// causal_attention(q, bank_k, bank_v, row_limits=idx+1) of selective_forward
+// (model.py:715-720) — and the mask_offset rule of layer_forward
+// (model.py:467-476) for query rows and dense prefill — without materialising
+// the (H, m, n) logits of tensor_core.py:166-170.
+//
+// One CTA = 128 packed query rows x one KV head. GQA packing: packed row
+// p = i*G + g is selected row i, query head kvh*G + g, so every K/V tile is
+// fetched once for all G heads that share it. Keys stream in 128-key tiles
+// up to the CTA's largest row limit (rows are sorted by position, so a tile's
+// rows span a narrow range and little work is masked).
+//
+//   warp 0      TMA producer: K and V tiles ([keys][D] bf16, 128B swizzle), 2 stages
+//   warp 1      tcgen05.mma issuer: S_j = Q K_j^T into TMEM (double-buffered),
+//               O += P_j V_j (P from smem, V as an MN-major operand)
+//   warps 2..5  softmax: thread t owns packed row t — its S row comes out of
+//               TMEM with tcgen05.ld, max/exp2/sum run in-thread (no shuffles),
+//               P (bf16) goes to smem for the PV MMA. Lazy rescaling: the
+//               running max only moves (and O in TMEM is rescaled) when a tile
+//               raises it by more than 2^8, so p <= 256 and O rarely needs a
+//               TMEM round trip. Final O / l -> bf16 context rows.
+#include "cc_common.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+namespace cc {
+
+constexpr int kFaRows = 128;
+constexpr int kFaKeys = 128;
+constexpr int kFaThreads = 192;
+constexpr float kFaRescaleThreshold = 8.0f;  // log2 domain
+
+template <int D>
+struct FaCfg {
+  static constexpr int KB = D / 64;               // 128-byte K-blocks per row of Q / K
+  static constexpr int Q_BYTES = kFaRows * D * 2;  // 32 KB (D=128)
+  static constexpr int KT_BYTES = kFaKeys * D * 2; // one K (or V) tile
+  static constexpr int P_BYTES = kFaRows * kFaKeys * 2;
+  static constexpr int STAGES = 2;
+  static constexpr int SMEM = Q_BYTES + 2 * STAGES * KT_BYTES + P_BYTES + 1024 + 256;
+  static constexpr uint32_t IDESC_S = umma_idesc(128, kFaKeys, false);
+  static constexpr uint32_t IDESC_PV = umma_idesc(128, D, false) | (1u << 16);  // B (V) MN-major
+  static constexpr int S_COL0 = 0, S_COL1 = kFaKeys, O_COL = 2 * kFaKeys;
+};
+
+// MN-major 128B-swizzled operand: 64-element rows of 128 B, MN atoms LBO
+// apart, 8-row K groups SBO apart.
+__device__ __forceinline__ uint64_t umma_desc_mn_sw128(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const void* desc, uint64_t* bar, int32_t x, int32_t y,
+                                            int32_t z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(desc), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+      "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+      "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+      "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+      "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+      "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kFaThreads, 1)
+    fa_sparse_row_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                         const __nv_bfloat16* __restrict__ q, int64_t ldq, const int64_t* __restrict__ pos, int64_t m,
+                         int64_t n_keys, int n_q_heads, int n_kv_heads, float factor,
+                         const float* __restrict__ row_factor, __nv_bfloat16* __restrict__ out, int64_t ldo,
+                         int n_qtiles) {
+  using Cfg = FaCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + Cfg::Q_BYTES;                       // [STAGES][KT_BYTES]
+  uint8_t* sV = sK + Cfg::STAGES * Cfg::KT_BYTES;
+  uint8_t* sP = sV + Cfg::STAGES * Cfg::KT_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::P_BYTES);
+  uint64_t* k_full = bars;        // [2]
+  uint64_t* v_full = bars + 2;    // [2]
+  uint64_t* kv_empty = bars + 4;  // [2]
+  uint64_t* s_full = bars + 6;    // [2]
+  uint64_t* p_full = bars + 8;
+  uint64_t* pv_done = bars + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  int* s_kmax = reinterpret_cast<int*>(bars + 11);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = n_q_heads / n_kv_heads;
+  const int kvh = blockIdx.y;
+  const int qtile = n_qtiles - 1 - (int)blockIdx.x;  // heavy (late-position) tiles first
+  const int64_t packed_total = m * G;
+  const int64_t p0 = (int64_t)qtile * kFaRows;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+      mbar_init(&s_full[s], 1);
+    }
+    mbar_init(p_full, 4);
+    mbar_init(pv_done, 1);
+    *s_kmax = 0;
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+
+  // ---- prologue: softmax warps gather their Q row into swizzled smem -----
+  int lim = 0;
+  float scale2 = 0.f;
+  int64_t out_off = -1;
+  if (warp >= 2) {
+    const int r = (warp & 3) * 32 + lane;  // TMEM lane quarter = warp % 4
+    const int64_t p = p0 + r;
+    uint4 zero = make_uint4(0, 0, 0, 0);
+    const uint4* src = nullptr;
+    if (p < packed_total) {
+      const int64_t i = p / G;
+      const int head = kvh * G + (int)(p % G);
+      const int64_t ps = pos[i];
+      lim = (int)min(ps + 1, n_keys);
+      scale2 = (row_factor ? row_factor[i] : factor) * 1.4426950408889634f;
+      src = reinterpret_cast<const uint4*>(q + i * ldq + (int64_t)head * D);
+      out_off = i * ldo + (int64_t)head * D;
+    }
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+      const uint4 v = src ? __ldg(src + c) : zero;
+      const int kb = c >> 3, cc = c & 7;
+      *reinterpret_cast<uint4*>(sQ + kb * (kFaRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
+    }
+    fence_proxy_async_smem();
+    int mx = lim;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) atomicMax(s_kmax, mx);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int n_tiles = (*s_kmax + kFaKeys - 1) / kFaKeys;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0 && n_tiles > 0) {
+      tma_prefetch_desc(&tmK);
+      tma_prefetch_desc(&tmV);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j & 1;
+        const uint32_t ph = (j >> 1) & 1;
+        mbar_wait(&kv_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&k_full[s], Cfg::KT_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < Cfg::KB; ++kb)
+          tma_load_3d(sK + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmK, &k_full[s], kb * 64, kvh, j * kFaKeys);
+        mbar_arrive_expect_tx(&v_full[s], Cfg::KT_BYTES);
+#pragma unroll
+        for (int kb = 0; kb < Cfg::KB; ++kb)
+          tma_load_3d(sV + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmV, &v_full[s], kb * 64, kvh, j * kFaKeys);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    auto issue_s = [&](int j) {
+      const int s = j & 1;
+      mbar_wait(&k_full[s], (j >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK + s * Cfg::KT_BYTES);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k >> 2) * (kFaRows * 128) + (k & 3) * 32;
+          const uint32_t koff = (k >> 2) * (kFaKeys * 128) + (k & 3) * 32;
+          tc_mma<false>(tmem + (s ? Cfg::S_COL1 : Cfg::S_COL0), umma_desc_sw128(q0 + off),
+                        umma_desc_sw128(k0 + koff), Cfg::IDESC_S, k > 0 ? 1u : 0u);
+        }
+        tc_commit(&s_full[s]);
+      }
+      __syncwarp();
+    };
+    auto issue_pv = [&](int j) {
+      const int s = j & 1;
+      mbar_wait(p_full, j & 1);
+      mbar_wait(&v_full[s], (j >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t p0a = smem_u32(sP), v0 = smem_u32(sV + s * Cfg::KT_BYTES);
+#pragma unroll
+        for (int k = 0; k < kFaKeys / 16; ++k) {
+          const uint32_t off = (k >> 2) * (kFaRows * 128) + (k & 3) * 32;
+          tc_mma<false>(tmem + Cfg::O_COL, umma_desc_sw128(p0a + off),
+                        umma_desc_mn_sw128(v0 + k * 16 * 128, kFaKeys * 128, 1024), Cfg::IDESC_PV,
+                        (j > 0 || k > 0) ? 1u : 0u);
+        }
+        tc_commit(&kv_empty[s]);
+        tc_commit(pv_done);
+      }
+      __syncwarp();
+    };
+    if (n_tiles > 0) issue_s(0);
+    if (n_tiles > 1) issue_s(1);
+    for (int j = 0; j < n_tiles; ++j) {
+      issue_pv(j);
+      if (j + 2 < n_tiles) issue_s(j + 2);
+    }
+  } else {
+    // ---------------- softmax + epilogue (row per thread) ----------------
+    const int quarter = warp & 3;
+    const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
+    const int r = quarter * 32 + lane;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      const int s = j & 1;
+      mbar_wait(&s_full[s], (j >> 1) & 1);
+      tc_fence_after();
+      float sv[kFaKeys];
+#pragma unroll
+      for (int c = 0; c < kFaKeys / 32; ++c)
+        tmem_ld32(tmem + lane_base + (s ? Cfg::S_COL1 : Cfg::S_COL0) + c * 32, sv + c * 32);
+      const int key0 = j * kFaKeys;
+      float mt = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kFaKeys; ++c) {
+        float x = sv[c] * scale2;
+        x = (key0 + c < lim) ? x : -INFINITY;
+        sv[c] = x;
+        mt = fmaxf(mt, x);
+      }
+      // lazy rescale: move the running max only when the tile exceeds it by > 2^8
+      float alpha = 1.f;
+      bool resc = false;
+      if (mt > m_run + kFaRescaleThreshold) {
+        alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
+        m_run = mt;
+        resc = true;
+      }
+      const float base = (m_run == -INFINITY) ? 0.f : m_run;
+      float lsum = 0.f;
+      uint32_t pk[kFaKeys / 2];
+#pragma unroll
+      for (int c = 0; c < kFaKeys / 2; ++c) {
+        const float a = exp2f(sv[2 * c] - base), b = exp2f(sv[2 * c + 1] - base);
+        lsum += a + b;
+        pk[c] = pack2_bf16(a, b);
+      }
+      l_run = l_run * alpha + lsum;
+      if (j > 0) {
+        mbar_wait(pv_done, (j - 1) & 1);  // P buffer free, O stable
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, resc)) {
+          const float a = resc ? alpha : 1.f;
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            float ov[32];
+            tmem_ld32(tmem + lane_base + Cfg::O_COL + c * 32, ov);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) ov[e] *= a;
+            tmem_st32(tmem + lane_base + Cfg::O_COL + c * 32, ov);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+      }
+      // P row -> smem (K-major, 128B swizzle: 2 regions of 64 keys)
+#pragma unroll
+      for (int c = 0; c < kFaKeys / 8; ++c) {
+        const int kb = c >> 3, cc = c & 7;
+        *reinterpret_cast<uint4*>(sP + kb * (kFaRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+    }
+    if (n_tiles > 0) {
+      mbar_wait(pv_done, (n_tiles - 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      float ov[32];
+      tmem_ld32(tmem + lane_base + Cfg::O_COL + c * 32, ov);
+      if (out_off >= 0) {
+        uint4* dst = reinterpret_cast<uint4*>(out + out_off + c * 32);
+#pragma unroll
+        for (int qd = 0; qd < 4; ++qd)
+          dst[qd] = make_uint4(pack2_bf16(ov[8 * qd] * inv, ov[8 * qd + 1] * inv),
+                               pack2_bf16(ov[8 * qd + 2] * inv, ov[8 * qd + 3] * inv),
+                               pack2_bf16(ov[8 * qd + 4] * inv, ov[8 * qd + 5] * inv),
+                               pack2_bf16(ov[8 * qd + 6] * inv, ov[8 * qd + 7] * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 fa_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) == cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// [n_keys][Hkv][D] bf16 bank as a 3-D tensor map, box {64, 1, 128 keys}.
+static int make_kv_map(CUtensorMap* map, const void* base, int64_t n_keys, int hkv, int d) {
+  auto enc = fa_encode();
+  if (!enc) return fail(CC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)hkv, (cuuint64_t)n_keys};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 2, (cuuint64_t)hkv * d * 2};
+  cuuint32_t box[3] = {64, 1, (cuuint32_t)kFaKeys};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CC_ERR_CUDA, "cuTensorMapEncodeTiled (kv) failed (%d)", (int)r);
+  return CC_OK;
+}
+
+template <int D>
+static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64_t m, const void* k_cache,
+                     const void* v_cache, int64_t n_keys, int32_t hq, int32_t hkv, float factor,
+                     const float* row_factor, void* out, int64_t ldo, cudaStream_t st) {
+  CUtensorMap tk, tv;
+  int rc = make_kv_map(&tk, k_cache, n_keys, hkv, D);
+  if (rc) return rc;
+  rc = make_kv_map(&tv, v_cache, n_keys, hkv, D);
+  if (rc) return rc;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fa_sparse_row_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaCfg<D>::SMEM);
+    attr = true;
+  }
+  const int G = hq / hkv;
+  const int n_qtiles = (int)((m * G + kFaRows - 1) / kFaRows);
+  dim3 grid(n_qtiles, hkv);
+  fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
+      tk, tv, (const __nv_bfloat16*)q, ldq, positions, m, n_keys, hq, hkv, factor, row_factor,
+      (__nv_bfloat16*)out, ldo, n_qtiles);
+  CC_LAUNCH_CHECK("fa_sparse_row");
+  return CC_OK;
+}
+
+}  // namespace cc
+
+using namespace cc;
+
+extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions, int64_t m,
+                                       const void* k_cache, const void* v_cache, int64_t n_keys, int32_t n_q_heads,
+                                       int32_t n_kv_heads, int32_t head_dim, float factor, const float* row_factor,
+                                       void* out, int64_t ldo, void* stream) {
+  CC_CHECK_ARG(n_kv_heads > 0 && n_q_heads % n_kv_heads == 0, CC_ERR_DIMENSION,
+               "query heads %d not a multiple of kv heads %d", n_q_heads, n_kv_heads);
+  CC_CHECK_ARG(head_dim == 64 || head_dim == 128, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
+  CC_CHECK_ARG(n_keys > 0, CC_ERR_VALUE, "attention row with no visible keys");
+  CC_CHECK_ARG(((uintptr_t)k_cache % 16) == 0 && ((uintptr_t)v_cache % 16) == 0 && ((uintptr_t)q % 16) == 0 &&
+                   (ldq % 8) == 0 && (ldo % 8) == 0,
+               CC_ERR_UNSUPPORTED, "attention operands must be 16-byte aligned");
+  if (m <= 0) return CC_OK;
+  cudaStream_t st = as_stream(stream);
+  if (head_dim == 128)
+    return fa_launch<128>(q, ldq, positions, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
+                          out, ldo, st);
+  return fa_launch<64>(q, ldq, positions, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
+                       out, ldo, st);
+}

@@ -180,22 +180,47 @@ def _attn_ref(q, k, v, limits, factor):
     return torch.einsum("hmn,nhd->mhd", w, vv)
 
 
-@pytest.mark.parametrize("D,Hq,Hkv,m,n", [(128, 28, 4, 300, 2000), (64, 4, 2, 100, 1040), (128, 8, 8, 5, 70)])
-def test_sparse_row_attention(D, Hq, Hkv, m, n):
+@pytest.mark.parametrize("entry", ["cc_sparse_row_attention", "cc_sparse_row_attention_mma"])
+@pytest.mark.parametrize("D,Hq,Hkv,m,n,spread", [(128, 28, 4, 300, 2000, "sorted"), (64, 4, 2, 100, 1040, "sorted"),
+                                                 (128, 8, 8, 5, 70, "sorted"), (128, 28, 4, 1000, 1000, "dense"),
+                                                 (64, 14, 2, 777, 5000, "tail")])
+def test_sparse_row_attention(entry, D, Hq, Hkv, m, n, spread):
     from paper_2510_10129_b200 import _lib as L
     g = torch.Generator(device=DEV).manual_seed(D + m)
     q = torch.randn(m, Hq, D, device=DEV, generator=g).to(torch.bfloat16)
-    k = torch.randn(n, Hkv, D, device=DEV, generator=g).to(torch.bfloat16)
+    k = (torch.randn(n, Hkv, D, device=DEV, generator=g) * 2).to(torch.bfloat16)
     v = torch.randn(n, Hkv, D, device=DEV, generator=g).to(torch.bfloat16)
-    pos = torch.sort(torch.randperm(n, generator=torch.Generator().manual_seed(1))[:m]).values.to(DEV)
-    out = torch.empty(m, Hq * D, device=DEV, dtype=torch.bfloat16)
+    if spread == "dense":
+        pos = torch.arange(n, device=DEV)
+    elif spread == "tail":
+        pos = torch.arange(n - m, n, device=DEV)
+    else:
+        pos = torch.sort(torch.randperm(n, generator=torch.Generator().manual_seed(1))[:m]).values.to(DEV)
+    out = torch.zeros(m, Hq * D, device=DEV, dtype=torch.bfloat16)
     factor = 1.0 / math.sqrt(D)
-    L.call("cc_sparse_row_attention", q.data_ptr(), Hq * D, pos.data_ptr(), m, k.data_ptr(), v.data_ptr(), n, Hq,
+    L.call(entry, q.data_ptr(), Hq * D, pos.data_ptr(), m, k.data_ptr(), v.data_ptr(), n, Hq,
            Hkv, D, factor, None, out.data_ptr(), Hq * D, torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     ref = _attn_ref(q, k, v, pos + 1, factor)
     err = (out.double().view(m, Hq, D) - ref).abs().max().item()
     assert err < 2e-2, err
+
+
+def test_sparse_row_attention_row_factor():
+    from paper_2510_10129_b200 import _lib as L
+    g = torch.Generator(device=DEV).manual_seed(9)
+    m, n, Hq, Hkv, D = 40, 600, 8, 2, 128
+    q = torch.randn(m, Hq, D, device=DEV, generator=g).to(torch.bfloat16)
+    k = torch.randn(n, Hkv, D, device=DEV, generator=g).to(torch.bfloat16)
+    v = torch.randn(n, Hkv, D, device=DEV, generator=g).to(torch.bfloat16)
+    pos = torch.arange(n - m, n, device=DEV)
+    rf = torch.full((m,), 0.9 / (math.sqrt(D) * 0.8), device=DEV)
+    out = torch.empty(m, Hq * D, device=DEV, dtype=torch.bfloat16)
+    L.call("cc_sparse_row_attention", q.data_ptr(), Hq * D, pos.data_ptr(), m, k.data_ptr(), v.data_ptr(), n, Hq,
+           Hkv, D, 0.0, rf.data_ptr(), out.data_ptr(), Hq * D, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = _attn_ref(q, k, v, pos + 1, 0.9 / (math.sqrt(D) * 0.8))
+    assert (out.double().view(m, Hq, D) - ref).abs().max().item() < 2e-2
 
 
 def test_banked_attention_f32_matches_reference_math():
