@@ -222,13 +222,13 @@ def run_ours(args, rank: int, world: int):
     m_sel = len(out.plan.indices)
 
     # ---- timed region: K steps, CUDA events, L2 flushed between steps ----
-    timer = _lib.KernelTimer()
     evs = []
     barrier()
     torch.cuda.synchronize()
+    _lib.profile_collect()  # drop anything recorded before the timed region
     torch.cuda.nvtx.range_push("timed")
     with ClockSampler(local) as clocks:
-        _lib.set_timer(timer)
+        _lib.profile_enable(True)
         for _ in range(args.steps):
             flush.fill_(1)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -236,7 +236,7 @@ def run_ours(args, rank: int, world: int):
             out = step()
             e1.record()
             evs.append((e0, e1))
-        _lib.set_timer(None)
+        _lib.profile_enable(False)
         torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     barrier()
@@ -246,34 +246,41 @@ def run_ours(args, rank: int, world: int):
         t = torch.tensor([ttft], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ttft = float(t.item())
-    ksum = timer.summary()
-    launches = sum(v["launches"] * (2 if k == "cc_lm_head_argmax" else 1) for k, v in ksum.items())
 
-    # per-kernel rooflines (averaged over the timed steps)
-    gemm_bf16 = [r for r in timer.records if r[0] == "cc_gemm" and r[3].get("kind") == 0]
-    gemm_ms = sum(a.elapsed_time(b) for _, a, b, _ in gemm_bf16)
-    gemm_fl = sum(m["flops"] for *_, m in gemm_bf16)
-    attn = ksum.get("cc_sparse_row_attention", {"ms": 0, "flops": 0, "launches": 0})
-    asm = ksum.get("cc_assemble_kv", {"ms": 0, "bytes": 0, "launches": 0})
-    gemm_tf = [r for r in timer.records if r[0] == "cc_gemm" and r[3].get("kind") == 1]
-    tf_ms = sum(a.elapsed_time(b) for _, a, b, _ in gemm_tf)
-    tf_fl = sum(m["flops"] for *_, m in gemm_tf)
+    # per-kernel rooflines from the in-library CUDA-event profiler (timed steps)
+    recs = _lib.profile_collect()
+    ops: dict = {}
+    for op, work, ms in recs:
+        d = ops.setdefault(op, {"launches": 0, "ms": 0.0, "work": 0.0})
+        d["launches"] += 1
+        d["ms"] += ms
+        d["work"] += work
+    launches = sum(v["launches"] * (2 if k == "lm_head" else 1) for k, v in ops.items())
     sust = pk["bf16_sustained"] or pk["bf16"]
-    achieved = gemm_fl / (gemm_ms * 1e-3) / 1e12 if gemm_ms else 0.0
-    stages = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps}
-              for k, v in ksum.items()}
-    kernels = {
-        "gemm_bf16_tcgen05": {"tflops": achieved, "frac_of_sustained": achieved / sust,
-                              "ms_per_step": gemm_ms / args.steps},
-        "gemm_3xtf32_tcgen05": {"tflops_effective_fp32": (tf_fl / (tf_ms * 1e-3) / 1e12) if tf_ms else 0.0,
-                                "ms_per_step": tf_ms / args.steps},
-        "sparse_row_attention": {"tflops": attn["flops"] / (attn["ms"] * 1e-3) / 1e12 if attn["ms"] else 0.0,
-                                 "frac_of_sustained": (attn["flops"] / (attn["ms"] * 1e-3) / 1e12 / sust)
-                                 if attn["ms"] else 0.0, "ms_per_step": attn["ms"] / args.steps},
-        "assemble_kv": {"gbs": asm["bytes"] / (asm["ms"] * 1e-3) / 1e9 if asm["ms"] else 0.0,
-                        "frac_of_hbm": (asm["bytes"] / (asm["ms"] * 1e-3) / 1e9 / pk["hbm"]) if asm["ms"] else 0.0,
-                        "ms_per_step": asm["ms"] / args.steps},
-    }
+    hbm_ops = {"assemble_kv", "lm_head"}
+    kernels = {}
+    for k, v in ops.items():
+        e = {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps}
+        if v["work"] and v["ms"]:
+            rate = v["work"] / (v["ms"] * 1e-3)
+            if k in hbm_ops:
+                e.update(gbs=rate / 1e9, frac_of_hbm=rate / 1e9 / pk["hbm"])
+            elif k == "gemm_3xtf32":
+                e.update(tflops_effective_fp32=rate / 1e12)
+            else:
+                e.update(tflops=rate / 1e12, frac_of_bf16_sustained=rate / 1e12 / sust)
+        kernels[k] = e
+    top = max((k for k in ops if ops[k]["work"]), key=lambda k: ops[k]["ms"])
+    tv = ops[top]
+    if top in hbm_ops:
+        roof = {"bound": "hbm", "achieved": tv["work"] / (tv["ms"] * 1e-3) / 1e9, "peak": pk["hbm"], "unit": "GB/s"}
+    else:
+        roof = {"bound": "tensor", "achieved": tv["work"] / (tv["ms"] * 1e-3) / 1e12, "peak": sust,
+                "unit": "TFLOP/s"}
+    roof.update(kernel=top, frac=roof["achieved"] / roof["peak"], traffic=None,
+                share_of_step=tv["ms"] / args.steps / ttft,
+                peak_source=f"{pk['source']} ({'HBM copy' if roof['bound'] == 'hbm' else 'bf16 sustained'})")
+    stages = None
 
     # ---- full-attention prefill of the same primary on the same GPU -------
     full_ms = None
@@ -371,11 +378,8 @@ def run_ours(args, rank: int, world: int):
         "speedup_vs_full": (full_ms / ttft) if full_ms else None,
         "default_rule": {"window_threshold": 5, "recomputed_rows": len(dflt.plan.indices),
                          "effective_ratio": dflt.plan.effective_ratio},
-        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tcgen05 (selective-recompute projections + MLP)",
-                     "achieved": achieved, "peak": sust, "unit": "TFLOP/s",
-                     "frac": achieved / sust if sust else None, "traffic": None,
-                     "peak_source": f"{pk['source']} bf16 sustained"},
-        "kernels": kernels, "stages": stages,
+        "roofline": roof,
+        "kernels": kernels,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks.summary(), "sweep": sweep or None, "setup_s": setup_s,
     }

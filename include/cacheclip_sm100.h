@@ -217,6 +217,73 @@ int cc_lm_head_argmax(const float* h_row, const float* gain, float eps, int32_t 
 /* Row gather for the residual stream (compaction helpers). */
 int cc_gather_i64(const int64_t* src, const int64_t* idx, int64_t n, int64_t* dst, void* stream);
 
+/* ------------------------------------------------------------------------
+ * (7) Native layer executor — the per-layer loops of selective_forward,
+ *     extend_cache, prefill_full (model.py:506-728) and the scoring model's
+ *     peek_forward (model.py:568-607) as one call each. Weights are described
+ *     by plain pointers (device layouts documented in weights.py).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  const void* w_qkv; const float* b_qkv; int64_t n_qkv;  /* [(Hq+2Hkv)*D, d] */
+  const void* w_o; const float* b_o;                     /* [d, Hq*D]        */
+  const float* attn_norm; const float* mlp_norm;
+  const void* w_up; const float* b_up; int64_t n_up;     /* GLU-interleaved or w_in */
+  const void* w_down; const float* b_down;               /* [d, d_ff]        */
+} cc_layer_weights;
+
+typedef struct {
+  int32_t n_layers, n_heads, n_kv_heads, head_dim, d_model, d_ff;
+  int64_t vocab;
+  int32_t dtype;       /* CC_BF16 (bf16 engine) or CC_F32 (3xTF32 banked engine) */
+  int32_t mlp_gated, act;
+  float norm_eps;
+  const void* embed; const float* final_norm; const void* lm_head; int32_t head_dtype;
+  const cc_layer_weights* layers;  /* host array [n_layers] */
+  const double* inv_freq;          /* host [head_dim/2], tensor_core.py:48-50 */
+} cc_model_desc;
+
+/* Where the QKV epilogue writes K/V and what attention reads, per layer:
+ * pointer(l) = base + l * stride (bytes; stride 0 = one shared buffer). */
+typedef struct {
+  void* k_scatter; int64_t k_scatter_stride;
+  void* v_scatter; int64_t v_scatter_stride;
+  const int64_t* dst_rows;              /* cache row per input row (NULL: identity) */
+  void* k_raw; int64_t k_raw_stride;    /* optional position-free K (precompute)     */
+  const int64_t* raw_rows;
+  const void* attn_k; int64_t attn_k_stride;
+  const void* attn_v; int64_t attn_v_stride;
+} cc_kv_plan;
+
+/* Last-layer scoring (selector.py:157-165): weights workspace
+ * [n_seqs][Hq][Q][max_chunk] fp32, scores[col_off[s] + j]. */
+typedef struct {
+  int64_t col0; const int64_t* chunk_lens; const int64_t* col_off; int64_t max_chunk;
+  float* weights; float* scores;
+} cc_score_spec;
+
+int64_t cc_forward_rows_workspace_bytes(const cc_model_desc* md, int64_t rows);
+int64_t cc_forward_banked_workspace_bytes(const cc_model_desc* md, int64_t rows);
+/* bf16 engine: rows (ids, positions) through every layer; logits of the last
+ * row + argmax when logits != NULL. attn_pairs = sum of visible keys (for the
+ * profiler's algorithmic FLOPs only). The residual stream stays at the start
+ * of the workspace ([rows][d] fp32). */
+int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t rows,
+                    const cc_kv_plan* plan, int64_t n_keys, double attn_pairs, const float* row_factor,
+                    void* workspace, float* logits, int64_t* argmax, void* stream);
+/* fp32 engine over sequences with banks (tables: device cc_bank_seq[n_layers][n_seqs]). */
+int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t rows,
+                      const cc_bank_seq* tables, int32_t n_seqs, int32_t max_new, int64_t max_bank,
+                      void* v_dst, int64_t v_dst_stride, void* k_raw_dst, int64_t k_raw_stride,
+                      const cc_score_spec* score, void* workspace, void* stream);
+
+/* Launch profiler: CUDA events around every launch while enabled; collect
+ * returns (op id, algorithmic work, ms) per launch and clears. op ids:
+ * 0 gemm bf16, 1 gemm 3xTF32, 2 attention (tcgen05), 3 attention (mma.sync),
+ * 4 banked fp32 attention, 5 rmsnorm, 6 KV assembly, 7 select, 8 score
+ * reduction, 9 lm_head, 10 rope table. */
+void cc_profile_enable(int32_t on);
+int64_t cc_profile_collect(int32_t* ops, double* work, float* ms, int64_t cap);
+
 #ifdef __cplusplus
 }
 #endif

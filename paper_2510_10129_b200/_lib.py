@@ -52,6 +52,31 @@ class GemmArgs(ctypes.Structure):
     ]
 
 
+class LayerWeightsDesc(ctypes.Structure):
+    _fields_ = [("w_qkv", vp), ("b_qkv", vp), ("n_qkv", i64), ("w_o", vp), ("b_o", vp),
+                ("attn_norm", vp), ("mlp_norm", vp), ("w_up", vp), ("b_up", vp), ("n_up", i64),
+                ("w_down", vp), ("b_down", vp)]
+
+
+class ModelDesc(ctypes.Structure):
+    _fields_ = [("n_layers", i32), ("n_heads", i32), ("n_kv_heads", i32), ("head_dim", i32),
+                ("d_model", i32), ("d_ff", i32), ("vocab", i64), ("dtype", i32), ("mlp_gated", i32),
+                ("act", i32), ("norm_eps", f32), ("embed", vp), ("final_norm", vp), ("lm_head", vp),
+                ("head_dtype", i32), ("layers", ctypes.POINTER(LayerWeightsDesc)),
+                ("inv_freq", ctypes.POINTER(ctypes.c_double))]
+
+
+class KvPlan(ctypes.Structure):
+    _fields_ = [("k_scatter", vp), ("k_scatter_stride", i64), ("v_scatter", vp), ("v_scatter_stride", i64),
+                ("dst_rows", vp), ("k_raw", vp), ("k_raw_stride", i64), ("raw_rows", vp),
+                ("attn_k", vp), ("attn_k_stride", i64), ("attn_v", vp), ("attn_v_stride", i64)]
+
+
+class ScoreSpec(ctypes.Structure):
+    _fields_ = [("col0", i64), ("chunk_lens", vp), ("col_off", vp), ("max_chunk", i64),
+                ("weights", vp), ("scores", vp)]
+
+
 _SIGS = {
     "cc_abi_version": ([], i32),
     "cc_last_error": ([], ctypes.c_char_p),
@@ -71,7 +96,36 @@ _SIGS = {
     "cc_lm_head_workspace_bytes": ([i64], i64),
     "cc_lm_head_argmax": ([vp, vp, f32, i32, vp, i32, i64, vp, vp, vp, vp], i32),
     "cc_gather_i64": ([vp, vp, i64, vp, vp], i32),
+    "cc_forward_rows_workspace_bytes": ([ctypes.POINTER(ModelDesc), i64], i64),
+    "cc_forward_banked_workspace_bytes": ([ctypes.POINTER(ModelDesc), i64], i64),
+    "cc_forward_rows": ([ctypes.POINTER(ModelDesc), vp, vp, i64, ctypes.POINTER(KvPlan), i64, ctypes.c_double,
+                         vp, vp, vp, vp, vp], i32),
+    "cc_forward_banked": ([ctypes.POINTER(ModelDesc), vp, vp, i64, vp, i32, i32, i64, vp, i64, vp, i64,
+                           ctypes.POINTER(ScoreSpec), vp, vp], i32),
+    "cc_profile_enable": ([i32], None),
+    "cc_profile_collect": ([vp, vp, vp, i64], i64),
 }
+
+PROFILE_OPS = ("gemm_bf16", "gemm_3xtf32", "attention_tcgen05", "attention_mma", "banked_attention_f32",
+               "rmsnorm", "assemble_kv", "select_topk", "score_reduce", "lm_head", "rope_table")
+
+
+def profile_enable(on: bool) -> None:
+    load().cc_profile_enable(1 if on else 0)
+
+
+def profile_collect():
+    """[(op name, algorithmic work, ms)] for every launch since enable; clears."""
+    import numpy as np
+    lib = load()
+    cap = 1 << 16
+    ops = np.zeros(cap, np.int32)
+    work = np.zeros(cap, np.float64)
+    ms = np.zeros(cap, np.float32)
+    n = int(lib.cc_profile_collect(ops.ctypes.data, work.ctypes.data, ms.ctypes.data, cap))
+    n = min(n, cap)
+    return [(PROFILE_OPS[o] if 0 <= o < len(PROFILE_OPS) else f"op{o}", float(w), float(t))
+            for o, w, t in zip(ops[:n], work[:n], ms[:n])]
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
 

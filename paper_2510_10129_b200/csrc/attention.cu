@@ -417,6 +417,7 @@ extern "C" int cc_sparse_row_attention_mma(const void* q, int64_t ldq, const int
   dim3 grid((unsigned)tiles, n_kv_heads);
   const int smem = 2 * 2 * kAttnKeys * head_dim * 2;
   cudaStream_t st = as_stream(stream);
+  ProfScope ps(st, OP_ATTENTION_MMA, 0);
   if (head_dim == 128) {
     static bool set = false;
     if (!set) {
@@ -449,6 +450,7 @@ extern "C" int cc_banked_attention_f32(const cc_bank_seq* seqs_dev, int32_t n_se
                (long long)ncols_cap);
   const int smem =
       (int)((kBankRows * head_dim + kBankRows * ncols_cap + kBankKeys * (head_dim + 1)) * sizeof(float));
+  ProfScope ps(as_stream(stream), OP_BANKED, 0);
   dim3 grid((max_new + kBankRows - 1) / kBankRows, n_q_heads, n_seqs);
   cudaStream_t st = as_stream(stream);
   if (head_dim == 64) {

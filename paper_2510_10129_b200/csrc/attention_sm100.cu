@@ -365,7 +365,7 @@ static int make_kv_map(CUtensorMap* map, const void* base, int64_t n_keys, int h
 template <int D>
 static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64_t m, const void* k_cache,
                      const void* v_cache, int64_t n_keys, int32_t hq, int32_t hkv, float factor,
-                     const float* row_factor, void* out, int64_t ldo, cudaStream_t st) {
+                     const float* row_factor, void* out, int64_t ldo, cudaStream_t st, double flops) {
   CUtensorMap tk, tv;
   int rc = make_kv_map(&tk, k_cache, n_keys, hkv, D);
   if (rc) return rc;
@@ -379,6 +379,7 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64
   const int G = hq / hkv;
   const int n_qtiles = (int)((m * G + kFaRows - 1) / kFaRows);
   dim3 grid(n_qtiles, hkv);
+  ProfScope ps(st, OP_ATTENTION, flops);
   fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
       tk, tv, (const __nv_bfloat16*)q, ldq, positions, m, n_keys, hq, hkv, factor, row_factor,
       (__nv_bfloat16*)out, ldo, n_qtiles);
@@ -389,6 +390,10 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64
 }  // namespace cc
 
 using namespace cc;
+
+// algorithmic work of the next attention launch (set by the executor, which
+// knows sum(pos+1) on the host; 0 when unknown)
+double g_attn_flops = 0.0;
 
 extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions, int64_t m,
                                        const void* k_cache, const void* v_cache, int64_t n_keys, int32_t n_q_heads,
@@ -405,7 +410,7 @@ extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t
   cudaStream_t st = as_stream(stream);
   if (head_dim == 128)
     return fa_launch<128>(q, ldq, positions, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
-                          out, ldo, st);
+                          out, ldo, st, g_attn_flops);
   return fa_launch<64>(q, ldq, positions, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
-                       out, ldo, st);
+                       out, ldo, st, g_attn_flops);
 }

@@ -1,0 +1,259 @@
+// Native layer executor: the per-layer loops of selective_forward /
+// extend_cache / prefill_full (model.py:506-728) and of the scoring model's
+// peek_forward (model.py:568-607), driven from C++ so a 28-layer pass is one
+// C-ABI call instead of ~250 Python-side launches. Every launch goes through
+// the same C-ABI entry points (cc_gemm, cc_sparse_row_attention, ...), so the
+// validation, error codes and the launch profiler are shared.
+#include "cc_common.cuh"
+
+#include <vector>
+
+extern double g_attn_flops;
+
+namespace cc {
+
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct Carve {
+  uint8_t* base;
+  size_t off = 0;
+  template <typename T>
+  T* take(size_t count) {
+    T* p = reinterpret_cast<T*>(base + off);
+    off = align256(off + count * sizeof(T));
+    return p;
+  }
+};
+
+static size_t rows_ws_bytes(const cc_model_desc* md, int64_t R) {
+  const size_t d = md->d_model, qw = (size_t)md->n_heads * md->head_dim, ff = md->d_ff;
+  size_t s = 0;
+  s += align256(R * d * 4);          // h
+  s += align256(R * d * 2);          // x
+  s += align256(R * qw * 2);         // q
+  s += align256(R * qw * 2);         // ctx
+  s += align256(R * ff * 2);         // act
+  s += 2 * align256(R * (md->head_dim / 2) * 4);  // cos, sin
+  s += align256(64);                 // head workspace
+  return s;
+}
+
+static size_t banked_ws_bytes(const cc_model_desc* md, int64_t R) {
+  const size_t d = md->d_model, qw = (size_t)md->n_heads * md->head_dim, kw = (size_t)md->n_kv_heads * md->head_dim,
+               ff = md->d_ff;
+  size_t s = 0;
+  s += align256(R * d * 4);       // h
+  s += align256(R * 3 * d * 4);   // x split
+  s += align256(R * qw * 4);      // q
+  s += align256(R * kw * 4);      // k new
+  s += align256(R * kw * 4);      // v scratch
+  s += align256(R * 3 * qw * 4);  // ctx split
+  s += align256(R * 3 * ff * 4);  // act split
+  s += 2 * align256(R * (md->head_dim / 2) * 4);
+  return s;
+}
+
+static int gemm_call(int kind, int epi, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const void* B,
+                     int64_t ldb, const float* bias, void* C, int64_t ldc, int c_mode, int act, int64_t n_out,
+                     void* stream) {
+  cc_gemm_args a{};
+  a.kind = kind;
+  a.epilogue = epi;
+  a.M = M;
+  a.N = N;
+  a.K = K;
+  a.A = A;
+  a.lda = lda;
+  a.B = B;
+  a.ldb = ldb;
+  a.bias = bias;
+  a.C = C;
+  a.ldc = ldc;
+  a.c_mode = c_mode;
+  a.act = act;
+  a.glu_block = 128;
+  a.n_out = n_out;
+  return cc_gemm(&a, stream);
+}
+
+#define CC_TRY(x)          \
+  do {                     \
+    int rc_ = (x);         \
+    if (rc_) return rc_;   \
+  } while (0)
+
+// RMSNorm -> gate/up (fused activation) -> down + residual
+static int run_mlp(const cc_model_desc* md, const cc_layer_weights& lw, float* h, void* x, void* act, int64_t R,
+                   int kind, int x_mode, void* stream) {
+  const int64_t d = md->d_model, ff = md->d_ff;
+  const int64_t kmul = kind == CC_GEMM_TF32X3 ? 3 : 1;
+  CC_TRY(cc_rmsnorm(h, R, (int)d, d, lw.mlp_norm, md->norm_eps, x, x_mode, stream));
+  if (md->mlp_gated) {
+    CC_TRY(gemm_call(kind, CC_EPI_GLU, R, lw.n_up, d, x, kmul * d, lw.w_up, kmul * d, lw.b_up, act, ff, x_mode,
+                     md->act, ff, stream));
+  } else {
+    CC_TRY(gemm_call(kind, CC_EPI_ACT, R, ff, d, x, kmul * d, lw.w_up, kmul * d, lw.b_up, act, ff, x_mode, md->act, 0,
+                     stream));
+  }
+  return gemm_call(kind, CC_EPI_RESIDUAL, R, d, ff, act, kmul * ff, lw.w_down, kmul * ff, lw.b_down, h, d, CC_F32, 0,
+                   0, stream);
+}
+
+}  // namespace cc
+
+using namespace cc;
+
+extern "C" {
+
+int64_t cc_forward_rows_workspace_bytes(const cc_model_desc* md, int64_t rows) {
+  return (int64_t)rows_ws_bytes(md, rows);
+}
+
+int64_t cc_forward_banked_workspace_bytes(const cc_model_desc* md, int64_t rows) {
+  return (int64_t)banked_ws_bytes(md, rows);
+}
+
+int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t R,
+                    const cc_kv_plan* plan, int64_t n_keys, double attn_pairs, const float* row_factor,
+                    void* workspace, float* logits, int64_t* argmax, void* stream) {
+  CC_CHECK_ARG(md && plan && workspace, CC_ERR_VALUE, "null model / plan / workspace");
+  CC_CHECK_ARG(md->dtype == CC_BF16, CC_ERR_UNSUPPORTED, "cc_forward_rows runs bf16 models");
+  if (R <= 0) return CC_OK;
+  const int64_t d = md->d_model, qw = (int64_t)md->n_heads * md->head_dim;
+  const int64_t kw = (int64_t)md->n_kv_heads * md->head_dim;
+  Carve cv{reinterpret_cast<uint8_t*>(workspace)};
+  float* h = cv.take<float>(R * d);
+  __nv_bfloat16* x = cv.take<__nv_bfloat16>(R * d);
+  __nv_bfloat16* q = cv.take<__nv_bfloat16>(R * qw);
+  __nv_bfloat16* ctx = cv.take<__nv_bfloat16>(R * qw);
+  __nv_bfloat16* act = cv.take<__nv_bfloat16>(R * md->d_ff);
+  float* cs = cv.take<float>(R * (md->head_dim / 2));
+  float* sn = cv.take<float>(R * (md->head_dim / 2));
+  void* hws = cv.take<uint8_t>(64);
+  CC_TRY(cc_rope_table(positions, R, md->inv_freq, md->head_dim, cs, sn, stream));
+  const float factor = (float)(1.0 / sqrt((double)md->head_dim));  // np.float32(1/sqrt(d))
+  auto lp = [](const void* base, int64_t stride, int l) -> void* {
+    return base ? (void*)((const uint8_t*)base + stride * l) : nullptr;
+  };
+  for (int l = 0; l < md->n_layers; ++l) {
+    const cc_layer_weights& lw = md->layers[l];
+    if (l == 0)
+      CC_TRY(cc_embed_rmsnorm(ids, R, md->embed, CC_BF16, md->vocab, (int)d, h, lw.attn_norm, md->norm_eps, x,
+                              CC_BF16, stream));
+    else
+      CC_TRY(cc_rmsnorm(h, R, (int)d, d, lw.attn_norm, md->norm_eps, x, CC_BF16, stream));
+    cc_gemm_args a{};
+    a.kind = CC_GEMM_BF16;
+    a.epilogue = CC_EPI_QKV_ROPE;
+    a.M = R;
+    a.N = lw.n_qkv;
+    a.K = d;
+    a.A = x;
+    a.lda = d;
+    a.B = lw.w_qkv;
+    a.ldb = d;
+    a.bias = lw.b_qkv;
+    a.n_q_heads = md->n_heads;
+    a.n_kv_heads = md->n_kv_heads;
+    a.head_dim = md->head_dim;
+    a.rope_cos = cs;
+    a.rope_sin = sn;
+    a.q_out = q;
+    a.ldq = qw;
+    a.q_mode = CC_BF16;
+    a.k_cache = lp(plan->k_scatter, plan->k_scatter_stride, l);
+    a.v_cache = lp(plan->v_scatter, plan->v_scatter_stride, l);
+    a.cache_dtype = CC_BF16;
+    a.dst_rows = plan->dst_rows;
+    a.k_raw = lp(plan->k_raw, plan->k_raw_stride, l);
+    a.raw_rows = plan->raw_rows;
+    CC_TRY(cc_gemm(&a, stream));
+    g_attn_flops = 4.0 * md->n_heads * md->head_dim * attn_pairs;
+    CC_TRY(cc_sparse_row_attention(q, qw, positions, R, lp(plan->attn_k, plan->attn_k_stride, l),
+                                   lp(plan->attn_v, plan->attn_v_stride, l), n_keys, md->n_heads, md->n_kv_heads,
+                                   md->head_dim, factor, row_factor, ctx, qw, stream));
+    g_attn_flops = 0.0;
+    CC_TRY(gemm_call(CC_GEMM_BF16, CC_EPI_RESIDUAL, R, d, qw, ctx, qw, lw.w_o, qw, lw.b_o, h, d, CC_F32, 0, 0,
+                     stream));
+    CC_TRY(run_mlp(md, lw, h, x, act, R, CC_GEMM_BF16, CC_BF16, stream));
+  }
+  (void)kw;
+  if (logits)
+    CC_TRY(cc_lm_head_argmax(h + (R - 1) * d, md->final_norm, md->norm_eps, (int)d, md->lm_head, md->head_dtype,
+                             md->vocab, logits, argmax, hws, stream));
+  return CC_OK;
+}
+
+int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t R,
+                      const cc_bank_seq* tables, int32_t n_seqs, int32_t max_new, int64_t max_bank, void* v_dst,
+                      int64_t v_dst_stride, void* k_raw_dst, int64_t k_raw_stride, const cc_score_spec* score,
+                      void* workspace, void* stream) {
+  CC_CHECK_ARG(md && tables && workspace, CC_ERR_VALUE, "null model / tables / workspace");
+  CC_CHECK_ARG(md->dtype == CC_F32, CC_ERR_UNSUPPORTED, "cc_forward_banked runs fp32 (3xTF32) models");
+  if (R <= 0) return CC_OK;
+  const int64_t d = md->d_model, qw = (int64_t)md->n_heads * md->head_dim;
+  const int64_t kw = (int64_t)md->n_kv_heads * md->head_dim;
+  Carve cv{reinterpret_cast<uint8_t*>(workspace)};
+  float* h = cv.take<float>(R * d);
+  float* x = cv.take<float>(R * 3 * d);
+  float* q = cv.take<float>(R * qw);
+  float* k_new = cv.take<float>(R * kw);
+  float* v_scr = cv.take<float>(R * kw);
+  float* ctx = cv.take<float>(R * 3 * qw);
+  float* act = cv.take<float>(R * 3 * md->d_ff);
+  float* cs = cv.take<float>(R * (md->head_dim / 2));
+  float* sn = cv.take<float>(R * (md->head_dim / 2));
+  CC_TRY(cc_rope_table(positions, R, md->inv_freq, md->head_dim, cs, sn, stream));
+  const float factor = (float)(1.0 / sqrt((double)md->head_dim));  // np.float32(1/sqrt(d))
+  const int L = md->n_layers;
+  for (int l = 0; l < L; ++l) {
+    const cc_layer_weights& lw = md->layers[l];
+    if (l == 0)
+      CC_TRY(cc_embed_rmsnorm(ids, R, md->embed, CC_F32, md->vocab, (int)d, h, lw.attn_norm, md->norm_eps, x,
+                              CC_F32_SPLIT3, stream));
+    else
+      CC_TRY(cc_rmsnorm(h, R, (int)d, d, lw.attn_norm, md->norm_eps, x, CC_F32_SPLIT3, stream));
+    const bool last_scoring = score && l == L - 1;
+    float* vd = v_dst ? (float*)((uint8_t*)v_dst + v_dst_stride * l) : v_scr;
+    cc_gemm_args a{};
+    a.kind = CC_GEMM_TF32X3;
+    a.epilogue = CC_EPI_QKV_ROPE;
+    a.M = R;
+    a.N = last_scoring ? (int64_t)(md->n_heads + md->n_kv_heads) * md->head_dim : lw.n_qkv;
+    a.K = d;
+    a.A = x;
+    a.lda = 3 * d;
+    a.B = lw.w_qkv;
+    a.ldb = 3 * d;
+    a.bias = lw.b_qkv;
+    a.n_q_heads = md->n_heads;
+    a.n_kv_heads = md->n_kv_heads;
+    a.head_dim = md->head_dim;
+    a.rope_cos = cs;
+    a.rope_sin = sn;
+    a.q_out = q;
+    a.ldq = qw;
+    a.q_mode = CC_F32;
+    a.k_cache = k_new;
+    a.v_cache = vd;
+    a.cache_dtype = CC_F32;
+    a.k_raw = k_raw_dst ? (void*)((uint8_t*)k_raw_dst + k_raw_stride * l) : nullptr;
+    CC_TRY(cc_gemm(&a, stream));
+    const cc_bank_seq* tl = tables + (int64_t)l * n_seqs;
+    if (last_scoring) {
+      CC_TRY(cc_banked_attention_f32(tl, n_seqs, max_new, max_bank, q, k_new, vd, md->n_heads, md->n_kv_heads,
+                                     md->head_dim, factor, ctx, CC_F32_SPLIT3, score->weights, score->col0,
+                                     score->max_chunk, stream));
+      return cc_reduce_scores(score->weights, n_seqs, md->n_heads, max_new, score->max_chunk, score->chunk_lens,
+                              score->col_off, score->max_chunk, score->scores, stream);
+    }
+    CC_TRY(cc_banked_attention_f32(tl, n_seqs, max_new, max_bank, q, k_new, vd, md->n_heads, md->n_kv_heads,
+                                   md->head_dim, factor, ctx, CC_F32_SPLIT3, nullptr, 0, 0, stream));
+    CC_TRY(gemm_call(CC_GEMM_TF32X3, CC_EPI_RESIDUAL, R, d, qw, ctx, 3 * qw, lw.w_o, 3 * qw, lw.b_o, h, d, CC_F32,
+                     0, 0, stream));
+    CC_TRY(run_mlp(md, lw, h, x, act, R, CC_GEMM_TF32X3, CC_F32_SPLIT3, stream));
+  }
+  return CC_OK;
+}
+
+}  // extern "C"

@@ -371,6 +371,7 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   const int num_kb = (int)((kop + Cfg::BK - 1) / Cfg::BK);
   const int tiles = num_m * num_n;
   const int grid = tiles < num_sms() ? tiles : num_sms();
+  ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
   gemm_kernel<BN, kTF32><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb);
   CC_LAUNCH_CHECK("gemm");
   return CC_OK;

@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <vector>
 
 namespace cc {
 
@@ -25,6 +26,42 @@ int fail(int code, const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
   return code;
+}
+
+// ---- launch profiler ----------------------------------------------------
+struct ProfRec {
+  int op;
+  double work;
+  cudaEvent_t e0, e1;
+};
+static std::mutex g_prof_mu;
+static bool g_prof_on = false;
+static std::vector<ProfRec> g_prof;
+static std::vector<cudaEvent_t> g_event_pool;
+
+static cudaEvent_t pool_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+bool prof_enabled() { return g_prof_on; }
+
+void prof_record(cudaStream_t st, int op, double work, cudaEvent_t* e0, bool begin) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (begin) {
+    *e0 = pool_event();
+    cudaEventRecord(*e0, st);
+  } else {
+    cudaEvent_t e1 = pool_event();
+    cudaEventRecord(e1, st);
+    g_prof.push_back({op, work, *e0, e1});
+  }
 }
 
 int num_sms() {
@@ -269,6 +306,32 @@ using namespace cc;
 extern "C" {
 
 int cc_abi_version(void) { return CC_ABI_VERSION; }
+
+void cc_profile_enable(int32_t on) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = on != 0;
+}
+
+int64_t cc_profile_collect(int32_t* ops, double* work, float* ms, int64_t cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  const int64_t n = (int64_t)g_prof.size();
+  if (n) cudaEventSynchronize(g_prof.back().e1);
+  int64_t k = 0;
+  for (auto& r : g_prof) {
+    if (k < cap) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.e0, r.e1);
+      ops[k] = r.op;
+      work[k] = r.work;
+      ms[k] = t;
+    }
+    ++k;
+    g_event_pool.push_back(r.e0);
+    g_event_pool.push_back(r.e1);
+  }
+  g_prof.clear();
+  return n;
+}
 const char* cc_last_error(void) { return g_err; }
 
 int cc_device_check(int dev) {
@@ -297,6 +360,7 @@ int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_
   CC_CHECK_ARG(dst_k && (reinterpret_cast<uintptr_t>(dst_k) | reinterpret_cast<uintptr_t>(dst_v)) % 16 == 0,
                CC_ERR_UNSUPPORTED, "destination not 16-byte aligned");
   const int64_t threads = n_dst_rows * (int64_t)(kv_heads * head_dim / V);
+  ProfScope ps(as_stream(stream), OP_ASSEMBLE, 2.0 * 2 * n_dst_rows * n_layers * kv_heads * head_dim * (dtype == CC_BF16 ? 2 : 4));
   const int bs = 256;
   const int64_t grid = (threads + bs - 1) / bs;
   if (dtype == CC_BF16) {
@@ -323,6 +387,7 @@ int cc_rope_table(const int64_t* positions, int64_t n, const double* inv_freq_ho
   if (n <= 0) return CC_OK;
   const int half = head_dim / 2;
   const int64_t total = n * half;
+  ProfScope ps(as_stream(stream), OP_ROPE, 0);
   rope_table_kernel<<<(total + 255) / 256, 256, 0, as_stream(stream)>>>(positions, n, inv, half, cos_out, sin_out);
   CC_LAUNCH_CHECK("rope_table");
   return CC_OK;
@@ -334,6 +399,7 @@ int cc_embed_rmsnorm(const int64_t* ids, int64_t rows, const void* embed, int32_
   (void)vocab;
   CC_CHECK_ARG(d > 0 && d <= kNormThreads * kNormMaxPer, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
   if (rows <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_NORM, 0);
   embed_rmsnorm_kernel<<<rows, kNormThreads, 0, as_stream(stream)>>>(ids, embed, embed_dtype, d, h_out, gain, eps,
                                                                        x_out, x_mode, nullptr, 0);
   CC_LAUNCH_CHECK("embed_rmsnorm");
@@ -344,6 +410,7 @@ int cc_rmsnorm(const float* h, int64_t rows, int32_t d, int64_t ld_h, const floa
                int32_t x_mode, void* stream) {
   CC_CHECK_ARG(d > 0 && d <= kNormThreads * kNormMaxPer, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
   if (rows <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_NORM, 0);
   embed_rmsnorm_kernel<<<rows, kNormThreads, 0, as_stream(stream)>>>(nullptr, nullptr, 0, d, nullptr, gain, eps,
                                                                        x_out, x_mode, h, ld_h);
   CC_LAUNCH_CHECK("rmsnorm");

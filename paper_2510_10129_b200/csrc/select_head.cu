@@ -270,6 +270,7 @@ int cc_reduce_scores(const float* weights, int32_t n_seqs, int32_t n_heads, int3
   if (n_seqs <= 0 || max_chunk <= 0) return CC_OK;
   CC_CHECK_ARG(n_heads > 0 && n_query > 0, CC_ERR_VALUE, "query must be non-empty");
   dim3 grid((unsigned)((max_chunk + 255) / 256), n_seqs);
+  ProfScope ps(as_stream(stream), OP_SCORES, 0);
   reduce_scores_kernel<<<grid, 256, 0, as_stream(stream)>>>(weights, n_heads, n_query, w_ld, chunk_lens_dev,
                                                              col_offset_dev, scores);
   CC_LAUNCH_CHECK("reduce_scores");
@@ -294,6 +295,7 @@ int cc_select_topk_windows(const float* scores, int64_t n, const int64_t* chunk_
   int64_t* tok_off = reinterpret_cast<int64_t*>(ws + ((n + 15) / 16) * 16);
   int64_t* win_off = tok_off + (n_chunks + 1);
   int32_t* win_take = reinterpret_cast<int32_t*>(win_off + (n_chunks + 1));
+  ProfScope ps(as_stream(stream), OP_SELECT, 0);
   select_topk_windows_kernel<<<1, kSelThreads, 0, as_stream(stream)>>>(
       scores, n, chunk_lens_dev, n_chunks, n_windows, budget, window_len, threshold, expand, index_offset,
       out_indices, out_count, win_selected, win_kept, cand, tok_off, win_off, win_take);
@@ -312,6 +314,7 @@ int cc_lm_head_argmax(const float* h_row, const float* gain, float eps, int32_t 
   CC_CHECK_ARG(d > 0 && d % 8 == 0 && d <= 16384, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
   CC_CHECK_ARG(vocab > 0 && vocab < 0xFFFFFFFFll, CC_ERR_DIMENSION, "vocab %lld", (long long)vocab);
   cudaStream_t st = as_stream(stream);
+  ProfScope ps(st, OP_HEAD, 2.0 * (double)vocab * d * (dtype == CC_BF16 ? 2 : 4));
   unsigned long long* best = reinterpret_cast<unsigned long long*>(workspace);
   cudaMemsetAsync(best, 0, sizeof(unsigned long long), st);
   const int rows_per_block = kHeadThreads / 32;

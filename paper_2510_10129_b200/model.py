@@ -19,7 +19,7 @@ from .config import ModelConfig
 from .errors import DimensionError
 from .flops import PipelineTrace, trace_layer
 from .kv_store import ChunkCache, MergedCache, host_to_device
-from .runtime import bank_tables, final_logits, forward_banked, forward_rows
+from .runtime import KvPlan, bank_tables, final_logits, forward_banked, forward_rows
 from .weights import Model, from_params, init_model  # noqa: F401  (re-export)
 
 
@@ -82,12 +82,12 @@ def _dense(model: Model, ids: torch.Tensor, want_logits: bool):
     V = torch.empty_like(K)
     pos = _positions(0, n, dev)
     if c.dtype == "bf16":
-        bank = torch.empty(n, c.kv_heads, c.d_head, dtype=torch.bfloat16, device=dev)
-        res = forward_rows(model, ids, pos, lambda l: (bank, V[l], None, K[l], None, bank, V[l]), n,
-                           want_logits=want_logits, pairs=visible_pairs(n))
+        bank = torch.empty(n, c.kv_heads, c.d_head, dtype=torch.bfloat16, device=dev)  # rotated K, reused per layer
+        plan = KvPlan(k_scatter=bank, v_scatter=V, attn_k=bank, attn_v=V, k_raw=K)
+        res = forward_rows(model, ids, pos, plan, n, want_logits=want_logits, pairs=visible_pairs(n))
         return K, V, res.logits, res.argmax
     tables = bank_tables(c.n_layers, [(None, None, 0, 0, n)], dev)
-    h = forward_banked(model, ids, pos, tables, 1, n, 0, v_dst=lambda l: V[l], k_raw_dst=lambda l: K[l])
+    h = forward_banked(model, ids, pos, tables, 1, n, 0, v_dst=V, k_raw_dst=K)
     logits = argmax = None
     if want_logits:
         logits, argmax = final_logits(model, h[n - 1])
@@ -185,8 +185,9 @@ def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | No
     rf = _row_factor(model, knobs, nq, m, dev)
     ks, vs = cache.k_store, cache.v_store
     pairs = (int(np.sum(sel_idx + 1)) if m else 0) + (visible_pairs(nq, base) if nq else 0)
-    res = forward_rows(model, ids, pos, lambda l: (ks[l], vs[l], pos, None, None, ks[l], vs[l]), base + nq,
-                       row_factor=rf, want_logits=want_logits and nq > 0, pairs=pairs)
+    plan = KvPlan(k_scatter=ks, v_scatter=vs, attn_k=ks, attn_v=vs, dst_rows=pos)
+    res = forward_rows(model, ids, pos, plan, base + nq, row_factor=rf, want_logits=want_logits and nq > 0,
+                       pairs=pairs)
     if trace is not None:
         for _ in range(c.n_layers):
             if m:

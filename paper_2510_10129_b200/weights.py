@@ -13,6 +13,7 @@ bf16 models store bf16 matrices; fp32 models store the 3xTF32 weight split
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 import json
 from dataclasses import dataclass, field
@@ -25,6 +26,10 @@ from .config import ModelConfig, expected_tensors
 from .errors import MissingTensorError, TensorShapeError, WeightFormatError
 
 GLU_BLOCK = 128
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
 
 
 @dataclass
@@ -52,6 +57,31 @@ class Model:
     lm_head: torch.Tensor | None
     fingerprint: str = ""
     device: torch.device = field(default_factory=lambda: torch.device("cuda"))
+    _desc: object = field(default=None, repr=False, compare=False)
+
+    def desc(self):
+        """C-ABI description (cc_model_desc) of this model's device weights;
+        built once, kept alive with the model."""
+        if self._desc is None:
+            c = self.config
+            arr = (_lib.LayerWeightsDesc * c.n_layers)()
+            for i, lw in enumerate(self.layers):
+                arr[i] = _lib.LayerWeightsDesc(
+                    lw.w_qkv.data_ptr(), _ptr(lw.b_qkv), lw.w_qkv.shape[0], lw.w_o.data_ptr(), _ptr(lw.b_o),
+                    lw.attn_norm.data_ptr(), lw.mlp_norm.data_ptr(), lw.w_up.data_ptr(), _ptr(lw.b_up),
+                    lw.w_up.shape[0], lw.w_down.data_ptr(), _ptr(lw.b_down))
+            inv = (ctypes.c_double * (c.d_head // 2))(*c.rope.inv_freq.tolist())
+            act = _lib.CC_ACT_SILU if c.activation == "silu" else _lib.CC_ACT_GELU_TANH
+            head = self.lm_head
+            d = _lib.ModelDesc(
+                c.n_layers, c.n_heads, c.kv_heads, c.d_head, c.d_model, c.d_ff, c.vocab_size,
+                _lib.CC_BF16 if c.dtype == "bf16" else _lib.CC_F32, int(c.mlp_gated), act, c.norm_eps,
+                self.embed.data_ptr(), self.final_norm.data_ptr(), _ptr(head),
+                _lib.CC_BF16 if head is not None and head.dtype == torch.bfloat16 else _lib.CC_F32,
+                ctypes.cast(arr, ctypes.POINTER(_lib.LayerWeightsDesc)),
+                ctypes.cast(inv, ctypes.POINTER(ctypes.c_double)))
+            self._desc = (d, arr, inv)
+        return self._desc[0]
 
     @property
     def wdtype(self) -> torch.dtype:

@@ -241,11 +241,11 @@ def test_banked_attention_f32_matches_reference_math():
     out = torch.empty(S * Q, Hq * D, device=DEV)
     factor = float(np.float32(1 / math.sqrt(D)))
     maxb = max(b.shape[1] for b in banks)
-    L.call("cc_banked_attention_f32", tables[0].data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
+    L.call("cc_banked_attention_f32", tables.data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
            vd.data_ptr(), Hq, Hkv, D, factor, out.data_ptr(), L.CC_F32, None, 0, 0,
            torch.cuda.current_stream().cuda_stream)
     w = torch.zeros(S, Hq, Q, maxb, device=DEV)
-    L.call("cc_banked_attention_f32", tables[0].data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
+    L.call("cc_banked_attention_f32", tables.data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
            vd.data_ptr(), Hq, Hkv, D, factor, out.data_ptr(), L.CC_F32, w.data_ptr(), 0, maxb,
            torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
