@@ -250,11 +250,11 @@ def run_ours(args, rank: int, world: int):
     # per-kernel rooflines from the in-library CUDA-event profiler (timed steps)
     recs = _lib.profile_collect()
     ops: dict = {}
-    for op, work, ms in recs:
+    for op, wk, ms in recs:
         d = ops.setdefault(op, {"launches": 0, "ms": 0.0, "work": 0.0})
         d["launches"] += 1
         d["ms"] += ms
-        d["work"] += work
+        d["work"] += wk
     launches = sum(v["launches"] * (2 if k == "lm_head" else 1) for k, v in ops.items())
     sust = pk["bf16_sustained"] or pk["bf16"]
     hbm_ops = {"assemble_kv", "lm_head"}
