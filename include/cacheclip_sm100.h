@@ -216,6 +216,12 @@ int cc_lm_head_argmax(const float* h_row, const float* gain, float eps, int32_t 
 
 /* Row gather for the residual stream (compaction helpers). */
 int cc_gather_i64(const int64_t* src, const int64_t* idx, int64_t n, int64_t* dst, void* stream);
+/* Rows of the fused selective_forward + extend_cache pass, built on device
+ * from the selection kernel's output (no host round trip of the indices):
+ * r < m: pos = sel[r], id = token_ids[sel[r]]; m <= r < m+nq: pos = base+r-m,
+ * id = query_ids[r-m]. */
+int cc_build_rows(const int64_t* sel, int64_t m, const int64_t* token_ids, const int64_t* query_ids, int64_t nq,
+                  int64_t base, int64_t* ids_out, int64_t* pos_out, void* stream);
 
 /* ------------------------------------------------------------------------
  * (7) Native layer executor — the per-layer loops of selective_forward,

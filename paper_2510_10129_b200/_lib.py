@@ -96,6 +96,7 @@ _SIGS = {
     "cc_lm_head_workspace_bytes": ([i64], i64),
     "cc_lm_head_argmax": ([vp, vp, f32, i32, vp, i32, i64, vp, vp, vp, vp], i32),
     "cc_gather_i64": ([vp, vp, i64, vp, vp], i32),
+    "cc_build_rows": ([vp, i64, vp, vp, i64, i64, vp, vp, vp], i32),
     "cc_forward_rows_workspace_bytes": ([ctypes.POINTER(ModelDesc), i64], i64),
     "cc_forward_banked_workspace_bytes": ([ctypes.POINTER(ModelDesc), i64], i64),
     "cc_forward_rows": ([ctypes.POINTER(ModelDesc), vp, vp, i64, ctypes.POINTER(KvPlan), i64, ctypes.c_double,

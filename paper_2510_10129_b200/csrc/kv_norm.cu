@@ -293,6 +293,22 @@ __global__ void convert_kernel(const float* __restrict__ src, int64_t rows, int6
   }
 }
 
+// Rows of the fused recompute+query pass: selected rows (position = merged
+// row, id = merged token id) followed by the query rows appended at `base`.
+__global__ void build_rows_kernel(const int64_t* __restrict__ sel, int64_t m, const int64_t* __restrict__ token_ids,
+                                  const int64_t* __restrict__ query_ids, int64_t nq, int64_t base,
+                                  int64_t* __restrict__ ids_out, int64_t* __restrict__ pos_out) {
+  int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m) {
+    const int64_t p = sel[r];
+    pos_out[r] = p;
+    ids_out[r] = token_ids[p];
+  } else if (r < m + nq) {
+    pos_out[r] = base + (r - m);
+    ids_out[r] = query_ids[r - m];
+  }
+}
+
 __global__ void gather_i64_kernel(const int64_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
                                   int64_t* __restrict__ dst) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -423,6 +439,16 @@ int cc_convert_matrix(const float* src, int64_t rows, int64_t cols, void* dst, i
   if (n <= 0) return CC_OK;
   convert_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(src, rows, cols, dst, dst_mode, split_weight);
   CC_LAUNCH_CHECK("convert_matrix");
+  return CC_OK;
+}
+
+int cc_build_rows(const int64_t* sel, int64_t m, const int64_t* token_ids, const int64_t* query_ids, int64_t nq,
+                  int64_t base, int64_t* ids_out, int64_t* pos_out, void* stream) {
+  const int64_t n = m + nq;
+  if (n <= 0) return CC_OK;
+  build_rows_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(sel, m, token_ids, query_ids, nq, base, ids_out,
+                                                                     pos_out);
+  CC_LAUNCH_CHECK("build_rows");
   return CC_OK;
 }
 

@@ -314,7 +314,7 @@ int cc_lm_head_argmax(const float* h_row, const float* gain, float eps, int32_t 
   CC_CHECK_ARG(d > 0 && d % 8 == 0 && d <= 16384, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
   CC_CHECK_ARG(vocab > 0 && vocab < 0xFFFFFFFFll, CC_ERR_DIMENSION, "vocab %lld", (long long)vocab);
   cudaStream_t st = as_stream(stream);
-  ProfScope ps(st, OP_HEAD, 2.0 * (double)vocab * d * (dtype == CC_BF16 ? 2 : 4));
+  ProfScope ps(st, OP_HEAD, (double)vocab * d * (dtype == CC_BF16 ? 2 : 4));  // weight bytes read
   unsigned long long* best = reinterpret_cast<unsigned long long*>(workspace);
   cudaMemsetAsync(best, 0, sizeof(unsigned long long), st);
   const int rows_per_block = kHeadThreads / 32;

@@ -126,10 +126,10 @@ def _dtype_code(dt: torch.dtype) -> int:
 
 def _segments(spec) -> np.ndarray:
     """[(chunk, src_row0, dst_row0, n_rows)] -> packed cc_kv_segment bytes."""
-    arr = (_lib.KvSegment * len(spec))()
+    arr = np.empty((len(spec), 6), dtype=np.int64)  # == cc_kv_segment (6 x 8 bytes)
     for i, (c, s0, d0, n) in enumerate(spec):
-        arr[i] = _lib.KvSegment(c.k.data_ptr(), c.v.data_ptr(), c.n_rows, s0, d0, n)
-    return np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+        arr[i] = (c.k.data_ptr(), c.v.data_ptr(), c.n_rows, s0, d0, n)
+    return arr.view(np.uint8).reshape(-1)
 
 
 @dataclass(frozen=True)
@@ -160,12 +160,38 @@ class MergedCache:
         self._n_rows = int(n_rows)
         self.token_ids = list(token_ids)
         self.layout = layout
-        self.source = list(source)
+        # source may be None: derived lazily from the layout (merge order)
+        self._source = None if source is None else list(source)
         self.tokenizer_id = tokenizer_id
         self.model_fingerprint = model_fingerprint
         self.recomputed_rows = tuple(recomputed_rows)
-        if self._n_rows != len(self.token_ids) or self._n_rows != len(self.source):
+        self._ids_dev = None
+        if self._n_rows != len(self.token_ids) or (self._source is not None and self._n_rows != len(self._source)):
             raise CacheConsistencyError("rows, token ids, and source map disagree")
+
+    @property
+    def source(self) -> list[tuple[int, int]]:
+        """(chunk, row) per merged row, (-1, i) for appended rows (kv_store.py:227-233)."""
+        if self._source is None:
+            lay = self.layout
+            src = [(0, r) for r in range(lay.sink_len)]
+            for ci, n in enumerate(lay.chunk_lens):
+                src.extend((ci, lay.sink_len + j) for j in range(n))
+            src.extend((-1, i) for i in range(lay.total, self._n_rows))
+            self._source = src
+        return self._source
+
+    @source.setter
+    def source(self, value) -> None:
+        self._source = list(value)
+
+    def token_ids_device(self) -> torch.Tensor:
+        """Device copy of token_ids (uploaded once, extended in place on append)."""
+        if self._ids_dev is None or self._ids_dev.numel() < self._n_rows:
+            buf = torch.empty(max(self.capacity, self._n_rows), dtype=torch.int64, device=self.k_store.device)
+            buf[: self._n_rows].copy_(host_to_device(np.asarray(self.token_ids, dtype=np.int64), buf.device))
+            self._ids_dev = buf
+        return self._ids_dev
 
     @property
     def n_rows(self) -> int:
@@ -202,15 +228,21 @@ class MergedCache:
             new[:, : self._n_rows].copy_(old[:, : self._n_rows])
             setattr(self, name, new)
 
-    def _append_rows(self, token_ids) -> None:
+    def _append_rows(self, token_ids, ids_dev: torch.Tensor | None = None) -> None:
         base = self._n_rows
         self.token_ids.extend(int(t) for t in token_ids)
-        self.source.extend((-1, base + i) for i in range(len(token_ids)))
+        if self._source is not None:
+            self._source.extend((-1, base + i) for i in range(len(token_ids)))
         self._n_rows += len(token_ids)
+        if self._ids_dev is not None:
+            if ids_dev is not None and self._ids_dev.numel() >= self._n_rows:
+                self._ids_dev[base:self._n_rows].copy_(ids_dev)
+            else:
+                self._ids_dev = None
 
     def copy(self) -> "MergedCache":
         return MergedCache(self.k_store.clone(), self.v_store.clone(), self._n_rows, self.token_ids,
-                           self.layout, self.source, self.tokenizer_id, self.model_fingerprint,
+                           self.layout, self._source, self.tokenizer_id, self.model_fingerprint,
                            self.recomputed_rows)
 
 
@@ -247,12 +279,10 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
     total = sink + sum(lens)
     cap = max(total, capacity or 0)
     token_ids = list(prefix_ids)
-    source: list[tuple[int, int]] = [(0, r) for r in range(sink)]
     spec = []
     dst = 0
     for ci, c in enumerate(chunks):
-        token_ids.extend(c.chunk_ids)
-        source.extend((ci, sink + j) for j in range(c.chunk_len))
+        token_ids.extend(c.token_ids[sink:])
         s0 = 0 if ci == 0 else sink
         n = c.n_rows - s0
         if n:
@@ -270,5 +300,6 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
     if trace is not None:
         for _ in range(L):
             trace.rope("merge_overhead", total * H, D)
-    return MergedCache(k_store, v_store, total, token_ids, MergeLayout(sink, lens), source,
+    # source map is derived lazily from the layout (MergedCache.source)
+    return MergedCache(k_store, v_store, total, token_ids, MergeLayout(sink, lens), None,
                        first.tokenizer_id, first.model_fingerprint)

@@ -38,6 +38,10 @@ def _ids_tensor(model: Model, token_ids: Sequence[int]) -> torch.Tensor:
     return host_to_device(ids, model.device)
 
 
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
 def _positions(start: int, n: int, device) -> torch.Tensor:
     return torch.arange(start, start + n, dtype=torch.int64, device=device)
 
@@ -164,24 +168,24 @@ def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | No
     m = 0 if sel_idx is None else int(sel_idx.size)
     nq = 0 if query_ids is None else len(query_ids)
     base = cache.n_rows
+    R = m + nq
+    if R == 0:
+        return None, None
     cache.ensure_capacity(base + nq)
-    parts_ids, parts_pos = [], []
-    if m:
-        tok = np.asarray(cache.token_ids, dtype=np.int64)[sel_idx]
-        parts_ids.append(tok)
-        parts_pos.append(sel_idx.astype(np.int64))
+    q_dev = None
     if nq:
         q = np.asarray(list(query_ids), dtype=np.int64)
         if q.min() < 0 or q.max() >= c.vocab_size:
             raise ValueError(f"token id outside vocab of size {c.vocab_size}")
-        parts_ids.append(q)
-        parts_pos.append(np.arange(base, base + nq, dtype=np.int64))
-    if not parts_ids:
-        return None, None
-    host = np.concatenate(parts_ids + parts_pos)
-    dev_buf = host_to_device(host, dev)
-    R = m + nq
-    ids, pos = dev_buf[:R], dev_buf[R:]
+        q_dev = host_to_device(q, dev)
+    if m and sel_idx_dev is None:
+        sel_idx_dev = host_to_device(np.ascontiguousarray(sel_idx, dtype=np.int64), dev)
+    # rows assembled on device: selected rows (id gathered from the merged ids)
+    # then the query rows at base.. (cc_build_rows)
+    rows = torch.empty(2, R, dtype=torch.int64, device=dev)
+    ids, pos = rows[0], rows[1]
+    _lib.call("cc_build_rows", _p(sel_idx_dev), m, cache.token_ids_device().data_ptr() if m else None, _p(q_dev),
+              nq, base, ids.data_ptr(), pos.data_ptr(), torch.cuda.current_stream().cuda_stream)
     rf = _row_factor(model, knobs, nq, m, dev)
     ks, vs = cache.k_store, cache.v_store
     pairs = (int(np.sum(sel_idx + 1)) if m else 0) + (visible_pairs(nq, base) if nq else 0)
@@ -198,9 +202,9 @@ def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | No
         if nq and want_logits:
             trace.matmul(query_stage, 1, c.d_model, c.vocab_size)
     if append and nq:
-        cache._append_rows(query_ids)
+        cache._append_rows(query_ids, q_dev)
     if m:
-        cache.recomputed_rows = tuple(int(i) for i in sel_idx)
+        cache.recomputed_rows = tuple(np.asarray(sel_idx, dtype=np.int64).tolist())
     return res.logits, res.argmax
 
 

@@ -180,11 +180,14 @@ def bank_tables(layers: int, seqs: list[tuple], device) -> torch.Tensor:
     """seqs: [(k [L,n,H,D] or None, v or None, n_bank, row0, n_new)] -> device
     cc_bank_seq[layers][len(seqs)] (single pinned H2D copy)."""
     n = len(seqs)
-    arr = (_lib.BankSeq * (n * layers))()
-    for li in range(layers):
-        for si, (k, v, nb, row0, nn) in enumerate(seqs):
-            kp = k[li].data_ptr() if k is not None else 0
-            vp = v[li].data_ptr() if v is not None else 0
-            arr[li * n + si] = _lib.BankSeq(kp, vp, nb, row0, nn)
-    raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
-    return torch.from_numpy(raw).pin_memory().to(device, non_blocking=True)
+    per = np.empty((n, 5), dtype=np.int64)     # (k base, v base, n_bank, row0, n_new)
+    stride = np.zeros((n, 2), dtype=np.int64)  # layer strides of k, v in bytes
+    for si, (k, v, nb, row0, nn) in enumerate(seqs):
+        per[si] = (k.data_ptr() if k is not None else 0, v.data_ptr() if v is not None else 0, nb, row0, nn)
+        if k is not None:
+            stride[si] = (k.stride(0) * k.element_size(), v.stride(0) * v.element_size())
+    arr = np.repeat(per[None], layers, axis=0)  # [L, S, 5] == cc_bank_seq[L][S]
+    lidx = np.arange(layers, dtype=np.int64)[:, None]
+    arr[:, :, 0] += lidx * stride[None, :, 0] * (per[None, :, 0] != 0)
+    arr[:, :, 1] += lidx * stride[None, :, 1] * (per[None, :, 1] != 0)
+    return torch.from_numpy(arr.reshape(-1).view(np.uint8)).pin_memory().to(device, non_blocking=True)

@@ -155,14 +155,45 @@ def top_candidates(scores, budget: int) -> np.ndarray:
 
 def select_tokens(scores: ImportanceScores, config: SelectionConfig) -> AuxSelection:
     """Budgeted top-k filtered by the window rule, aux-token space (selector.py:182-214)."""
-    sel, _ = select_tokens_device(scores, config)
-    return sel
+    return select_tokens_device(scores, config).aux_selection()
 
 
-def select_tokens_device(scores: ImportanceScores, config: SelectionConfig, index_offset: int = 0):
-    """select_tokens plus the device copy of the (offset) indices for the
-    recompute launch. The only host sync of the pipeline: count, indices and
-    window flags come back in one D2H copy."""
+@dataclass
+class DeviceSelection:
+    """Selection kernel output after the pipeline's single host sync: the
+    count, indices and window flags came back in one D2H copy; the device
+    indices feed the recompute launch directly. Python objects (windows,
+    tuples) are built afterwards, while the GPU runs."""
+    count: int
+    idx_dev: torch.Tensor          # [count] int64, index_offset applied
+    idx_host: np.ndarray           # [count] int64, index_offset applied
+    win_selected: np.ndarray
+    win_kept: np.ndarray
+    n_tokens: int
+    chunk_lens: tuple[int, ...]
+    config: SelectionConfig
+    index_offset: int
+
+    def windows(self) -> tuple[WindowRecord, ...]:
+        wl = self.config.window_len
+        out = []
+        wid, base = 0, 0
+        ws_sel, ws_kept = self.win_selected.tolist(), self.win_kept.tolist()
+        for ci, clen in enumerate(self.chunk_lens):
+            for ws in range(0, clen, wl):
+                we = min(ws + wl, clen)
+                out.append(WindowRecord(wid, ci, base + ws, base + we, ws_sel[wid], bool(ws_kept[wid]),
+                                        (we - ws) < wl))
+                wid += 1
+            base += clen
+        return tuple(out)
+
+    def aux_selection(self) -> AuxSelection:
+        aux_idx = tuple((self.idx_host - self.index_offset).tolist())
+        return AuxSelection(aux_idx, self.windows(), self.n_tokens, self.config.recomp_ratio)
+
+
+def select_tokens_device(scores: ImportanceScores, config: SelectionConfig, index_offset: int = 0) -> DeviceSelection:
     n = int(scores.device_scores.numel())
     budget = selection_budget(config.recomp_ratio, n)
     idx, cnt, wsel, wkept = _run_select(scores.device_scores, scores.chunk_lens, budget, config.window_len,
@@ -171,20 +202,9 @@ def select_tokens_device(scores: ImportanceScores, config: SelectionConfig, inde
     # one D2H read: count | window counts | kept flags | indices
     flags = torch.cat([cnt, wsel.long(), wkept.long(), idx]).cpu().numpy()
     k = int(flags[0])
-    wsel_h, wkept_h = flags[1:1 + n_win], flags[1 + n_win:1 + 2 * n_win]
-    idx_h = flags[1 + 2 * n_win:1 + 2 * n_win + k].astype(np.int64)
-    windows = []
-    wid, base = 0, 0
-    for ci, clen in enumerate(scores.chunk_lens):
-        for ws in range(0, clen, config.window_len):
-            we = min(ws + config.window_len, clen)
-            windows.append(WindowRecord(wid, ci, base + ws, base + we, int(wsel_h[wid]), bool(wkept_h[wid]),
-                                        (we - ws) < config.window_len))
-            wid += 1
-        base += clen
-    aux_idx = tuple(int(i) - index_offset for i in idx_h)
-    sel = AuxSelection(aux_idx, tuple(windows), n, config.recomp_ratio)
-    return sel, (idx[:k], idx_h)
+    return DeviceSelection(k, idx[:k], flags[1 + 2 * n_win:1 + 2 * n_win + k].astype(np.int64),
+                           flags[1:1 + n_win], flags[1 + n_win:1 + 2 * n_win], n, tuple(scores.chunk_lens), config,
+                           index_offset)
 
 
 def map_selection(aux_selection: AuxSelection, aux_spans: Sequence[TokenSpan], primary_spans: Sequence[TokenSpan],
