@@ -1,6 +1,6 @@
-// Attention kernels.
+// Legacy (mma.sync) sparse-row attention — the round-1 baseline.
 //
-// (1) sparse_row_attention_kernel — causal_attention(..., row_limits=idx+1)
+// sparse_row_attention_kernel — causal_attention(..., row_limits=idx+1)
 //     of selective_forward (model.py:715-720) and the mask_offset rule of
 //     layer_forward (model.py:467-476), without materialising the (H, m, n)
 //     logits (tensor_core.py:166-170). Flash-style online softmax over a bf16
@@ -10,11 +10,8 @@
 //     so a tile spans a narrow position range). Round-1 version on
 //     mma.sync.m16n8k16 (bf16 -> fp32).
 //
-// (2) banked_attention_f32_kernel — the scoring model's attention, fp32
-//     faithful: logits, mask, max-shifted softmax and weights @ v are formed
-//     exactly like the reference (materialised row in shared memory), so the
-//     last-layer weights that become importance scores carry only fp32
-//     rounding differences (selector.py:157-165).
+// The tcgen05 kernel that replaced it for production is attention_sm100.cu;
+// this one stays as the measured legacy-tensor-core baseline.
 #include "cc_common.cuh"
 
 namespace cc {
@@ -267,138 +264,6 @@ __global__ void __launch_bounds__(kAttnThreads) sparse_row_attention_kernel(
   }
 }
 
-// ---------------------------------------------------------------------------
-// (2) fp32 banked attention (scoring model)
-// ---------------------------------------------------------------------------
-constexpr int kBankRows = 16;
-constexpr int kBankKeys = 64;
-constexpr int kBankThreads = 256;
-
-template <int HD>
-__global__ void __launch_bounds__(kBankThreads) banked_attention_f32_kernel(
-    const cc_bank_seq* __restrict__ seqs, const float* __restrict__ q, const float* __restrict__ k_new,
-    const float* __restrict__ v_new, int n_q_heads, int n_kv_heads, float factor, int ncols_cap,
-    void* __restrict__ out, int out_mode, float* __restrict__ weights_out, int64_t w_col0, int64_t w_ld) {
-  extern __shared__ float fsm[];
-  const cc_bank_seq sq = seqs[blockIdx.z];
-  const int head = blockIdx.y;
-  const int i0 = blockIdx.x * kBankRows;
-  if (i0 >= sq.n_new) return;
-  const int rows = min(kBankRows, (int)(sq.n_new - i0));
-  const int kvh = head / (n_q_heads / n_kv_heads);
-  const int64_t nb = sq.n_bank;
-  const int ncols = (int)(nb + i0 + rows);  // columns any row of this block can see
-  const int64_t qw = (int64_t)n_q_heads * HD;
-  const int64_t kvw = (int64_t)n_kv_heads * HD;
-
-  float* s_q = fsm;                                   // [kBankRows][HD]
-  float* s_log = s_q + kBankRows * HD;                // [kBankRows][ncols_cap]
-  float* s_kv = s_log + (int64_t)kBankRows * ncols_cap;  // [kBankKeys][HD+1]
-  constexpr int KP = HD + 1;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  for (int idx = threadIdx.x; idx < kBankRows * HD; idx += kBankThreads) {
-    const int r = idx / HD, d = idx % HD;
-    s_q[idx] = r < rows ? q[(sq.row0 + i0 + r) * qw + (int64_t)head * HD + d] : 0.f;
-  }
-  __syncthreads();
-
-  auto kv_row_ptr = [&](const float* bank, const float* fresh, int64_t col) -> const float* {
-    return col < nb ? bank + col * kvw + (int64_t)kvh * HD : fresh + (sq.row0 + (col - nb)) * kvw + (int64_t)kvh * HD;
-  };
-
-  // phase 1: logits = (q . k) * factor, masked by the causal rule
-  for (int c0 = 0; c0 < ncols; c0 += kBankKeys) {
-    const int nk = min(kBankKeys, ncols - c0);
-    for (int idx = threadIdx.x; idx < kBankKeys * HD; idx += kBankThreads) {
-      const int r = idx / HD, d = idx % HD;
-      s_kv[r * KP + d] = r < nk ? kv_row_ptr(sq.k, k_new, c0 + r)[d] : 0.f;
-    }
-    __syncthreads();
-    for (int rr = warp; rr < kBankRows; rr += kBankThreads / 32) {
-      const int limit = (int)(nb + i0 + rr + 1);
-      for (int kk = lane; kk < kBankKeys; kk += 32) {
-        const int col = c0 + kk;
-        if (kk >= nk || rr >= rows) continue;
-        float acc = 0.f;
-#pragma unroll 16
-        for (int d = 0; d < HD; ++d) acc = fmaf(s_q[rr * HD + d], s_kv[kk * KP + d], acc);
-        s_log[rr * ncols_cap + col] = col < limit ? __fmul_rn(acc, factor) : -INFINITY;
-      }
-    }
-    __syncthreads();
-  }
-  // phase 2: max-shifted softmax per row (tensor_core.py:88-96)
-  for (int rr = warp; rr < rows; rr += kBankThreads / 32) {
-    float* row = s_log + rr * ncols_cap;
-    float mx = -INFINITY;
-    for (int c = lane; c < ncols; c += 32) mx = fmaxf(mx, row[c]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    float sum = 0.f;
-    for (int c = lane; c < ncols; c += 32) {
-      const float e = expf(__fsub_rn(row[c], mx));
-      row[c] = e;
-      sum += e;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-    for (int c = lane; c < ncols; c += 32) row[c] = __fdiv_rn(row[c], sum);
-  }
-  __syncthreads();
-
-  if (weights_out) {
-    // last-layer map restricted to bank columns [w_col0, n_bank)
-    for (int rr = 0; rr < rows; ++rr) {
-      float* dst = weights_out + ((((int64_t)blockIdx.z * n_q_heads + head) * sq.n_new) + i0 + rr) * w_ld;
-      for (int c = (int)w_col0 + threadIdx.x; c < nb; c += kBankThreads) dst[c - w_col0] = s_log[rr * ncols_cap + c];
-    }
-    return;
-  }
-  // phase 3: context = weights @ v
-  constexpr int PER = kBankRows * HD / kBankThreads;  // outputs per thread
-  float acc[PER];
-#pragma unroll
-  for (int e = 0; e < PER; ++e) acc[e] = 0.f;
-  for (int c0 = 0; c0 < ncols; c0 += kBankKeys) {
-    const int nk = min(kBankKeys, ncols - c0);
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < kBankKeys * HD; idx += kBankThreads) {
-      const int r = idx / HD, d = idx % HD;
-      s_kv[r * KP + d] = r < nk ? kv_row_ptr(sq.v, v_new, c0 + r)[d] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int e = 0; e < PER; ++e) {
-      const int o = threadIdx.x + e * kBankThreads;
-      const int rr = o / HD, d = o % HD;
-      const float* wr = s_log + rr * ncols_cap + c0;
-      float a = acc[e];
-      for (int kk = 0; kk < nk; ++kk) a = fmaf(wr[kk], s_kv[kk * KP + d], a);
-      acc[e] = a;
-    }
-  }
-#pragma unroll
-  for (int e = 0; e < PER; ++e) {
-    const int o = threadIdx.x + e * kBankThreads;
-    const int rr = o / HD, d = o % HD;
-    if (rr >= rows) continue;
-    const int64_t grow = sq.row0 + i0 + rr;
-    const int64_t col = (int64_t)head * HD + d;
-    if (out_mode == CC_F32) {
-      reinterpret_cast<float*>(out)[grow * qw + col] = acc[e];
-    } else {
-      float hi, lo, lh, ll;
-      split_tf32(acc[e], hi, lo);
-      split_tf32(lo, lh, ll);
-      float* p = reinterpret_cast<float*>(out) + grow * qw * 3;
-      p[col] = hi;
-      p[qw + col] = hi;
-      p[2 * qw + col] = lh;
-    }
-  }
-}
-
 }  // namespace cc
 
 using namespace cc;
@@ -433,37 +298,5 @@ extern "C" int cc_sparse_row_attention_mma(const void* q, int64_t ldq, const int
         n_keys, n_q_heads, n_kv_heads, factor, row_factor, (__nv_bfloat16*)out, ldo);
   }
   CC_LAUNCH_CHECK("sparse_row_attention");
-  return CC_OK;
-}
-
-extern "C" int cc_banked_attention_f32(const cc_bank_seq* seqs_dev, int32_t n_seqs, int32_t max_new,
-                                       int64_t max_bank, const float* q, const float* k_new, const float* v_new,
-                                       int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim, float factor,
-                                       void* out, int32_t out_mode, float* weights_out, int64_t w_col0,
-                                       int64_t w_ld, void* stream) {
-  CC_CHECK_ARG(n_kv_heads > 0 && n_q_heads % n_kv_heads == 0, CC_ERR_DIMENSION, "bad head counts");
-  CC_CHECK_ARG(head_dim == 64 || head_dim == 128, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
-  CC_CHECK_ARG(out_mode == CC_F32 || out_mode == CC_F32_SPLIT3, CC_ERR_UNSUPPORTED, "out mode");
-  if (n_seqs <= 0 || max_new <= 0) return CC_OK;
-  const int64_t ncols_cap = max_bank + max_new;
-  CC_CHECK_ARG(ncols_cap <= 2048, CC_ERR_UNSUPPORTED, "banked attention supports <= 2048 columns (got %lld)",
-               (long long)ncols_cap);
-  const int smem =
-      (int)((kBankRows * head_dim + kBankRows * ncols_cap + kBankKeys * (head_dim + 1)) * sizeof(float));
-  ProfScope ps(as_stream(stream), OP_BANKED, 0);
-  dim3 grid((max_new + kBankRows - 1) / kBankRows, n_q_heads, n_seqs);
-  cudaStream_t st = as_stream(stream);
-  if (head_dim == 64) {
-    cudaFuncSetAttribute(banked_attention_f32_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    banked_attention_f32_kernel<64><<<grid, kBankThreads, smem, st>>>(seqs_dev, q, k_new, v_new, n_q_heads,
-                                                                      n_kv_heads, factor, (int)ncols_cap, out,
-                                                                      out_mode, weights_out, w_col0, w_ld);
-  } else {
-    cudaFuncSetAttribute(banked_attention_f32_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    banked_attention_f32_kernel<128><<<grid, kBankThreads, smem, st>>>(seqs_dev, q, k_new, v_new, n_q_heads,
-                                                                       n_kv_heads, factor, (int)ncols_cap, out,
-                                                                       out_mode, weights_out, w_col0, w_ld);
-  }
-  CC_LAUNCH_CHECK("banked_attention_f32");
   return CC_OK;
 }

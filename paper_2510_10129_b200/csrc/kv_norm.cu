@@ -237,38 +237,84 @@ __device__ __forceinline__ void write_x(void* x_out, int mode, int64_t row, int 
   }
 }
 
-constexpr int kNormThreads = 256;
-constexpr int kNormMaxPer = 32;  // d <= 8192
+constexpr int kNormThreads = 128;
+constexpr int kNormVec = 16;  // float4 per thread: d <= 128 * 16 * 4 = 8192
+
+// One CTA per row, 128 threads, the row held in registers as float4s.
+__device__ __forceinline__ void store_x4(void* x_out, int mode, int64_t row, int d, int j, const float* y) {
+  if (mode == CC_BF16) {
+    __nv_bfloat162 a = __floats2bfloat162_rn(y[0], y[1]), b = __floats2bfloat162_rn(y[2], y[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(x_out) + row * d + j) = u;
+  } else if (mode == CC_F32) {
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(x_out) + row * d + j) = make_float4(y[0], y[1], y[2], y[3]);
+  } else {
+    float hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float l, lh, ll;
+      split_tf32(y[e], hi[e], l);
+      split_tf32(l, lh, ll);
+      lo[e] = lh;
+    }
+    float* o = reinterpret_cast<float*>(x_out) + row * (int64_t)d * 3;
+    *reinterpret_cast<float4*>(o + j) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<float4*>(o + d + j) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<float4*>(o + 2 * d + j) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
 
 __global__ void __launch_bounds__(kNormThreads) embed_rmsnorm_kernel(
     const int64_t* __restrict__ ids, const void* __restrict__ embed, int embed_dtype, int d,
     float* __restrict__ h_out, const float* __restrict__ gain, float eps, void* __restrict__ x_out, int x_mode,
     const float* __restrict__ h_in, int64_t ld_h) {
-  __shared__ float red[33];
+  __shared__ float red[kNormThreads / 32];
   const int64_t row = blockIdx.x;
-  float vals[kNormMaxPer];
+  const int n4 = d >> 2;
+  float4 v[kNormVec];
   float ss = 0.f;
-  int cnt = 0;
-  for (int j = threadIdx.x; j < d; j += kNormThreads, ++cnt) {
-    float v;
-    if (h_in) {
-      v = h_in[row * ld_h + j];
-    } else {
-      const int64_t t = ids[row];
-      v = embed_dtype == CC_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(embed)[t * d + j])
-                                 : reinterpret_cast<const float*>(embed)[t * d + j];
-      if (h_out) h_out[row * d + j] = v;
+  const int64_t tok = h_in ? 0 : ids[row];
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    const int c = threadIdx.x + k * kNormThreads;
+    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < n4) {
+      if (h_in) {
+        v[k] = *reinterpret_cast<const float4*>(h_in + row * ld_h + 4 * c);
+      } else if (embed_dtype == CC_BF16) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(embed) + tok * d) + c);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        v[k] = make_float4(a.x, a.y, b.x, b.y);
+      } else {
+        v[k] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(embed) + tok * d) + c);
+      }
+      if (!h_in && h_out) *reinterpret_cast<float4*>(h_out + row * d + 4 * c) = v[k];
+      ss = fmaf(v[k].x, v[k].x, ss);
+      ss = fmaf(v[k].y, v[k].y, ss);
+      ss = fmaf(v[k].z, v[k].z, ss);
+      ss = fmaf(v[k].w, v[k].w, ss);
     }
-    vals[cnt] = v;
-    ss = fmaf(v, v, ss);
   }
-  const float tot = block_sum(ss, red);
-  const float ms = __fdiv_rn(tot, (float)d);
-  const float r = __fsqrt_rn(__fadd_rn(ms, eps));
-  cnt = 0;
-  for (int j = threadIdx.x; j < d; j += kNormThreads, ++cnt) {
-    float y = __fmul_rn(__fdiv_rn(vals[cnt], r), gain[j]);
-    write_x(x_out, x_mode, row, d, j, y);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < kNormThreads / 32; ++w) tot += red[w];
+  const float r = __fsqrt_rn(__fadd_rn(__fdiv_rn(tot, (float)d), eps));
+#pragma unroll
+  for (int k = 0; k < kNormVec; ++k) {
+    const int c = threadIdx.x + k * kNormThreads;
+    if (c < n4) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + c);
+      const float y[4] = {__fmul_rn(__fdiv_rn(v[k].x, r), g.x), __fmul_rn(__fdiv_rn(v[k].y, r), g.y),
+                          __fmul_rn(__fdiv_rn(v[k].z, r), g.z), __fmul_rn(__fdiv_rn(v[k].w, r), g.w)};
+      store_x4(x_out, x_mode, row, d, 4 * c, y);
+    }
   }
 }
 
@@ -413,7 +459,7 @@ int cc_embed_rmsnorm(const int64_t* ids, int64_t rows, const void* embed, int32_
                      int32_t d, float* h_out, const float* gain, float eps, void* x_out, int32_t x_mode,
                      void* stream) {
   (void)vocab;
-  CC_CHECK_ARG(d > 0 && d <= kNormThreads * kNormMaxPer, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
+  CC_CHECK_ARG(d > 0 && d % 4 == 0 && d <= kNormThreads * kNormVec * 4, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
   if (rows <= 0) return CC_OK;
   ProfScope ps(as_stream(stream), OP_NORM, 0);
   embed_rmsnorm_kernel<<<rows, kNormThreads, 0, as_stream(stream)>>>(ids, embed, embed_dtype, d, h_out, gain, eps,
@@ -424,7 +470,7 @@ int cc_embed_rmsnorm(const int64_t* ids, int64_t rows, const void* embed, int32_
 
 int cc_rmsnorm(const float* h, int64_t rows, int32_t d, int64_t ld_h, const float* gain, float eps, void* x_out,
                int32_t x_mode, void* stream) {
-  CC_CHECK_ARG(d > 0 && d <= kNormThreads * kNormMaxPer, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
+  CC_CHECK_ARG(d > 0 && d % 4 == 0 && d <= kNormThreads * kNormVec * 4, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
   if (rows <= 0) return CC_OK;
   ProfScope ps(as_stream(stream), OP_NORM, 0);
   embed_rmsnorm_kernel<<<rows, kNormThreads, 0, as_stream(stream)>>>(nullptr, nullptr, 0, d, nullptr, gain, eps,
