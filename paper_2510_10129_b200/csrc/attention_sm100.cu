@@ -5,21 +5,24 @@
 // (model.py:467-476) for query rows and dense prefill — without materialising
 // the (H, m, n) logits of tensor_core.py:166-170.
 //
-// One CTA = 128 packed query rows x one KV head. GQA packing: packed row
+// One CTA = two 128-row query tiles x one KV head. GQA packing: packed row
 // p = i*G + g is selected row i, query head kvh*G + g, so every K/V tile is
-// fetched once for all G heads that share it. Keys stream in 128-key tiles
-// up to the CTA's largest row limit (rows are sorted by position, so a tile's
-// rows span a narrow range and little work is masked).
+// fetched once for all G heads (and both query tiles) that share it. Keys
+// stream in 128-key tiles up to the CTA's largest row limit (rows are sorted
+// by position, so a tile spans a narrow range and little work is masked).
 //
 //   warp 0      TMA producer: K and V tiles ([keys][D] bf16, 128B swizzle), 2 stages
-//   warp 1      tcgen05.mma issuer: S_j = Q K_j^T into TMEM (double-buffered),
-//               O += P_j V_j (P from smem, V as an MN-major operand)
-//   warps 2..5  softmax: thread t owns packed row t — its S row comes out of
-//               TMEM with tcgen05.ld, max/exp2/sum run in-thread (no shuffles),
-//               P (bf16) goes to smem for the PV MMA. Lazy rescaling: the
-//               running max only moves (and O in TMEM is rescaled) when a tile
-//               raises it by more than 2^8, so p <= 256 and O rarely needs a
-//               TMEM round trip. Final O / l -> bf16 context rows.
+//   warp 1      tcgen05.mma issuer, ping-pong over the two query tiles:
+//               PV_A(j) | S_A(j+1) | PV_B(j) | S_B(j+1) ...  S = Q K^T lands in
+//               TMEM; O += P V reads P straight from TMEM (A operand) and V
+//               from smem as an MN-major operand.
+//   warps 2..5  softmax of tile A, warps 6..9 of tile B: thread t owns row t,
+//               reads its S row with tcgen05.ld, does max / exp2 / sum in-thread,
+//               writes P (bf16 pairs) back over its S row with tcgen05.st.
+//               Lazy rescale: the running max moves (and O is rescaled in TMEM)
+//               only when a tile raises it by > 2^8. One FFMA per element
+//               folds scale and max; a quarter of the exp2s run as a
+//               polynomial on the FMA pipe to offload MUFU.
 #include "cc_common.cuh"
 
 #include <cuda.h>
@@ -27,22 +30,22 @@
 
 namespace cc {
 
-constexpr int kFaRows = 128;
+constexpr int kFaTileRows = 128;
 constexpr int kFaKeys = 128;
-constexpr int kFaThreads = 192;
+constexpr int kFaThreads = 320;
 constexpr float kFaRescaleThreshold = 8.0f;  // log2 domain
 
 template <int D>
 struct FaCfg {
-  static constexpr int KB = D / 64;               // 128-byte K-blocks per row of Q / K
-  static constexpr int Q_BYTES = kFaRows * D * 2;  // 32 KB (D=128)
-  static constexpr int KT_BYTES = kFaKeys * D * 2; // one K (or V) tile
-  static constexpr int P_BYTES = kFaRows * kFaKeys * 2;
+  static constexpr int KB = D / 64;                   // 128-byte K-blocks per row of Q / K
+  static constexpr int QT_BYTES = kFaTileRows * D * 2;  // one query tile
+  static constexpr int KT_BYTES = kFaKeys * D * 2;      // one K (or V) tile
   static constexpr int STAGES = 2;
-  static constexpr int SMEM = Q_BYTES + 2 * STAGES * KT_BYTES + P_BYTES + 1024 + 256;
+  static constexpr int SMEM = 2 * QT_BYTES + 2 * STAGES * KT_BYTES + 1024 + 256;
   static constexpr uint32_t IDESC_S = umma_idesc(128, kFaKeys, false);
   static constexpr uint32_t IDESC_PV = umma_idesc(128, D, false) | (1u << 16);  // B (V) MN-major
-  static constexpr int S_COL0 = 0, S_COL1 = kFaKeys, O_COL = 2 * kFaKeys;
+  __host__ __device__ static constexpr int s_col(int t) { return t * 256; }
+  __host__ __device__ static constexpr int o_col(int t) { return t * 256 + 128; }
 };
 
 // MN-major 128B-swizzled operand: 64-element rows of 128 B, MN atoms LBO
@@ -66,6 +69,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const void* desc, uint64_
       : "memory");
 }
 
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -85,6 +98,15 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -94,36 +116,57 @@ __device__ __forceinline__ uint32_t pack2_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+__device__ __forceinline__ float ex2_mufu(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^x on the FMA pipe: round-to-nearest split x = n + f, |f| <= 1/2, degree-4
+// polynomial for 2^f (|rel err| < 5e-5, far below bf16 P rounding), 2^n via
+// the exponent field.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.0f);
+  const float magic = 12582912.0f;  // 1.5 * 2^23
+  const float t = x + magic;
+  const float f = x - (t - magic);
+  float p = fmaf(f, 9.6181291e-3f, 5.5504109e-2f);
+  p = fmaf(p, f, 2.4022651e-1f);
+  p = fmaf(p, f, 6.9314718e-1f);
+  p = fmaf(p, f, 1.0f);
+  const int n = __float_as_int(t) - __float_as_int(magic);
+  return __int_as_float(__float_as_int(p) + (n << 23));
+}
+
 template <int D>
 __global__ void __launch_bounds__(kFaThreads, 1)
     fa_sparse_row_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                          const __nv_bfloat16* __restrict__ q, int64_t ldq, const int64_t* __restrict__ pos, int64_t m,
                          int64_t n_keys, int n_q_heads, int n_kv_heads, float factor,
                          const float* __restrict__ row_factor, __nv_bfloat16* __restrict__ out, int64_t ldo,
-                         int n_qtiles) {
+                         int n_ctas) {
   using Cfg = FaCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + Cfg::Q_BYTES;                       // [STAGES][KT_BYTES]
+  uint8_t* sQ = smem;                                   // [2 tiles][KB][128 rows][128 B]
+  uint8_t* sK = sQ + 2 * Cfg::QT_BYTES;                  // [STAGES][KB][128 keys][128 B]
   uint8_t* sV = sK + Cfg::STAGES * Cfg::KT_BYTES;
-  uint8_t* sP = sV + Cfg::STAGES * Cfg::KT_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + Cfg::P_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sV + Cfg::STAGES * Cfg::KT_BYTES);
   uint64_t* k_full = bars;        // [2]
   uint64_t* v_full = bars + 2;    // [2]
   uint64_t* kv_empty = bars + 4;  // [2]
-  uint64_t* s_full = bars + 6;    // [2]
-  uint64_t* p_full = bars + 8;
-  uint64_t* pv_done = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
-  int* s_kmax = reinterpret_cast<int*>(bars + 11);
+  uint64_t* s_full = bars + 6;    // [2 tiles]
+  uint64_t* p_full = bars + 8;    // [2 tiles]
+  uint64_t* pv_done = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
+  int* s_kmax = reinterpret_cast<int*>(bars + 12);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = n_q_heads / n_kv_heads;
   const int kvh = blockIdx.y;
-  const int qtile = n_qtiles - 1 - (int)blockIdx.x;  // heavy (late-position) tiles first
+  const int cta = n_ctas - 1 - (int)blockIdx.x;  // heavy (late-position) tiles first
   const int64_t packed_total = m * G;
-  const int64_t p0 = (int64_t)qtile * kFaRows;
+  const int64_t p0 = (int64_t)cta * 2 * kFaTileRows;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
@@ -131,37 +174,39 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&kv_empty[s], 1);
       mbar_init(&s_full[s], 1);
+      mbar_init(&p_full[s], 4);
     }
-    mbar_init(p_full, 4);
     mbar_init(pv_done, 1);
     *s_kmax = 0;
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
 
-  // ---- prologue: softmax warps gather their Q row into swizzled smem -----
+  // ---- prologue: softmax warps gather their Q rows into swizzled smem ----
+  const int tq = warp >= 2 ? (warp - 2) >> 2 : 0;  // query tile of this softmax warp
+  const int quarter = warp & 3;                     // TMEM lane quarter
+  const int r = quarter * 32 + lane;                // row within the tile
   int lim = 0;
   float scale2 = 0.f;
   int64_t out_off = -1;
   if (warp >= 2) {
-    const int r = (warp & 3) * 32 + lane;  // TMEM lane quarter = warp % 4
-    const int64_t p = p0 + r;
-    uint4 zero = make_uint4(0, 0, 0, 0);
+    const int64_t p = p0 + tq * kFaTileRows + r;
+    const uint4 zero = make_uint4(0, 0, 0, 0);
     const uint4* src = nullptr;
     if (p < packed_total) {
       const int64_t i = p / G;
       const int head = kvh * G + (int)(p % G);
-      const int64_t ps = pos[i];
-      lim = (int)min(ps + 1, n_keys);
+      lim = (int)min(pos[i] + 1, n_keys);
       scale2 = (row_factor ? row_factor[i] : factor) * 1.4426950408889634f;
       src = reinterpret_cast<const uint4*>(q + i * ldq + (int64_t)head * D);
       out_off = i * ldo + (int64_t)head * D;
     }
+    uint8_t* qt = sQ + tq * Cfg::QT_BYTES;
 #pragma unroll
     for (int c = 0; c < D / 8; ++c) {
       const uint4 v = src ? __ldg(src + c) : zero;
       const int kb = c >> 3, cc = c & 7;
-      *reinterpret_cast<uint4*>(sQ + kb * (kFaRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
+      *reinterpret_cast<uint4*>(qt + kb * (kFaTileRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
     }
     fence_proxy_async_smem();
     int mx = lim;
@@ -195,127 +240,136 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    auto issue_s = [&](int j) {
-      const int s = j & 1;
-      mbar_wait(&k_full[s], (j >> 1) & 1);
-      tc_fence_after();
+    // ---------------- MMA issuer (ping-pong over the two query tiles) ----------------
+    auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
       if (lane == 0) {
-        const uint32_t q0 = smem_u32(sQ), k0 = smem_u32(sK + s * Cfg::KT_BYTES);
+        const uint32_t q0 = smem_u32(sQ + t * Cfg::QT_BYTES), k0 = smem_u32(sK + (j & 1) * Cfg::KT_BYTES);
 #pragma unroll
         for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kFaRows * 128) + (k & 3) * 32;
-          const uint32_t koff = (k >> 2) * (kFaKeys * 128) + (k & 3) * 32;
-          tc_mma<false>(tmem + (s ? Cfg::S_COL1 : Cfg::S_COL0), umma_desc_sw128(q0 + off),
-                        umma_desc_sw128(k0 + koff), Cfg::IDESC_S, k > 0 ? 1u : 0u);
+          const uint32_t qo = (k >> 2) * (kFaTileRows * 128) + (k & 3) * 32;
+          const uint32_t ko = (k >> 2) * (kFaKeys * 128) + (k & 3) * 32;
+          tc_mma<false>(tmem + Cfg::s_col(t), umma_desc_sw128(q0 + qo), umma_desc_sw128(k0 + ko), Cfg::IDESC_S,
+                        k > 0 ? 1u : 0u);
         }
-        tc_commit(&s_full[s]);
+        tc_commit(&s_full[t]);
       }
       __syncwarp();
     };
-    auto issue_pv = [&](int j) {
-      const int s = j & 1;
-      mbar_wait(p_full, j & 1);
-      mbar_wait(&v_full[s], (j >> 1) & 1);
+    auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P read from TMEM (over S_t)
+      mbar_wait(&p_full[t], j & 1);
       tc_fence_after();
       if (lane == 0) {
-        const uint32_t p0a = smem_u32(sP), v0 = smem_u32(sV + s * Cfg::KT_BYTES);
+        const uint32_t v0 = smem_u32(sV + (j & 1) * Cfg::KT_BYTES);
 #pragma unroll
-        for (int k = 0; k < kFaKeys / 16; ++k) {
-          const uint32_t off = (k >> 2) * (kFaRows * 128) + (k & 3) * 32;
-          tc_mma<false>(tmem + Cfg::O_COL, umma_desc_sw128(p0a + off),
-                        umma_desc_mn_sw128(v0 + k * 16 * 128, kFaKeys * 128, 1024), Cfg::IDESC_PV,
-                        (j > 0 || k > 0) ? 1u : 0u);
-        }
-        tc_commit(&kv_empty[s]);
-        tc_commit(pv_done);
+        for (int k = 0; k < kFaKeys / 16; ++k)
+          tc_mma_ts(tmem + Cfg::o_col(t), tmem + Cfg::s_col(t) + k * 8,
+                    umma_desc_mn_sw128(v0 + k * 16 * 128, kFaKeys * 128, 1024), Cfg::IDESC_PV,
+                    (j > 0 || k > 0) ? 1u : 0u);
       }
       __syncwarp();
     };
-    if (n_tiles > 0) issue_s(0);
-    if (n_tiles > 1) issue_s(1);
-    for (int j = 0; j < n_tiles; ++j) {
-      issue_pv(j);
-      if (j + 2 < n_tiles) issue_s(j + 2);
+    if (n_tiles > 0) {
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < n_tiles; ++j) {
+        const bool more = j + 1 < n_tiles;
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+        issue_pv(0, j);
+        if (more) {
+          mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+          tc_fence_after();
+          issue_s(0, j + 1);
+        }
+        issue_pv(1, j);
+        if (lane == 0) tc_commit(&kv_empty[j & 1]);
+        __syncwarp();
+        if (more) issue_s(1, j + 1);
+      }
+      if (lane == 0) tc_commit(pv_done);
+      __syncwarp();
     }
   } else {
     // ---------------- softmax + epilogue (row per thread) ----------------
-    const int quarter = warp & 3;
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
-    const int r = quarter * 32 + lane;
+    const uint32_t s_addr = tmem + lane_base + Cfg::s_col(tq);
+    const uint32_t o_addr = tmem + lane_base + Cfg::o_col(tq);
+    int warp_min = out_off >= 0 ? lim : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) warp_min = min(warp_min, __shfl_xor_sync(0xffffffffu, warp_min, o));
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
-      const int s = j & 1;
-      mbar_wait(&s_full[s], (j >> 1) & 1);
+      mbar_wait(&s_full[tq], j & 1);
       tc_fence_after();
       float sv[kFaKeys];
 #pragma unroll
-      for (int c = 0; c < kFaKeys / 32; ++c)
-        tmem_ld32(tmem + lane_base + (s ? Cfg::S_COL1 : Cfg::S_COL0) + c * 32, sv + c * 32);
+      for (int c = 0; c < kFaKeys / 32; ++c) tmem_ld32(s_addr + c * 32, sv + c * 32);
       const int key0 = j * kFaKeys;
+      if (key0 + kFaKeys > warp_min) {  // boundary tile: apply the per-row causal limit
+#pragma unroll
+        for (int c = 0; c < kFaKeys; ++c) sv[c] = (key0 + c < lim) ? sv[c] : -INFINITY;
+      }
       float mt = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < kFaKeys; ++c) {
-        float x = sv[c] * scale2;
-        x = (key0 + c < lim) ? x : -INFINITY;
-        sv[c] = x;
-        mt = fmaxf(mt, x);
-      }
-      // lazy rescale: move the running max only when the tile exceeds it by > 2^8
+      for (int c = 0; c < kFaKeys; ++c) mt = fmaxf(mt, sv[c]);
+      const float m_tile = mt * scale2;  // scale2 > 0: max commutes with the scale
       float alpha = 1.f;
       bool resc = false;
-      if (mt > m_run + kFaRescaleThreshold) {
-        alpha = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
-        m_run = mt;
+      if (m_tile > m_run + kFaRescaleThreshold) {
+        alpha = (m_run == -INFINITY) ? 0.f : ex2_mufu(m_run - m_tile);
+        m_run = m_tile;
         resc = true;
       }
-      const float base = (m_run == -INFINITY) ? 0.f : m_run;
+      const float nbase = (m_run == -INFINITY) ? 0.f : -m_run;
       float lsum = 0.f;
-      uint32_t pk[kFaKeys / 2];
 #pragma unroll
-      for (int c = 0; c < kFaKeys / 2; ++c) {
-        const float a = exp2f(sv[2 * c] - base), b = exp2f(sv[2 * c + 1] - base);
-        lsum += a + b;
-        pk[c] = pack2_bf16(a, b);
+      for (int c = 0; c < kFaKeys / 32; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          const float xa = fmaf(sv[c * 32 + 2 * e], scale2, nbase);
+          const float xb = fmaf(sv[c * 32 + 2 * e + 1], scale2, nbase);
+          float a, b;
+          if ((e & 3) == 3) {  // a quarter of the exponentials on the FMA pipe
+            a = ex2_poly(xa);
+            b = ex2_poly(xb);
+          } else {
+            a = ex2_mufu(xa);
+            b = ex2_mufu(xb);
+          }
+          lsum += a + b;
+          pk[e] = pack2_bf16(a, b);
+        }
+        tmem_st16u(s_addr + c * 16, pk);  // P over the S row: column c*16+e holds keys (2e, 2e+1) of chunk c
       }
       l_run = l_run * alpha + lsum;
-      if (j > 0) {
-        mbar_wait(pv_done, (j - 1) & 1);  // P buffer free, O stable
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, resc)) {
-          const float a = resc ? alpha : 1.f;
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        // O is stable here: PV_t(j-1) completed before S_t(j) (in-order tcgen05 pipe)
+        const float a = resc ? alpha : 1.f;
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            float ov[32];
-            tmem_ld32(tmem + lane_base + Cfg::O_COL + c * 32, ov);
+        for (int c = 0; c < D / 32; ++c) {
+          float ov[32];
+          tmem_ld32(o_addr + c * 32, ov);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) ov[e] *= a;
-            tmem_st32(tmem + lane_base + Cfg::O_COL + c * 32, ov);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          for (int e = 0; e < 32; ++e) ov[e] *= a;
+          tmem_st32(o_addr + c * 32, ov);
         }
       }
-      // P row -> smem (K-major, 128B swizzle: 2 regions of 64 keys)
-#pragma unroll
-      for (int c = 0; c < kFaKeys / 8; ++c) {
-        const int kb = c >> 3, cc = c & 7;
-        *reinterpret_cast<uint4*>(sP + kb * (kFaRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) =
-            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      }
-      fence_proxy_async_smem();
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(p_full);
+      if (lane == 0) mbar_arrive(&p_full[tq]);
     }
     if (n_tiles > 0) {
-      mbar_wait(pv_done, (n_tiles - 1) & 1);
+      mbar_wait(pv_done, 0);
       tc_fence_after();
     }
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       float ov[32];
-      tmem_ld32(tmem + lane_base + Cfg::O_COL + c * 32, ov);
+      tmem_ld32(o_addr + c * 32, ov);
       if (out_off >= 0) {
         uint4* dst = reinterpret_cast<uint4*>(out + out_off + c * 32);
 #pragma unroll
@@ -377,12 +431,12 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64
     attr = true;
   }
   const int G = hq / hkv;
-  const int n_qtiles = (int)((m * G + kFaRows - 1) / kFaRows);
-  dim3 grid(n_qtiles, hkv);
+  const int n_ctas = (int)((m * G + 2 * kFaTileRows - 1) / (2 * kFaTileRows));
+  dim3 grid(n_ctas, hkv);
   ProfScope ps(st, OP_ATTENTION, flops);
   fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
       tk, tv, (const __nv_bfloat16*)q, ldq, positions, m, n_keys, hq, hkv, factor, row_factor,
-      (__nv_bfloat16*)out, ldo, n_qtiles);
+      (__nv_bfloat16*)out, ldo, n_ctas);
   CC_LAUNCH_CHECK("fa_sparse_row");
   return CC_OK;
 }

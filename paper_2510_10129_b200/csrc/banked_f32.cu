@@ -101,31 +101,39 @@ __global__ void __launch_bounds__(kBkThreads) banked_f32_kernel(
   }
   __syncthreads();
 
-  // ---- phase 2: softmax per row (tensor_core.py:88-96), thread per row ----
-  if (tid < nrows) {
-    const int r = tid;
-    const int limit = (int)(nb + i0 + r / G + 1);
+  // ---- phase 2: softmax per row (tensor_core.py:88-96): 4 threads per row,
+  // columns interleaved, partial max / sum combined with quad shuffles -------
+  {
+    const int r = tid >> 2, part = tid & 3;  // 64 rows x 4 parts = 256 threads
+    const bool live = r < nrows;
+    const int limit = live ? (int)(nb + i0 + r / G + 1) : 0;
     float mx = -INFINITY;
-    for (int c = 0; c < limit; ++c) mx = fmaxf(mx, sT[(size_t)c * kBkRows + r]);
+    for (int c = part; c < limit; c += 4) mx = fmaxf(mx, sT[(size_t)c * kBkRows + r]);
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
     float sum = 0.f;
-    for (int c = 0; c < limit; ++c) {
+    for (int c = part; c < limit; c += 4) {
       const float e = expf(__fsub_rn(sT[(size_t)c * kBkRows + r], mx));
       sT[(size_t)c * kBkRows + r] = e;
       sum = __fadd_rn(sum, e);
     }
-    for (int c = 0; c < ncols; ++c) {
+    sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, 1));
+    sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, 2));
+    for (int c = part; c < ncols; c += 4) {
       float* p = sT + (size_t)c * kBkRows + r;
       *p = c < limit ? __fdiv_rn(*p, sum) : 0.f;
     }
-    if (weights_out) {  // last-layer map over bank columns [w_col0, nb)
+  }
+  if (weights_out) {  // last-layer map over bank columns [w_col0, nb): warp per row, coalesced stores
+    __syncthreads();
+    const int warp = tid >> 5, lane = tid & 31;
+    for (int r = warp; r < nrows; r += kBkThreads / 32) {
       const int i = i0 + r / G, head = kvh * G + r % G;
       float* dst = weights_out + ((((int64_t)blockIdx.z * n_q_heads + head) * sq.n_new) + i) * w_ld;
-      for (int64_t c = w_col0; c < nb; ++c) dst[c - w_col0] = sT[(size_t)c * kBkRows + r];
+      for (int64_t c = w_col0 + lane; c < nb; c += 32) dst[c - w_col0] = sT[(size_t)c * kBkRows + r];
     }
-  } else if (tid < kBkRows) {
-    for (int c = 0; c < ncols; ++c) sT[(size_t)c * kBkRows + tid] = 0.f;
+    return;
   }
-  if (weights_out) return;
   __syncthreads();
 
   // ---- phase 3: context = weights @ V (4 rows x 4*HD/64 dims per thread) ----
