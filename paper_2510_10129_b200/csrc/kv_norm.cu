@@ -266,6 +266,83 @@ __device__ __forceinline__ void store_x4(void* x_out, int mode, int64_t row, int
   }
 }
 
+// Warp per row, 8 rows per CTA: every lane issues all of its float4 loads
+// before the reduction (high memory-level parallelism, no block barrier).
+template <int V>
+__global__ void __launch_bounds__(256) rmsnorm_warp_kernel(
+    const int64_t* __restrict__ ids, const void* __restrict__ embed, int embed_dtype, int d,
+    float* __restrict__ h_out, const float* __restrict__ gain, float eps, void* __restrict__ x_out, int x_mode,
+    const float* __restrict__ h_in, int64_t ld_h, int64_t rows) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
+  if (row >= rows) return;
+  const int n4 = d >> 2;
+  const int64_t tok = h_in ? 0 : ids[row];
+  float4 v[V];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int c = lane + 32 * k;
+    v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < n4) {
+      if (h_in) {
+        v[k] = *reinterpret_cast<const float4*>(h_in + row * ld_h + 4 * c);
+      } else if (embed_dtype == CC_BF16) {
+        const uint2 u = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(embed) + tok * d) + c);
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        v[k] = make_float4(a.x, a.y, b.x, b.y);
+      } else {
+        v[k] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(embed) + tok * d) + c);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int c = lane + 32 * k;
+    if (c < n4) {
+      if (!h_in && h_out) *reinterpret_cast<float4*>(h_out + row * d + 4 * c) = v[k];
+      ss = fmaf(v[k].x, v[k].x, ss);
+      ss = fmaf(v[k].y, v[k].y, ss);
+      ss = fmaf(v[k].z, v[k].z, ss);
+      ss = fmaf(v[k].w, v[k].w, ss);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const float r = __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps));
+#pragma unroll
+  for (int k = 0; k < V; ++k) {
+    const int c = lane + 32 * k;
+    if (c < n4) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + c);
+      const float y[4] = {__fmul_rn(__fdiv_rn(v[k].x, r), g.x), __fmul_rn(__fdiv_rn(v[k].y, r), g.y),
+                          __fmul_rn(__fdiv_rn(v[k].z, r), g.z), __fmul_rn(__fdiv_rn(v[k].w, r), g.w)};
+      store_x4(x_out, x_mode, row, d, 4 * c, y);
+    }
+  }
+}
+
+static void launch_rmsnorm(const int64_t* ids, const void* embed, int embed_dtype, int d, float* h_out,
+                           const float* gain, float eps, void* x_out, int x_mode, const float* h_in, int64_t ld_h,
+                           int64_t rows, cudaStream_t st) {
+  const int per_lane = (d / 4 + 31) / 32;
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+#define CC_NORM_CASE(V)                                                                                        \
+  if (per_lane <= V) {                                                                                         \
+    rmsnorm_warp_kernel<V><<<grid, 256, 0, st>>>(ids, embed, embed_dtype, d, h_out, gain, eps, x_out, x_mode, \
+                                                 h_in, ld_h, rows);                                            \
+    return;                                                                                                    \
+  }
+  CC_NORM_CASE(2)
+  CC_NORM_CASE(8)
+  CC_NORM_CASE(16)
+  CC_NORM_CASE(32)
+  CC_NORM_CASE(48)
+  CC_NORM_CASE(64)
+#undef CC_NORM_CASE
+}
+
 __global__ void __launch_bounds__(kNormThreads) embed_rmsnorm_kernel(
     const int64_t* __restrict__ ids, const void* __restrict__ embed, int embed_dtype, int d,
     float* __restrict__ h_out, const float* __restrict__ gain, float eps, void* __restrict__ x_out, int x_mode,
@@ -462,8 +539,7 @@ int cc_embed_rmsnorm(const int64_t* ids, int64_t rows, const void* embed, int32_
   CC_CHECK_ARG(d > 0 && d % 4 == 0 && d <= kNormThreads * kNormVec * 4, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
   if (rows <= 0) return CC_OK;
   ProfScope ps(as_stream(stream), OP_NORM, 0);
-  embed_rmsnorm_kernel<<<rows, kNormThreads, 0, as_stream(stream)>>>(ids, embed, embed_dtype, d, h_out, gain, eps,
-                                                                       x_out, x_mode, nullptr, 0);
+  launch_rmsnorm(ids, embed, embed_dtype, d, h_out, gain, eps, x_out, x_mode, nullptr, 0, rows, as_stream(stream));
   CC_LAUNCH_CHECK("embed_rmsnorm");
   return CC_OK;
 }
@@ -473,8 +549,7 @@ int cc_rmsnorm(const float* h, int64_t rows, int32_t d, int64_t ld_h, const floa
   CC_CHECK_ARG(d > 0 && d % 4 == 0 && d <= kNormThreads * kNormVec * 4, CC_ERR_UNSUPPORTED, "d_model %d unsupported", d);
   if (rows <= 0) return CC_OK;
   ProfScope ps(as_stream(stream), OP_NORM, 0);
-  embed_rmsnorm_kernel<<<rows, kNormThreads, 0, as_stream(stream)>>>(nullptr, nullptr, 0, d, nullptr, gain, eps,
-                                                                       x_out, x_mode, h, ld_h);
+  launch_rmsnorm(nullptr, nullptr, 0, d, nullptr, gain, eps, x_out, x_mode, h, ld_h, rows, as_stream(stream));
   CC_LAUNCH_CHECK("rmsnorm");
   return CC_OK;
 }
