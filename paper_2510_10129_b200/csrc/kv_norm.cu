@@ -266,23 +266,23 @@ __device__ __forceinline__ void store_x4(void* x_out, int mode, int64_t row, int
   }
 }
 
-// Warp per row, 8 rows per CTA: every lane issues all of its float4 loads
-// before the reduction (high memory-level parallelism, no block barrier).
+// One 256-thread CTA per row, at most V float4 per thread held in registers
+// (few registers -> ~48 resident warps per SM), all loads issued before use.
 template <int V>
 __global__ void __launch_bounds__(256) rmsnorm_warp_kernel(
     const int64_t* __restrict__ ids, const void* __restrict__ embed, int embed_dtype, int d,
     float* __restrict__ h_out, const float* __restrict__ gain, float eps, void* __restrict__ x_out, int x_mode,
     const float* __restrict__ h_in, int64_t ld_h, int64_t rows) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + warp;
-  if (row >= rows) return;
+  __shared__ float red[8];
+  const int lane = threadIdx.x;  // "lane" strides the row by 256 float4s
+  const int64_t row = blockIdx.x;
   const int n4 = d >> 2;
   const int64_t tok = h_in ? 0 : ids[row];
   float4 v[V];
   float ss = 0.f;
 #pragma unroll
   for (int k = 0; k < V; ++k) {
-    const int c = lane + 32 * k;
+    const int c = lane + 256 * k;
     v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c < n4) {
       if (h_in) {
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(256) rmsnorm_warp_kernel(
   }
 #pragma unroll
   for (int k = 0; k < V; ++k) {
-    const int c = lane + 32 * k;
+    const int c = lane + 256 * k;
     if (c < n4) {
       if (!h_in && h_out) *reinterpret_cast<float4*>(h_out + row * d + 4 * c) = v[k];
       ss = fmaf(v[k].x, v[k].x, ss);
@@ -310,10 +310,15 @@ __global__ void __launch_bounds__(256) rmsnorm_warp_kernel(
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((lane & 31) == 0) red[lane >> 5] = ss;
+  __syncthreads();
+  ss = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) ss += red[w];
   const float r = __fsqrt_rn(__fadd_rn(__fdiv_rn(ss, (float)d), eps));
 #pragma unroll
   for (int k = 0; k < V; ++k) {
-    const int c = lane + 32 * k;
+    const int c = lane + 256 * k;
     if (c < n4) {
       const float4 g = __ldg(reinterpret_cast<const float4*>(gain) + c);
       const float y[4] = {__fmul_rn(__fdiv_rn(v[k].x, r), g.x), __fmul_rn(__fdiv_rn(v[k].y, r), g.y),
@@ -326,20 +331,18 @@ __global__ void __launch_bounds__(256) rmsnorm_warp_kernel(
 static void launch_rmsnorm(const int64_t* ids, const void* embed, int embed_dtype, int d, float* h_out,
                            const float* gain, float eps, void* x_out, int x_mode, const float* h_in, int64_t ld_h,
                            int64_t rows, cudaStream_t st) {
-  const int per_lane = (d / 4 + 31) / 32;
-  const unsigned grid = (unsigned)((rows + 7) / 8);
+  const int per_lane = (d / 4 + 255) / 256;
+  const unsigned grid = (unsigned)rows;
 #define CC_NORM_CASE(V)                                                                                        \
   if (per_lane <= V) {                                                                                         \
     rmsnorm_warp_kernel<V><<<grid, 256, 0, st>>>(ids, embed, embed_dtype, d, h_out, gain, eps, x_out, x_mode, \
                                                  h_in, ld_h, rows);                                            \
     return;                                                                                                    \
   }
+  CC_NORM_CASE(1)
   CC_NORM_CASE(2)
+  CC_NORM_CASE(4)
   CC_NORM_CASE(8)
-  CC_NORM_CASE(16)
-  CC_NORM_CASE(32)
-  CC_NORM_CASE(48)
-  CC_NORM_CASE(64)
 #undef CC_NORM_CASE
 }
 
