@@ -26,7 +26,7 @@ i32, i64, f32, vp = ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_voi
 
 class KvSegment(ctypes.Structure):
     _fields_ = [("k", vp), ("v", vp), ("src_rows", i64), ("src_row0", i64),
-                ("dst_row0", i64), ("n_rows", i64)]
+                ("dst_row0", i64), ("n_rows", i64), ("pos0", i64)]
 
 
 class BankSeq(ctypes.Structure):
@@ -88,6 +88,9 @@ _SIGS = {
     "cc_convert_matrix": ([vp, i64, i64, vp, i32, i32, vp], i32),
     "cc_gemm": ([ctypes.POINTER(GemmArgs), vp], i32),
     "cc_sparse_row_attention": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),
+    "cc_sparse_row_attention_partial": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, vp, vp], i32),
+    "cc_local_limits": ([vp, i64, vp, i64, vp, vp], i32),
+    "cc_lse_merge": ([vp, vp, i32, i64, i64, i32, i32, vp, i64, i32, vp], i32),
     "cc_sparse_row_attention_mma": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),
     "cc_banked_attention_f32": ([vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, f32, vp, i32, vp, i64, i64, vp], i32),
     "cc_reduce_scores": ([vp, i32, i32, i32, i64, vp, vp, i64, vp, vp], i32),

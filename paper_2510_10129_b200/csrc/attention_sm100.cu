@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
                          const __nv_bfloat16* __restrict__ q, int64_t ldq, const int64_t* __restrict__ pos, int64_t m,
                          int64_t n_keys, int n_q_heads, int n_kv_heads, float factor,
                          const float* __restrict__ row_factor, __nv_bfloat16* __restrict__ out, int64_t ldo,
-                         int n_ctas) {
+                         int n_ctas, float* __restrict__ o_part, float* __restrict__ lse_part) {
   using Cfg = FaCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   const int r = quarter * 32 + lane;                // row within the tile
   int lim = 0;
   float scale2 = 0.f;
-  int64_t out_off = -1;
+  int64_t out_off = -1, part_row = -1;
   if (warp >= 2) {
     const int64_t p = p0 + tq * kFaTileRows + r;
     const uint4 zero = make_uint4(0, 0, 0, 0);
@@ -196,6 +196,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     if (p < packed_total) {
       const int64_t i = p / G;
       const int head = kvh * G + (int)(p % G);
+      part_row = i * n_q_heads + head;
       lim = (int)min(pos[i] + 1, n_keys);
       scale2 = (row_factor ? row_factor[i] : factor) * 1.4426950408889634f;
       src = reinterpret_cast<const uint4*>(q + i * ldq + (int64_t)head * D);
@@ -366,11 +367,23 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       tc_fence_after();
     }
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    if (o_part && part_row >= 0)  // split-KV partial: log2-domain LSE of this shard's keys
+      lse_part[part_row] = (l_run > 0.f && m_run != -INFINITY) ? m_run + __log2f(l_run) : -INFINITY;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
       float ov[32];
       tmem_ld32(o_addr + c * 32, ov);
-      if (out_off >= 0) {
+      if (o_part) {
+        if (part_row >= 0) {
+          float4* dst = reinterpret_cast<float4*>(o_part + part_row * D + c * 32);
+          const bool live = l_run > 0.f && n_tiles > 0;
+#pragma unroll
+          for (int qd = 0; qd < 8; ++qd)
+            dst[qd] = live ? make_float4(ov[4 * qd] * inv, ov[4 * qd + 1] * inv, ov[4 * qd + 2] * inv,
+                                         ov[4 * qd + 3] * inv)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      } else if (out_off >= 0) {
         uint4* dst = reinterpret_cast<uint4*>(out + out_off + c * 32);
 #pragma unroll
         for (int qd = 0; qd < 4; ++qd)
@@ -419,7 +432,8 @@ static int make_kv_map(CUtensorMap* map, const void* base, int64_t n_keys, int h
 template <int D>
 static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64_t m, const void* k_cache,
                      const void* v_cache, int64_t n_keys, int32_t hq, int32_t hkv, float factor,
-                     const float* row_factor, void* out, int64_t ldo, cudaStream_t st, double flops) {
+                     const float* row_factor, void* out, int64_t ldo, cudaStream_t st, double flops,
+                     float* o_part = nullptr, float* lse_part = nullptr) {
   CUtensorMap tk, tv;
   int rc = make_kv_map(&tk, k_cache, n_keys, hkv, D);
   if (rc) return rc;
@@ -436,9 +450,63 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64
   ProfScope ps(st, OP_ATTENTION, flops);
   fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
       tk, tv, (const __nv_bfloat16*)q, ldq, positions, m, n_keys, hq, hkv, factor, row_factor,
-      (__nv_bfloat16*)out, ldo, n_ctas);
+      (__nv_bfloat16*)out, ldo, n_ctas, o_part, lse_part);
   CC_LAUNCH_CHECK("fa_sparse_row");
   return CC_OK;
+}
+
+// Split-KV merge: one warp per (row, head), lanes over head_dim.
+__global__ void lse_merge_kernel(const float* __restrict__ o_parts, const float* __restrict__ lse_parts, int n_parts,
+                                 int64_t part_stride, int64_t m, int hq, int d, void* __restrict__ out, int64_t ldo,
+                                 int out_dtype) {
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gw >= m * hq) return;
+  const int64_t i = gw / hq;
+  const int h = (int)(gw % hq);
+  float mx = -INFINITY;
+  for (int w = 0; w < n_parts; ++w) mx = fmaxf(mx, lse_parts[(w * part_stride + i) * hq + h]);
+  float wsum = 0.f;
+  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // d <= 256
+  for (int w = 0; w < n_parts; ++w) {
+    const float l = lse_parts[(w * part_stride + i) * hq + h];
+    if (l == -INFINITY) continue;
+    const float a = exp2f(l - mx);
+    wsum += a;
+    const float* o = o_parts + ((w * part_stride + i) * hq + h) * (int64_t)d;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (lane + 32 * k < d) acc[k] = fmaf(a, o[lane + 32 * k], acc[k]);
+  }
+  const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int c = lane + 32 * k;
+    if (c >= d) continue;
+    const int64_t off = i * ldo + (int64_t)h * d + c;
+    if (out_dtype == CC_BF16)
+      reinterpret_cast<__nv_bfloat16*>(out)[off] = __float2bfloat16_rn(acc[k] * inv);
+    else
+      reinterpret_cast<float*>(out)[off] = acc[k] * inv;
+  }
+}
+
+__global__ void fill_neg_inf_kernel(float* __restrict__ p, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = -INFINITY;
+}
+
+__global__ void local_limits_kernel(const int64_t* __restrict__ row_pos, int64_t m,
+                                    const int64_t* __restrict__ local_pos, int64_t n, int64_t* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const int64_t p = row_pos[i];
+  int64_t lo = 0, hi = n;  // first index with local_pos > p
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (local_pos[mid] <= p) lo = mid + 1; else hi = mid;
+  }
+  out[i] = lo - 1;
 }
 
 }  // namespace cc
@@ -467,4 +535,48 @@ extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t
                           out, ldo, st, g_attn_flops);
   return fa_launch<64>(q, ldq, positions, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
                        out, ldo, st, g_attn_flops);
+}
+
+extern "C" int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const int64_t* limits, int64_t m,
+                                               const void* k_cache, const void* v_cache, int64_t n_keys,
+                                               int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim, float factor,
+                                               const float* row_factor, float* o_part, float* lse, void* stream) {
+  CC_CHECK_ARG(n_kv_heads > 0 && n_q_heads % n_kv_heads == 0, CC_ERR_DIMENSION, "bad head counts");
+  CC_CHECK_ARG(head_dim == 64 || head_dim == 128, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
+  CC_CHECK_ARG(o_part && lse, CC_ERR_VALUE, "partial attention needs o_part and lse outputs");
+  if (m <= 0) return CC_OK;
+  cudaStream_t st = as_stream(stream);
+  if (n_keys <= 0) {  // an empty shard contributes nothing: O = 0, LSE = -inf
+    cudaMemsetAsync(o_part, 0, (size_t)m * n_q_heads * head_dim * sizeof(float), st);
+    const int64_t n = m * n_q_heads;
+    fill_neg_inf_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(lse, n);
+    CC_LAUNCH_CHECK("partial attention (empty shard)");
+    return CC_OK;
+  }
+  if (head_dim == 128)
+    return fa_launch<128>(q, ldq, limits, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
+                          nullptr, 0, st, g_attn_flops, o_part, lse);
+  return fa_launch<64>(q, ldq, limits, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
+                       nullptr, 0, st, g_attn_flops, o_part, lse);
+}
+
+extern "C" int cc_local_limits(const int64_t* row_pos, int64_t m, const int64_t* local_pos, int64_t n_local,
+                               int64_t* limits, void* stream) {
+  if (m <= 0) return CC_OK;
+  local_limits_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(row_pos, m, local_pos, n_local,
+                                                                                  limits);
+  CC_LAUNCH_CHECK("local_limits");
+  return CC_OK;
+}
+
+extern "C" int cc_lse_merge(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t part_stride,
+                            int64_t m, int32_t n_q_heads, int32_t head_dim, void* out, int64_t ldo, int32_t out_dtype,
+                            void* stream) {
+  CC_CHECK_ARG(head_dim > 0 && head_dim <= 256, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
+  if (m <= 0 || n_parts <= 0) return CC_OK;
+  const int64_t warps = m * n_q_heads;
+  lse_merge_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(
+      o_parts, lse_parts, n_parts, part_stride, m, n_q_heads, head_dim, out, ldo, out_dtype);
+  CC_LAUNCH_CHECK("lse_merge");
+  return CC_OK;
 }

@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const cc_kv_segment* __re
   T* vd = copy_v ? dst_v + row * row_elems + col : nullptr;
   const int64_t dst_layer = dst_rows_cap * row_elems;
 
-  const double pos = (double)(row + pos_offset);
+  const double pos = (double)(sg.pos0 + (row - sg.dst_row0) + pos_offset);
   float c[V / 2], s[V / 2];
 #pragma unroll
   for (int p = 0; p < V / 2; ++p) {

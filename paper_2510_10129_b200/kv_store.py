@@ -126,9 +126,11 @@ def _dtype_code(dt: torch.dtype) -> int:
 
 def _segments(spec) -> np.ndarray:
     """[(chunk, src_row0, dst_row0, n_rows)] -> packed cc_kv_segment bytes."""
-    arr = np.empty((len(spec), 6), dtype=np.int64)  # == cc_kv_segment (6 x 8 bytes)
-    for i, (c, s0, d0, n) in enumerate(spec):
-        arr[i] = (c.k.data_ptr(), c.v.data_ptr(), c.n_rows, s0, d0, n)
+    arr = np.empty((len(spec), 7), dtype=np.int64)  # == cc_kv_segment (7 x 8 bytes)
+    for i, item in enumerate(spec):
+        c, s0, d0, n = item[:4]
+        pos0 = item[4] if len(item) > 4 else d0  # RoPE position of the first row
+        arr[i] = (c.k.data_ptr(), c.v.data_ptr(), c.n_rows, s0, d0, n, pos0)
     return arr.view(np.uint8).reshape(-1)
 
 

@@ -64,6 +64,37 @@ def gemm(kind: int, epilogue: int, M: int, N: int, K: int, A: torch.Tensor, B: t
     _lib.call("cc_gemm", ctypes.byref(a), _s())
 
 
+def rope_table(model: Model, positions: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """Per-row fp32 cos/sin tables (float64 angles, tensor_core.py:41-51)."""
+    c = model.config
+    n = positions.numel()
+    cos = torch.empty(n, c.d_head // 2, dtype=torch.float32, device=positions.device)
+    sin = torch.empty_like(cos)
+    inv = c.rope.inv_freq
+    _lib.call("cc_rope_table", positions.data_ptr(), n, inv.ctypes.data, c.d_head, cos.data_ptr(), sin.data_ptr(),
+              _s())
+    return cos, sin
+
+
+def _mlp(model: Model, lw, h: torch.Tensor, x: torch.Tensor, act_buf: torch.Tensor, kind: int, x_mode: int) -> None:
+    """RMSNorm(h) -> gate/up GEMM (fused activation) -> down GEMM + residual, for
+    Python-driven layer loops (the sequence-sharded path)."""
+    c = model.config
+    R, d = h.shape
+    if R == 0:
+        return
+    _lib.call("cc_rmsnorm", h.data_ptr(), R, d, d, lw.mlp_norm.data_ptr(), c.norm_eps, x.data_ptr(), x_mode, _s())
+    act = _lib.CC_ACT_SILU if c.activation == "silu" else _lib.CC_ACT_GELU_TANH
+    if c.mlp_gated:
+        gemm(kind, _lib.CC_EPI_GLU, R, lw.w_up.shape[0], d, x, lw.w_up, bias=lw.b_up, C=act_buf, ldc=c.d_ff,
+             c_mode=x_mode, act=act, n_out=c.d_ff)
+    else:
+        gemm(kind, _lib.CC_EPI_ACT, R, c.d_ff, d, x, lw.w_up, bias=lw.b_up, C=act_buf, ldc=c.d_ff, c_mode=x_mode,
+             act=act)
+    gemm(kind, _lib.CC_EPI_RESIDUAL, R, d, c.d_ff, act_buf, lw.w_down, bias=lw.b_down, C=h, ldc=d,
+         c_mode=_lib.CC_F32)
+
+
 def _layer_stride(t: torch.Tensor | None) -> int:
     """Bytes between consecutive layers of a [L, rows, H, D] tensor (0 for a
     single shared [rows, H, D] buffer)."""

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_struct_layouts_match_header():
     from paper_2510_10129_b200 import _lib
-    assert ctypes.sizeof(_lib.KvSegment) == 48
+    assert ctypes.sizeof(_lib.KvSegment) == 56
     assert ctypes.sizeof(_lib.BankSeq) == 40
 
 
