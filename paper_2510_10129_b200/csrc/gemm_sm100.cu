@@ -97,6 +97,23 @@ __device__ __forceinline__ void store_row32(void* base, int mode, int64_t row, i
     }
   } else {  // CC_F32_SPLIT3 : [hi | hi | lo]
     float* p = reinterpret_cast<float*>(base) + row * ld * 3 + col0;
+    if (full && ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && (width & 3) == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float hi[4], lh[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float lo, ll;
+          split_tf32(v[4 * q + e], hi[e], lo);
+          split_tf32(lo, lh[e], ll);
+        }
+        const float4 h4 = make_float4(hi[0], hi[1], hi[2], hi[3]);
+        reinterpret_cast<float4*>(p)[q] = h4;
+        reinterpret_cast<float4*>(p + width)[q] = h4;
+        reinterpret_cast<float4*>(p + 2 * width)[q] = make_float4(lh[0], lh[1], lh[2], lh[3]);
+      }
+      return;
+    }
     for (int j = 0; j < 32; ++j) {
       if (col0 + j < width) {
         float hi, lo, lh, ll;
