@@ -59,20 +59,47 @@ __global__ void __launch_bounds__(kBkThreads) banked_f32_kernel(
   };
   const int tr = tid / 16, tc = tid % 16;  // 16 x 16 threads, 4 x 4 micro-tiles
 
+  // Tiles are register double-buffered: the next tile's loads are in flight
+  // while the current one is consumed from shared memory.
+  constexpr int LPT = kBkKeys * (HD / 4) / kBkThreads;  // float4 per thread per tile
+  float4 pre[LPT];
+  auto fetch_k = [&](int c0) {
+    const int nk = min(kBkKeys, ncols - c0);
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+      const int idx = tid + e * kBkThreads;
+      const int kk = idx % kBkKeys, d4 = idx / kBkKeys;
+      pre[e] = kk < nk ? *reinterpret_cast<const float4*>(kv_row(sq.k, k_new, c0 + kk) + 4 * d4)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  auto fetch_v = [&](int c0) {
+    const int nk = min(kBkKeys, ncols - c0);
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+      const int idx = tid + e * kBkThreads;
+      const int kk = idx / (HD / 4), d4 = idx % (HD / 4);
+      pre[e] = kk < nk ? *reinterpret_cast<const float4*>(kv_row(sq.v, v_new, c0 + kk) + 4 * d4)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+
   // ---- phase 1: S^T = (K Q^T) * factor, masked (limit of row r = nb + i + 1)
+  fetch_k(0);
   for (int c0 = 0; c0 < ncols; c0 += kBkKeys) {
     const int nk = min(kBkKeys, ncols - c0);
     __syncthreads();
-    for (int idx = tid; idx < kBkKeys * (HD / 4); idx += kBkThreads) {
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+      const int idx = tid + e * kBkThreads;
       const int kk = idx % kBkKeys, d4 = idx / kBkKeys;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (kk < nk) v = *reinterpret_cast<const float4*>(kv_row(sq.k, k_new, c0 + kk) + 4 * d4);
-      tile[(4 * d4 + 0) * kBkKeys + kk] = v.x;
-      tile[(4 * d4 + 1) * kBkKeys + kk] = v.y;
-      tile[(4 * d4 + 2) * kBkKeys + kk] = v.z;
-      tile[(4 * d4 + 3) * kBkKeys + kk] = v.w;
+      tile[(4 * d4 + 0) * kBkKeys + kk] = pre[e].x;
+      tile[(4 * d4 + 1) * kBkKeys + kk] = pre[e].y;
+      tile[(4 * d4 + 2) * kBkKeys + kk] = pre[e].z;
+      tile[(4 * d4 + 3) * kBkKeys + kk] = pre[e].w;
     }
     __syncthreads();
+    if (c0 + kBkKeys < ncols) fetch_k(c0 + kBkKeys);
     float acc[4][4] = {};
 #pragma unroll 8
     for (int d = 0; d < HD; ++d) {
@@ -100,6 +127,8 @@ __global__ void __launch_bounds__(kBkThreads) banked_f32_kernel(
     }
   }
   __syncthreads();
+
+  if (!weights_out) fetch_v(0);  // first V tile in flight during the softmax
 
   // ---- phase 2: softmax per row (tensor_core.py:88-96): 4 threads per row,
   // columns interleaved, partial max / sum combined with quad shuffles -------
@@ -142,13 +171,14 @@ __global__ void __launch_bounds__(kBkThreads) banked_f32_kernel(
   for (int c0 = 0; c0 < ncols; c0 += kBkKeys) {
     const int nk = min(kBkKeys, ncols - c0);
     __syncthreads();
-    for (int idx = tid; idx < kBkKeys * (HD / 4); idx += kBkThreads) {
+#pragma unroll
+    for (int e = 0; e < LPT; ++e) {
+      const int idx = tid + e * kBkThreads;
       const int kk = idx / (HD / 4), d4 = idx % (HD / 4);
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (kk < nk) v = *reinterpret_cast<const float4*>(kv_row(sq.v, v_new, c0 + kk) + 4 * d4);
-      *reinterpret_cast<float4*>(tile + kk * HD + 4 * d4) = v;
+      *reinterpret_cast<float4*>(tile + kk * HD + 4 * d4) = pre[e];
     }
     __syncthreads();
+    if (c0 + kBkKeys < ncols) fetch_v(c0 + kBkKeys);
     for (int kk = 0; kk < nk; ++kk) {
       const float4 w = *reinterpret_cast<const float4*>(sT + (size_t)(c0 + kk) * kBkRows + 4 * tr);
       const float wv[4] = {w.x, w.y, w.z, w.w};
