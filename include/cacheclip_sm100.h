@@ -277,6 +277,9 @@ typedef struct {
   const int64_t* raw_rows;
   const void* attn_k; int64_t attn_k_stride;
   const void* attn_v; int64_t attn_v_stride;
+  void* const* layer_ready;             /* optional host array of cudaEvent_t: layer l's
+                                           QKV/attention wait for layer_ready[l] (a merge
+                                           still streaming in on another stream) */
 } cc_kv_plan;
 
 /* Last-layer scoring (selector.py:157-165): weights workspace

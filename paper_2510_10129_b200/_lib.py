@@ -69,7 +69,8 @@ class ModelDesc(ctypes.Structure):
 class KvPlan(ctypes.Structure):
     _fields_ = [("k_scatter", vp), ("k_scatter_stride", i64), ("v_scatter", vp), ("v_scatter_stride", i64),
                 ("dst_rows", vp), ("k_raw", vp), ("k_raw_stride", i64), ("raw_rows", vp),
-                ("attn_k", vp), ("attn_k_stride", i64), ("attn_v", vp), ("attn_v_stride", i64)]
+                ("attn_k", vp), ("attn_k_stride", i64), ("attn_v", vp), ("attn_v_stride", i64),
+                ("layer_ready", ctypes.POINTER(vp))]
 
 
 class ScoreSpec(ctypes.Structure):

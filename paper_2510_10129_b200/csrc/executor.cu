@@ -137,6 +137,10 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
   };
   for (int l = 0; l < md->n_layers; ++l) {
     const cc_layer_weights& lw = md->layers[l];
+    if (plan->layer_ready && plan->layer_ready[l]) {
+      const cudaError_t e = cudaStreamWaitEvent(as_stream(stream), (cudaEvent_t)plan->layer_ready[l], 0);
+      if (e != cudaSuccess) return fail(CC_ERR_CUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
+    }
     if (l == 0)
       CC_TRY(cc_embed_rmsnorm(ids, R, md->embed, CC_BF16, md->vocab, (int)d, h, lw.attn_norm, md->norm_eps, x,
                               CC_BF16, stream));

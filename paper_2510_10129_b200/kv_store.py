@@ -168,6 +168,7 @@ class MergedCache:
         self.model_fingerprint = model_fingerprint
         self.recomputed_rows = tuple(recomputed_rows)
         self._ids_dev = None
+        self.layer_ready = None  # per-layer events while a streamed merge is in flight
         if self._n_rows != len(self.token_ids) or (self._source is not None and self._n_rows != len(self._source)):
             raise CacheConsistencyError("rows, token ids, and source map disagree")
 
@@ -255,10 +256,13 @@ def compute_positions(chunk_lens: Sequence[int], prefix_len: int) -> np.ndarray:
 
 
 def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: PipelineTrace | None = None,
-                 *, capacity: int | None = None) -> MergedCache:
+                 *, capacity: int | None = None, device=None) -> MergedCache:
     """Concatenate chunk caches keeping only the first copy of the prefix and
     rotate keys to global positions in one HBM pass (kv_store.py:193-258).
-    ``capacity`` reserves rows for in-place appends (query rows)."""
+    ``capacity`` reserves rows for in-place appends (query rows). Chunk caches
+    may also be host-resident (pinned): they are then streamed in layer by
+    layer onto ``device`` and ``MergedCache.layer_ready`` holds one event per
+    layer for consumers that overlap with the transfer."""
     if not chunks:
         raise CacheConsistencyError("nothing to merge")
     first = chunks[0]
@@ -291,17 +295,47 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
             spec.append((c, s0, dst, n))
         dst += n
     L, H, D = first.n_layers, geom[0], geom[1]
-    k_store = torch.empty(L, cap, H, D, dtype=first.k.dtype, device=first.k.device)
+    streamed = not first.k.is_cuda
+    if streamed and device is None:
+        raise CacheConsistencyError("host-resident chunk caches need a target device")
+    dev = torch.device(device) if streamed else first.k.device
+    k_store = torch.empty(L, cap, H, D, dtype=first.k.dtype, device=dev)
     v_store = torch.empty_like(k_store)
-    if total:
-        segs = host_to_device(_segments(spec), first.k.device)
+    layer_ready = None
+    if total and not streamed:
+        segs = host_to_device(_segments(spec), dev)
         inv = rope.inv_freq
         _lib.call("cc_assemble_kv", segs.data_ptr(), len(spec), total, L, H, D, _dtype_code(first.k.dtype),
-                  inv.ctypes.data, 0, k_store.data_ptr(), v_store.data_ptr(), cap, _stream(),
-                  meta={"bytes": 2.0 * 2 * total * L * H * D * first.k.element_size()})
+                  inv.ctypes.data, 0, k_store.data_ptr(), v_store.data_ptr(), cap, _stream())
+    elif total:
+        # Host-resident (pinned) chunk caches: the assembly kernel reads them
+        # straight over PCIe (zero-copy), one layer per launch, and each layer
+        # records an event so a consumer can start on layer l while later
+        # layers are still streaming in.
+        for i, c in enumerate(chunks):
+            if not (c.k.is_pinned() and c.v.is_pinned()):
+                raise CacheConsistencyError(f"chunk {i}: host caches must be in pinned memory")
+        base = _segments(spec).view(np.int64).reshape(len(spec), 7)
+        per_layer = np.repeat(base[None], L, axis=0)
+        for si, (c, *_rest) in enumerate(spec):
+            per_layer[:, si, 0] += np.arange(L, dtype=np.int64) * c.k.stride(0) * c.k.element_size()
+            per_layer[:, si, 1] += np.arange(L, dtype=np.int64) * c.v.stride(0) * c.v.element_size()
+        segs = host_to_device(per_layer.reshape(-1).view(np.uint8), dev)
+        seg_bytes = len(spec) * 7 * 8
+        inv = rope.inv_freq
+        layer_ready = []
+        for layer in range(L):
+            _lib.call("cc_assemble_kv", segs.data_ptr() + layer * seg_bytes, len(spec), total, 1, H, D,
+                      _dtype_code(first.k.dtype), inv.ctypes.data, 0, k_store[layer].data_ptr(),
+                      v_store[layer].data_ptr(), cap, _stream())
+            ev = torch.cuda.Event()
+            ev.record()
+            layer_ready.append(ev)
     if trace is not None:
         for _ in range(L):
             trace.rope("merge_overhead", total * H, D)
     # source map is derived lazily from the layout (MergedCache.source)
-    return MergedCache(k_store, v_store, total, token_ids, MergeLayout(sink, lens), None,
-                       first.tokenizer_id, first.model_fingerprint)
+    merged = MergedCache(k_store, v_store, total, token_ids, MergeLayout(sink, lens), None,
+                         first.tokenizer_id, first.model_fingerprint)
+    merged.layer_ready = layer_ready
+    return merged

@@ -189,9 +189,11 @@ def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | No
     rf = _row_factor(model, knobs, nq, m, dev)
     ks, vs = cache.k_store, cache.v_store
     pairs = (int(np.sum(sel_idx + 1)) if m else 0) + (visible_pairs(nq, base) if nq else 0)
-    plan = KvPlan(k_scatter=ks, v_scatter=vs, attn_k=ks, attn_v=vs, dst_rows=pos)
+    plan = KvPlan(k_scatter=ks, v_scatter=vs, attn_k=ks, attn_v=vs, dst_rows=pos,
+                  layer_ready=getattr(cache, "layer_ready", None))
     res = forward_rows(model, ids, pos, plan, base + nq, row_factor=rf, want_logits=want_logits and nq > 0,
                        pairs=pairs)
+    cache.layer_ready = None  # every layer is now ordered before this stream's work
     if trace is not None:
         for _ in range(c.n_layers):
             if m:

@@ -114,12 +114,17 @@ class KvPlan:
     dst_rows: torch.Tensor | None = None
     k_raw: torch.Tensor | None = None
     raw_rows: torch.Tensor | None = None
+    layer_ready: list | None = None   # torch.cuda.Event per layer (streamed merge) or None
 
     def to_c(self) -> _lib.KvPlan:
+        ready = None
+        if self.layer_ready:
+            self._ready_arr = (ctypes.c_void_p * len(self.layer_ready))(*[e.cuda_event for e in self.layer_ready])
+            ready = ctypes.cast(self._ready_arr, ctypes.POINTER(ctypes.c_void_p))
         return _lib.KvPlan(_p(self.k_scatter), _layer_stride(self.k_scatter), _p(self.v_scatter),
                            _layer_stride(self.v_scatter), _p(self.dst_rows), _p(self.k_raw),
                            _layer_stride(self.k_raw), _p(self.raw_rows), _p(self.attn_k), _layer_stride(self.attn_k),
-                           _p(self.attn_v), _layer_stride(self.attn_v))
+                           _p(self.attn_v), _layer_stride(self.attn_v), ready)
 
 
 @dataclass

@@ -318,3 +318,39 @@ def test_lm_head_argmax():
     ref = W.double() @ x
     assert (logits.double() - ref).abs().max().item() < 1e-3
     assert int(am.item()) == int(torch.argmax(logits).item())
+
+
+def test_streamed_merge_from_pinned_host_matches_device_merge():
+    """Host-resident (pinned) chunk caches are merged straight from host memory
+    layer by layer (zero-copy reads, per-layer events) — bitwise equal to the
+    device-resident merge; the pipeline result is identical too."""
+    import paper_2510_10129_b200 as cc
+    from oracle.synth import C1_EXACT as w
+    cfgp = cc.ModelConfig(n_layers=w.primary.n_layers, n_heads=w.primary.n_heads, d_model=w.primary.d_model,
+                          d_head=w.primary.d_head, d_ff=w.primary.d_ff, vocab_size=w.primary.vocab_size,
+                          rope_base=w.primary.rope_base, activation="silu", mlp_gated=True,
+                          n_kv_heads=w.primary.kv_heads, dtype="bf16", tokenizer_id="chars")
+    cfga = cc.ModelConfig(n_layers=w.aux.n_layers, n_heads=w.aux.n_heads, d_model=w.aux.d_model,
+                          d_head=w.aux.d_head, d_ff=w.aux.d_ff, vocab_size=w.aux.vocab_size,
+                          rope_base=w.aux.rope_base, activation="silu", mlp_gated=True,
+                          n_kv_heads=w.aux.kv_heads, dtype="fp32", tokenizer_id="chars")
+    primary = cc.from_params(cfgp, orc.seeded_params(w.primary, 0))
+    aux = cc.from_params(cfga, orc.seeded_params(w.aux, 1))
+    prefix, chunk_ids, query = w.token_ids(0)
+    chunks = [cc.prefill_chunk(primary, prefix, c) for c in chunk_ids]
+    aux_chunks = [cc.prefill_chunk(aux, prefix, c) for c in chunk_ids]
+    host = [cc.ChunkCache(c.k.cpu().pin_memory(), c.v.cpu().pin_memory(), c.token_ids, c.prefix_len,
+                          c.tokenizer_id, c.model_fingerprint) for c in chunks]
+    host_aux = [cc.ChunkCache(c.k.cpu().pin_memory(), c.v.cpu().pin_memory(), c.token_ids, c.prefix_len,
+                              c.tokenizer_id, c.model_fingerprint) for c in aux_chunks]
+    a = cc.merge_caches(chunks, primary.config.rope, capacity=2000)
+    b = cc.merge_caches(host, primary.config.rope, capacity=2000, device=DEV)
+    assert b.layer_ready is not None and len(b.layer_ready) == primary.config.n_layers
+    torch.cuda.synchronize()
+    for l in range(primary.config.n_layers):
+        assert torch.equal(a.keys[l], b.keys[l]) and torch.equal(a.values[l], b.values[l])
+    cfg = cc.SelectionConfig(w.ratio, w.window_len, w.window_threshold)
+    r1 = cc.cacheclip_prefill(primary, aux, chunks, aux_chunks, query, cfg)
+    r2 = cc.cacheclip_prefill(primary, aux, host, host_aux, query, cfg)
+    assert r1.plan.indices == r2.plan.indices
+    np.testing.assert_array_equal(r1.logits, r2.logits)
