@@ -140,9 +140,11 @@ __global__ void __launch_bounds__(256) assemble_kernel(const cc_kv_segment* __re
                                                        int64_t dst_rows_cap, int copy_v) {
   constexpr int V = Vec16<T>::N;
   const int vecs_per_row = kv_heads * head_dim / V;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // grid-stride: a full grid does one pass; a capped grid (streaming from
+  // host memory) keeps PCIe saturated while occupying only a few SMs
+  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < n_dst_rows * vecs_per_row;
+       gid += (int64_t)gridDim.x * blockDim.x) {
   const int64_t row = gid / vecs_per_row;
-  if (row >= n_dst_rows) return;
   const int vi = (int)(gid - row * vecs_per_row);
   const int col = vi * V;               // element offset inside the row
   const int pair0 = (col % head_dim) / 2;
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(const cc_kv_segment* __re
 #pragma unroll
     for (int p = 0; p < V / 2; ++p) rope_pair(x[2 * p], x[2 * p + 1], c[p], s[p], y[2 * p], y[2 * p + 1]);
     store_vec<T>(kd + l * dst_layer, y);
+  }
   }
 }
 
@@ -486,9 +489,22 @@ int cc_device_check(int dev) {
   return CC_OK;
 }
 
+int cc_assemble_kv_capped(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows, int32_t n_layers,
+                          int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
+                          int64_t pos_offset, void* dst_k, void* dst_v, int64_t dst_rows_cap, int32_t max_ctas,
+                          void* stream);
+
 int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows, int32_t n_layers,
                    int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
                    int64_t pos_offset, void* dst_k, void* dst_v, int64_t dst_rows_cap, void* stream) {
+  return cc_assemble_kv_capped(segs_dev, n_segs, n_dst_rows, n_layers, kv_heads, head_dim, dtype, inv_freq_host,
+                               pos_offset, dst_k, dst_v, dst_rows_cap, 0, stream);
+}
+
+int cc_assemble_kv_capped(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows, int32_t n_layers,
+                          int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
+                          int64_t pos_offset, void* dst_k, void* dst_v, int64_t dst_rows_cap, int32_t max_ctas,
+                          void* stream) {
   CC_CHECK_ARG(segs_dev && n_segs > 0, CC_ERR_CONSISTENCY, "nothing to merge");
   CC_CHECK_ARG(n_layers > 0 && kv_heads > 0, CC_ERR_DIMENSION, "bad geometry");
   CC_CHECK_ARG(n_dst_rows <= dst_rows_cap, CC_ERR_DIMENSION, "destination capacity %lld < rows %lld",
@@ -504,7 +520,8 @@ int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_
   const int64_t threads = n_dst_rows * (int64_t)(kv_heads * head_dim / V);
   ProfScope ps(as_stream(stream), OP_ASSEMBLE, 2.0 * 2 * n_dst_rows * n_layers * kv_heads * head_dim * (dtype == CC_BF16 ? 2 : 4));
   const int bs = 256;
-  const int64_t grid = (threads + bs - 1) / bs;
+  int64_t grid = (threads + bs - 1) / bs;
+  if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
   if (dtype == CC_BF16) {
     assemble_kernel<__nv_bfloat16><<<grid, bs, 0, as_stream(stream)>>>(
         segs_dev, n_segs, n_dst_rows, n_layers, kv_heads, head_dim, inv, pos_offset,

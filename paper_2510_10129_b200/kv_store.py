@@ -120,6 +120,12 @@ class ChunkCache:
         return list(zip(k.unbind(0), self.v.unbind(0)))
 
 
+# CTAs of the zero-copy (host -> device) streamed merge: ~24 x 256 threads x
+# 32 B keeps > 150 KB in flight (PCIe Gen5 x16 latency-bandwidth product)
+# while leaving the other SMs to the scoring / recompute kernels.
+STREAM_CTAS = 24
+
+
 def _dtype_code(dt: torch.dtype) -> int:
     return _lib.CC_BF16 if dt == torch.bfloat16 else _lib.CC_F32
 
@@ -325,9 +331,9 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
         inv = rope.inv_freq
         layer_ready = []
         for layer in range(L):
-            _lib.call("cc_assemble_kv", segs.data_ptr() + layer * seg_bytes, len(spec), total, 1, H, D,
+            _lib.call("cc_assemble_kv_capped", segs.data_ptr() + layer * seg_bytes, len(spec), total, 1, H, D,
                       _dtype_code(first.k.dtype), inv.ctypes.data, 0, k_store[layer].data_ptr(),
-                      v_store[layer].data_ptr(), cap, _stream())
+                      v_store[layer].data_ptr(), cap, STREAM_CTAS, _stream())
             ev = torch.cuda.Event()
             ev.record()
             layer_ready.append(ev)
