@@ -17,6 +17,7 @@ from .flops import (STAGES, FlopReport, PipelineTrace, count_flops, event_macs, 
 from .kv_store import ChunkCache, MergedCache, MergeLayout, compute_positions, merge_caches
 from .model import (LayerCache, PrefillResult, decode_step, extend_cache, peek_forward, prefill_chunk,
                     prefill_full, selective_forward, visible_pairs)
+from .persist import CACHE_MAGIC, CACHE_VERSION, CACHE_VERSION_BF16, load_cache, save_cache
 from .pipeline import (STRATEGIES, ApeConfig, PrefillOutcome, ape_prefill, cacheclip_prefill,
                        direct_reuse_prefill, full_attention_prefill, reuse_context_ids)
 from .selector import (AuxSelection, ImportanceScores, SelectionConfig, SelectionPlan, WindowRecord,

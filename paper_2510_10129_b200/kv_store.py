@@ -162,8 +162,18 @@ class MergedCache:
 
     KEYS_ROTATED = True
 
-    def __init__(self, k_store: torch.Tensor, v_store: torch.Tensor, n_rows: int, token_ids, layout: MergeLayout,
-                 source, tokenizer_id: str, model_fingerprint: str, recomputed_rows=()) -> None:
+    def __init__(self, keys=None, values=None, token_ids=(), layout: MergeLayout | None = None, source=None,
+                 tokenizer_id: str = "", model_fingerprint: str = "", recomputed_rows=(), *,
+                 k_store: torch.Tensor | None = None, v_store: torch.Tensor | None = None,
+                 n_rows: int | None = None) -> None:
+        """Reference keyword form (keys/values per layer, kv_store.py:133-158), or
+        the internal storage form (k_store/v_store [L, capacity, H, D] + n_rows)."""
+        if k_store is None:
+            k_store = _as_layers(keys)
+            v_store = _as_layers(values, k_store.device)
+            if tuple(v_store.shape) != tuple(k_store.shape):
+                raise CacheConsistencyError(f"layer shape {tuple(v_store.shape)} != {tuple(k_store.shape)}")
+            n_rows = k_store.shape[1]
         self.k_store, self.v_store = k_store, v_store
         self._n_rows = int(n_rows)
         self.token_ids = list(token_ids)
@@ -250,9 +260,10 @@ class MergedCache:
                 self._ids_dev = None
 
     def copy(self) -> "MergedCache":
-        return MergedCache(self.k_store.clone(), self.v_store.clone(), self._n_rows, self.token_ids,
-                           self.layout, self._source, self.tokenizer_id, self.model_fingerprint,
-                           self.recomputed_rows)
+        return MergedCache(token_ids=self.token_ids, layout=self.layout, source=self._source,
+                           tokenizer_id=self.tokenizer_id, model_fingerprint=self.model_fingerprint,
+                           recomputed_rows=self.recomputed_rows, k_store=self.k_store.clone(),
+                           v_store=self.v_store.clone(), n_rows=self._n_rows)
 
 
 def compute_positions(chunk_lens: Sequence[int], prefix_len: int) -> np.ndarray:
@@ -341,7 +352,8 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
         for _ in range(L):
             trace.rope("merge_overhead", total * H, D)
     # source map is derived lazily from the layout (MergedCache.source)
-    merged = MergedCache(k_store, v_store, total, token_ids, MergeLayout(sink, lens), None,
-                         first.tokenizer_id, first.model_fingerprint)
+    merged = MergedCache(token_ids=token_ids, layout=MergeLayout(sink, lens), source=None,
+                         tokenizer_id=first.tokenizer_id, model_fingerprint=first.model_fingerprint,
+                         k_store=k_store, v_store=v_store, n_rows=total)
     merged.layer_ready = layer_ready
     return merged

@@ -119,7 +119,36 @@ def run(w: Workload, seed: int = 0) -> dict:
     )
 
 
+def write_reference_files() -> None:
+    """Small .cclp files written by the reference's own save_cache (format v1)."""
+    rng = np.random.default_rng(42)
+    heads, d_head, layers = 2, 4, 2
+    prefix = [1, 2]
+
+    def chunk(body):
+        n = len(prefix) + len(body)
+        return ref.ChunkCache(
+            keys=[rng.standard_normal((n, heads, d_head), dtype=np.float32) for _ in range(layers)],
+            values=[rng.standard_normal((n, heads, d_head), dtype=np.float32) for _ in range(layers)],
+            token_ids=prefix + list(body), prefix_len=len(prefix), tokenizer_id="t", model_fingerprint="m")
+
+    c0, c1 = chunk([10, 11, 12]), chunk([20, 21])
+    for c in (c1,):
+        for layer in range(layers):
+            c.keys[layer][:2] = c0.keys[layer][:2]
+            c.values[layer][:2] = c0.values[layer][:2]
+    ref.save_cache(c0, os.path.join(HERE, "ref_chunk.cclp"))
+    merged = ref.merge_caches([c0, c1], ref.RopeParams(d_head))
+    merged.recomputed_rows = (3,)
+    ref.save_cache(merged, os.path.join(HERE, "ref_merged.cclp"))
+    np.savez_compressed(os.path.join(HERE, "ref_files.npz"), chunk_token_ids=np.asarray(c0.token_ids),
+                        chunk_prefix_len=np.int64(c0.prefix_len), chunk_k=np.stack(c0.keys),
+                        chunk_v=np.stack(c0.values), merged_sink=np.int64(merged.layout.sink_len),
+                        merged_lens=np.asarray(merged.layout.chunk_lens), merged_k=np.stack(merged.keys))
+
+
 def main() -> None:
+    write_reference_files()
     for w in (C1, C1_EXACT, B1):
         out = run(w)
         path = os.path.join(HERE, f"{w.name}.npz")
