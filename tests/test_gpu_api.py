@@ -1,0 +1,110 @@
+"""Public API semantics on the device, mirroring the reference tests
+(test_model.py:161-305, test_pipeline.py): extend / peek / decode_step,
+selective_forward's validation-before-mutation rules, merge-layout fields."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cacheclip_oracle as orc
+from oracle.synth import C1
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import paper_2510_10129_b200 as cc
+    w = C1
+    oc = w.primary
+    cfg = cc.ModelConfig(n_layers=oc.n_layers, n_heads=oc.n_heads, d_model=oc.d_model, d_head=oc.d_head,
+                         d_ff=oc.d_ff, vocab_size=oc.vocab_size, rope_base=oc.rope_base, norm_eps=oc.norm_eps,
+                         activation=oc.activation, mlp_gated=oc.mlp_gated, n_kv_heads=oc.kv_heads, dtype="bf16",
+                         tokenizer_id="chars")
+    params = orc.seeded_params(oc, 0)
+    model = cc.from_params(cfg, params)
+    o_model = orc.OracleModel(oc, {k: (orc.round_to_bf16(v) if v.ndim == 2 else v) for k, v in params.items()})
+    rng = np.random.default_rng(5)
+    prefix = rng.integers(0, 512, 6).tolist()
+    chunk_ids = [rng.integers(0, 512, n).tolist() for n in (40, 57, 33)]
+    chunks = [cc.prefill_chunk(model, prefix, c) for c in chunk_ids]
+    return cc, model, o_model, prefix, chunk_ids, chunks
+
+
+def test_selective_forward_rejects_bad_selections(env):
+    cc, model, _, prefix, _, chunks = env
+    merged = cc.merge_caches(chunks, model.config.rope)
+    before = merged.keys[0].clone()
+    for bad in ((8, 8), (0,), (merged.n_rows,)):
+        with pytest.raises(ValueError):
+            cc.selective_forward(model, merged, bad)
+    assert torch.equal(merged.keys[0], before)  # nothing mutated
+    assert cc.selective_forward(model, merged, ()) is merged  # empty selection is a no-op
+
+
+def test_selective_forward_touches_only_selected_rows(env):
+    cc, model, _, _, _, chunks = env
+    merged = cc.merge_caches(chunks, model.config.rope)
+    untouched = [k.clone() for k in merged.keys]
+    picked = (7, 30, 61)
+    cc.selective_forward(model, merged, picked)
+    mask = torch.ones(merged.n_rows, dtype=torch.bool, device=untouched[0].device)
+    mask[list(picked)] = False
+    for layer in range(model.config.n_layers):
+        assert torch.equal(merged.keys[layer][mask], untouched[layer][mask])
+        assert not torch.equal(merged.keys[layer][~mask], untouched[layer][~mask])
+    assert merged.recomputed_rows == picked
+
+
+def test_extend_peek_decode(env):
+    cc, model, o_model, prefix, chunk_ids, chunks = env
+    merged = cc.merge_caches(chunks, model.config.rope)
+    n0 = merged.n_rows
+    peek, _ = cc.peek_forward(model, merged, [5, 7])
+    assert merged.n_rows == n0
+    logits, _ = cc.extend_cache(model, merged, [5, 7])
+    np.testing.assert_array_equal(peek, logits)
+    assert merged.n_rows == n0 + 2 and merged.token_ids[-2:] == [5, 7]
+    assert merged.source[-2:] == [(-1, n0), (-1, n0 + 1)]
+    np.testing.assert_array_equal(merged.positions, np.arange(n0 + 2))
+    # decode: contiguous positions only (model.py:649-666)
+    tok = int(np.argmax(logits))
+    l2, same = cc.decode_step(model, merged, tok, position=n0 + 2)
+    assert same is merged and merged.n_rows == n0 + 3
+    with pytest.raises(ValueError):
+        cc.decode_step(model, merged, tok, position=n0 + 9)
+    # against the oracle's direct-reuse + decode on the same bf16 weights
+    o_chunks = [orc.prefill_chunk(o_model, prefix, c) for c in chunk_ids]
+    o_merged = orc.merge(o_chunks, model.config.d_head, model.config.rope_base)
+    o_logits = orc.extend(o_model, o_merged, [5, 7])
+    o_l2 = orc.extend(o_model, o_merged, [tok])
+    std = o_logits.std()
+    assert np.abs(logits - o_logits).max() < 5e-2 * std
+    assert np.abs(l2 - o_l2).max() < 5e-2 * std
+
+
+def test_single_chunk_extend_equals_full_prefill(env):
+    """Merging one chunk then extending equals a full prefill of the same ids
+    (test_model.py:161-174, within the bf16 tolerance)."""
+    cc, model, _, prefix, chunk_ids, _ = env
+    one = cc.prefill_chunk(model, prefix, chunk_ids[0])
+    merged = cc.merge_caches([one], model.config.rope)
+    tail = [3, 1, 4, 1, 5]
+    logits, _ = cc.extend_cache(model, merged, tail)
+    full = cc.prefill_full(model, prefix + chunk_ids[0] + tail)
+    assert np.abs(logits - full.logits).max() < 5e-2 * full.logits.std()
+
+
+def test_merge_layout_fields(env):
+    cc, model, _, prefix, chunk_ids, chunks = env
+    merged = cc.merge_caches(chunks, model.config.rope)
+    assert merged.layout.sink_len == len(prefix)
+    assert merged.layout.chunk_lens == tuple(len(c) for c in chunk_ids)
+    assert merged.token_ids == prefix + [t for c in chunk_ids for t in c]
+    assert merged.source[:len(prefix)] == [(0, r) for r in range(len(prefix))]
+    assert merged.source[len(prefix)] == (0, len(prefix))
+    assert merged.source[-1] == (2, len(prefix) + len(chunk_ids[2]) - 1)
+    bad = cc.ChunkCache(chunks[1].k, chunks[1].v, chunks[1].token_ids, chunks[1].prefix_len, "other",
+                        chunks[1].model_fingerprint)
+    with pytest.raises(cc.CacheConsistencyError):
+        cc.merge_caches([chunks[0], bad], model.config.rope)
