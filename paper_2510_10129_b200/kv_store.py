@@ -348,9 +348,8 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
             ev = torch.cuda.Event()
             ev.record()
             layer_ready.append(ev)
-    if trace is not None:
-        for _ in range(L):
-            trace.rope("merge_overhead", total * H, D)
+    if trace is not None:  # one rotation per merged row per layer (kv_store.py:245-248), folded
+        trace.rope("merge_overhead", L * total * H, D)
     # source map is derived lazily from the layout (MergedCache.source)
     merged = MergedCache(token_ids=token_ids, layout=MergeLayout(sink, lens), source=None,
                          tokenizer_id=first.tokenizer_id, model_fingerprint=first.model_fingerprint,

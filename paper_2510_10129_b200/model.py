@@ -106,8 +106,7 @@ def prefill_full(model: Model, token_ids: Sequence[int], *, capture_maps: bool =
     ids = _ids_tensor(model, token_ids)
     K, V, logits, argmax = _dense(model, ids, True)
     n = ids.numel()
-    for _ in range(model.config.n_layers):
-        trace_layer(trace, model.config, stage, n, visible_pairs(n))
+    trace_layer(trace, model.config, stage, n, visible_pairs(n), times=model.config.n_layers)
     if trace is not None:
         trace.matmul(stage, 1, model.config.d_model, model.config.vocab_size)
     host = logits.cpu().numpy()
@@ -125,8 +124,7 @@ def prefill_chunk(model: Model, prefix_ids: Sequence[int], chunk_ids: Sequence[i
     ids = _ids_tensor(model, prefix_ids + chunk_ids)
     K, V, _, _ = _dense(model, ids, False)
     n = ids.numel()
-    for _ in range(model.config.n_layers):
-        trace_layer(trace, model.config, "chunk_precompute", n, visible_pairs(n))
+    trace_layer(trace, model.config, "chunk_precompute", n, visible_pairs(n), times=model.config.n_layers)
     if trace is not None:
         trace.matmul("chunk_precompute", 1, model.config.d_model, model.config.vocab_size)
     return ChunkCache(K, V, prefix_ids + chunk_ids, len(prefix_ids), model.config.tokenizer_id,
@@ -195,12 +193,10 @@ def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | No
                        pairs=pairs)
     cache.layer_ready = None  # every layer is now ordered before this stream's work
     if trace is not None:
-        for _ in range(c.n_layers):
-            if m:
-                trace_layer(trace, c, sel_stage, m, int(np.sum(sel_idx + 1)))
-        for _ in range(c.n_layers):
-            if nq:
-                trace_layer(trace, c, query_stage, nq, visible_pairs(nq, base))
+        if m:
+            trace_layer(trace, c, sel_stage, m, int(np.sum(sel_idx + 1)), times=c.n_layers)
+        if nq:
+            trace_layer(trace, c, query_stage, nq, visible_pairs(nq, base), times=c.n_layers)
         if nq and want_logits:
             trace.matmul(query_stage, 1, c.d_model, c.vocab_size)
     if append and nq:

@@ -270,13 +270,11 @@ def aux_score_tokens(aux_model: Model, aux_chunk_caches: Sequence[ChunkCache], q
     scores = torch.empty(int(chunk_lens.sum()), dtype=torch.float32, device=dev)
     spec = ScoreSpec(prefix, lens_d, off_d, int(chunk_lens.max()), scores)
     forward_banked(aux_model, ids_d, pos_d, tables, S, Q, int(n_rows.max()), score=spec)
-    if trace is not None:
-        for ch in aux_chunk_caches:
-            for _ in range(c.n_layers):
-                trace.rope("selection", ch.n_rows * c.kv_heads, c.d_head)
-            for _ in range(c.n_layers):
-                trace_layer(trace, c, "selection", Q, Q * ch.n_rows + Q * (Q + 1) // 2)
-            trace.matmul("selection", 1, c.d_model, c.vocab_size)
+    if trace is not None:  # the reference's per-chunk peek events, folded (linear counts)
+        rows_total = int(n_rows.sum())
+        trace.rope("selection", c.n_layers * rows_total * c.kv_heads, c.d_head)
+        trace_layer(trace, c, "selection", Q * S, Q * rows_total + S * (Q * (Q + 1) // 2), times=c.n_layers)
+        trace.matmul("selection", S, c.d_model, c.vocab_size)
     return ImportanceScores(scores, tuple(int(x) for x in chunk_lens))
 
 
