@@ -14,6 +14,10 @@ from .errors import CacheConsistencyError, DimensionError
 
 LIB_NAME = "libcacheclip_sm100.so"
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# tuning builds (same ABI, different compile-time knobs) can be swapped in by
+# naming another in-tree build of the library
+if os.environ.get("CACHECLIP_SM100_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["CACHECLIP_SM100_LIB"])
 
 CC_OK, CC_ERR_VALUE, CC_ERR_DIMENSION, CC_ERR_CONSISTENCY, CC_ERR_CUDA, CC_ERR_UNSUPPORTED = range(6)
 CC_F32, CC_BF16, CC_F32_SPLIT3 = 0, 1, 2

@@ -16,7 +16,8 @@
 //               PV_A(j) | S_A(j+1) | PV_B(j) | S_B(j+1) ...  S = Q K^T lands in
 //               TMEM; O += P V reads P straight from TMEM (A operand) and V
 //               from smem as an MN-major operand.
-//   warps 2..5  softmax of tile A, warps 6..9 of tile B: thread t owns row t,
+//   warps 2..3  idle after the prologue (warpgroup 0 gives up registers)
+//   warps 4..7  softmax of tile A, warps 8..11 of tile B: thread t owns row t,
 //               reads its S row with tcgen05.ld, does max / exp2 / sum in-thread,
 //               writes P (bf16 pairs) back over its S row with tcgen05.st.
 //               Lazy rescale: the running max moves (and O is rescaled in TMEM)
@@ -30,9 +31,24 @@
 
 namespace cc {
 
+#ifdef CC_FA_TRACE  // debug builds only: SM-clock timeline of the heaviest CTA
+__device__ long long g_fa_trace[16 * 128];
+#define FA_T(slot, j)                                                                        \
+  do {                                                                                       \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && (j) < 128)                         \
+      g_fa_trace[(slot) * 128 + (j)] = clock64();                                            \
+  } while (0)
+#else
+#define FA_T(slot, j) \
+  do {                \
+  } while (0)
+#endif
+
 constexpr int kFaTileRows = 128;
 constexpr int kFaKeys = 128;
-constexpr int kFaThreads = 320;
+constexpr int kFaThreads = 384;  // 3 warpgroups: producer/MMA, softmax A, softmax B
+constexpr int kFaCtlRegs = 56;    // setmaxnreg budgets: 128*56 + 256*224 <= 64K
+constexpr int kFaSoftmaxRegs = 224;
 constexpr float kFaRescaleThreshold = 8.0f;  // log2 domain
 
 template <int D>
@@ -138,6 +154,30 @@ __device__ __forceinline__ float ex2_poly(float x) {
   return __int_as_float(__float_as_int(p) + (n << 23));
 }
 
+// The same on a pair with the sm_100 paired-FP32 instructions (FADD2/FFMA2):
+// half the issue slots. t = x + 1.5*2^23 holds n in its low mantissa bits and
+// the magic's own bits vanish under << 23, so 2^n scaling is one IMAD.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.0f);
+  x.y = fmaxf(x.y, -126.0f);
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);
+  const float2 t = __fadd2_rn(x, magic);
+  const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = __ffma2_rn(n, make_float2(-1.0f, -1.0f), x);
+  float2 p = __ffma2_rn(f, make_float2(9.6181291e-3f, 9.6181291e-3f), make_float2(5.5504109e-2f, 5.5504109e-2f));
+  p = __ffma2_rn(p, f, make_float2(2.4022651e-1f, 2.4022651e-1f));
+  p = __ffma2_rn(p, f, make_float2(6.9314718e-1f, 6.9314718e-1f));
+  p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+// pairs (of 16 per 32-key chunk) whose exponentials run on the FMA pipe
+#ifndef CC_FA_POLY
+#define CC_FA_POLY 4
+#endif
+constexpr int kFaPolyPairs = CC_FA_POLY;
+
 template <int D>
 __global__ void __launch_bounds__(kFaThreads, 1)
     fa_sparse_row_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -183,13 +223,13 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   if (warp == 1) tmem_alloc(tmem_slot, 512);
 
   // ---- prologue: softmax warps gather their Q rows into swizzled smem ----
-  const int tq = warp >= 2 ? (warp - 2) >> 2 : 0;  // query tile of this softmax warp
+  const int tq = warp >= 4 ? (warp - 4) >> 2 : 0;  // query tile of this softmax warp
   const int quarter = warp & 3;                     // TMEM lane quarter
   const int r = quarter * 32 + lane;                // row within the tile
   int lim = 0;
   float scale2 = 0.f;
   int64_t out_off = -1, part_row = -1;
-  if (warp >= 2) {
+  if (warp >= 4) {
     const int64_t p = p0 + tq * kFaTileRows + r;
     const uint4 zero = make_uint4(0, 0, 0, 0);
     const uint4* src = nullptr;
@@ -221,77 +261,85 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const int n_tiles = (*s_kmax + kFaKeys - 1) / kFaKeys;
 
-  if (warp == 0) {
-    // ---------------- TMA producer ----------------
-    if (lane == 0 && n_tiles > 0) {
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      for (int j = 0; j < n_tiles; ++j) {
-        const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&kv_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], Cfg::KT_BYTES);
-#pragma unroll
-        for (int kb = 0; kb < Cfg::KB; ++kb)
-          tma_load_3d(sK + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmK, &k_full[s], kb * 64, kvh, j * kFaKeys);
-        mbar_arrive_expect_tx(&v_full[s], Cfg::KT_BYTES);
-#pragma unroll
-        for (int kb = 0; kb < Cfg::KB; ++kb)
-          tma_load_3d(sV + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmV, &v_full[s], kb * 64, kvh, j * kFaKeys);
-      }
-    }
-  } else if (warp == 1) {
-    // ---------------- MMA issuer (ping-pong over the two query tiles) ----------------
-    auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
-      if (lane == 0) {
-        const uint32_t q0 = smem_u32(sQ + t * Cfg::QT_BYTES), k0 = smem_u32(sK + (j & 1) * Cfg::KT_BYTES);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t qo = (k >> 2) * (kFaTileRows * 128) + (k & 3) * 32;
-          const uint32_t ko = (k >> 2) * (kFaKeys * 128) + (k & 3) * 32;
-          tc_mma<false>(tmem + Cfg::s_col(t), umma_desc_sw128(q0 + qo), umma_desc_sw128(k0 + ko), Cfg::IDESC_S,
-                        k > 0 ? 1u : 0u);
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kFaCtlRegs));
+    if (warp == 0) {
+      // ---------------- TMA producer ----------------
+      if (lane == 0 && n_tiles > 0) {
+        tma_prefetch_desc(&tmK);
+        tma_prefetch_desc(&tmV);
+        for (int j = 0; j < n_tiles; ++j) {
+          const int s = j & 1;
+          const uint32_t ph = (j >> 1) & 1;
+          mbar_wait(&kv_empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&k_full[s], Cfg::KT_BYTES);
+  #pragma unroll
+          for (int kb = 0; kb < Cfg::KB; ++kb)
+            tma_load_3d(sK + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmK, &k_full[s], kb * 64, kvh, j * kFaKeys);
+          mbar_arrive_expect_tx(&v_full[s], Cfg::KT_BYTES);
+  #pragma unroll
+          for (int kb = 0; kb < Cfg::KB; ++kb)
+            tma_load_3d(sV + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmV, &v_full[s], kb * 64, kvh, j * kFaKeys);
         }
-        tc_commit(&s_full[t]);
       }
-      __syncwarp();
-    };
-    auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P read from TMEM (over S_t)
-      mbar_wait(&p_full[t], j & 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t v0 = smem_u32(sV + (j & 1) * Cfg::KT_BYTES);
-#pragma unroll
-        for (int k = 0; k < kFaKeys / 16; ++k)
-          tc_mma_ts(tmem + Cfg::o_col(t), tmem + Cfg::s_col(t) + k * 8,
-                    umma_desc_mn_sw128(v0 + k * 16 * 128, kFaKeys * 128, 1024), Cfg::IDESC_PV,
-                    (j > 0 || k > 0) ? 1u : 0u);
-      }
-      __syncwarp();
-    };
-    if (n_tiles > 0) {
-      mbar_wait(&k_full[0], 0);
-      tc_fence_after();
-      issue_s(0, 0);
-      issue_s(1, 0);
-      for (int j = 0; j < n_tiles; ++j) {
-        const bool more = j + 1 < n_tiles;
-        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-        issue_pv(0, j);
-        if (more) {
-          mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-          tc_fence_after();
-          issue_s(0, j + 1);
+    } else if (warp == 1) {
+      // ---------------- MMA issuer (ping-pong over the two query tiles) ----------------
+      auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+        if (lane == 0) {
+          const uint32_t q0 = smem_u32(sQ + t * Cfg::QT_BYTES), k0 = smem_u32(sK + (j & 1) * Cfg::KT_BYTES);
+  #pragma unroll
+          for (int k = 0; k < D / 16; ++k) {
+            const uint32_t qo = (k >> 2) * (kFaTileRows * 128) + (k & 3) * 32;
+            const uint32_t ko = (k >> 2) * (kFaKeys * 128) + (k & 3) * 32;
+            tc_mma<false>(tmem + Cfg::s_col(t), umma_desc_sw128(q0 + qo), umma_desc_sw128(k0 + ko), Cfg::IDESC_S,
+                          k > 0 ? 1u : 0u);
+          }
+          tc_commit(&s_full[t]);
         }
-        issue_pv(1, j);
-        if (lane == 0) tc_commit(&kv_empty[j & 1]);
         __syncwarp();
-        if (more) issue_s(1, j + 1);
+      };
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P read from TMEM (over S_t)
+        mbar_wait(&p_full[t], j & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t v0 = smem_u32(sV + (j & 1) * Cfg::KT_BYTES);
+  #pragma unroll
+          for (int k = 0; k < kFaKeys / 16; ++k)
+            tc_mma_ts(tmem + Cfg::o_col(t), tmem + Cfg::s_col(t) + k * 8,
+                      umma_desc_mn_sw128(v0 + k * 16 * 128, kFaKeys * 128, 1024), Cfg::IDESC_PV,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        }
+        __syncwarp();
+      };
+      if (n_tiles > 0) {
+        mbar_wait(&k_full[0], 0);
+        tc_fence_after();
+        issue_s(0, 0);
+        issue_s(1, 0);
+        for (int j = 0; j < n_tiles; ++j) {
+          const bool more = j + 1 < n_tiles;
+          mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+          issue_pv(0, j);
+          FA_T(4, j);
+          if (more) {
+            mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+            tc_fence_after();
+            issue_s(0, j + 1);
+            FA_T(5, j);
+          }
+          issue_pv(1, j);
+          FA_T(6, j);
+          if (lane == 0) tc_commit(&kv_empty[j & 1]);
+          __syncwarp();
+          if (more) issue_s(1, j + 1);
+          FA_T(7, j);
+        }
+        if (lane == 0) tc_commit(pv_done);
+        __syncwarp();
       }
-      if (lane == 0) tc_commit(pv_done);
-      __syncwarp();
     }
   } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kFaSoftmaxRegs));
     // ---------------- softmax + epilogue (row per thread) ----------------
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + Cfg::s_col(tq);
@@ -302,6 +350,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&s_full[tq], j & 1);
+      if (quarter == 0) FA_T(tq * 2, j);
       tc_fence_after();
       float sv[kFaKeys];
 #pragma unroll
@@ -311,9 +360,14 @@ __global__ void __launch_bounds__(kFaThreads, 1)
 #pragma unroll
         for (int c = 0; c < kFaKeys; ++c) sv[c] = (key0 + c < lim) ? sv[c] : -INFINITY;
       }
-      float mt = -INFINITY;
+      // row max as four independent 3-input chains (FMNMX3), short dependency depth
+      float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < kFaKeys; ++c) mt = fmaxf(mt, sv[c]);
+      for (int c = 0; c < kFaKeys; c += 8) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) m4[u] = fmaxf(m4[u], fmaxf(sv[c + 2 * u], sv[c + 2 * u + 1]));
+      }
+      const float mt = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       const float m_tile = mt * scale2;  // scale2 > 0: max commutes with the scale
       float alpha = 1.f;
       bool resc = false;
@@ -323,27 +377,28 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         resc = true;
       }
       const float nbase = (m_run == -INFINITY) ? 0.f : -m_run;
-      float lsum = 0.f;
+      const float2 sc2 = make_float2(scale2, scale2), nb2 = make_float2(nbase, nbase);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int c = 0; c < kFaKeys / 32; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const float xa = fmaf(sv[c * 32 + 2 * e], scale2, nbase);
-          const float xb = fmaf(sv[c * 32 + 2 * e + 1], scale2, nbase);
-          float a, b;
-          if ((e & 3) == 3) {  // a quarter of the exponentials on the FMA pipe
-            a = ex2_poly(xa);
-            b = ex2_poly(xb);
+          const float2 x = __ffma2_rn(make_float2(sv[c * 32 + 2 * e], sv[c * 32 + 2 * e + 1]), sc2, nb2);
+          float2 p;
+          if ((e & 15) * kFaPolyPairs % 16 >= 16 - kFaPolyPairs) {  // kFaPolyPairs of 16 pairs on the FMA pipe
+            p = ex2_poly2(x);
           } else {
-            a = ex2_mufu(xa);
-            b = ex2_mufu(xb);
+            p.x = ex2_mufu(x.x);
+            p.y = ex2_mufu(x.y);
           }
-          lsum += a + b;
-          pk[e] = pack2_bf16(a, b);
+          acc[e & 3] = __fadd2_rn(acc[e & 3], p);
+          pk[e] = pack2_bf16(p.x, p.y);
         }
         tmem_st16u(s_addr + c * 16, pk);  // P over the S row: column c*16+e holds keys (2e, 2e+1) of chunk c
       }
+      const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
+      const float lsum = (s01.x + s01.y) + (s23.x + s23.y);
       l_run = l_run * alpha + lsum;
       if (j > 0 && __any_sync(0xffffffffu, resc)) {
         // O is stable here: PV_t(j-1) completed before S_t(j) (in-order tcgen05 pipe)
@@ -361,6 +416,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[tq]);
+      if (quarter == 0) FA_T(tq * 2 + 1, j);
     }
     if (n_tiles > 0) {
       mbar_wait(pv_done, 0);
@@ -512,6 +568,12 @@ __global__ void local_limits_kernel(const int64_t* __restrict__ row_pos, int64_t
 }  // namespace cc
 
 using namespace cc;
+
+#ifdef CC_FA_TRACE
+extern "C" int cc_debug_fa_trace(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_fa_trace, sizeof(long long) * 16 * 128) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 // algorithmic work of the next attention launch (set by the executor, which
 // knows sum(pos+1) on the host; 0 when unknown)
