@@ -206,6 +206,15 @@ int cc_banked_attention_f32(const cc_bank_seq* seqs_dev, int32_t n_seqs, int32_t
                             const float* v_new, int32_t n_q_heads, int32_t n_kv_heads,
                             int32_t head_dim, float factor, void* out, int32_t out_mode,
                             float* weights_out, int64_t w_col0, int64_t w_ld, void* stream);
+/* The same contract on the FP32 SIMT pipe (4x4 FFMA micro-tiles, logits in
+ * shared memory; bank + new rows must fit ~800 columns). cc_banked_attention_f32
+ * itself runs on tcgen05 (3xTF32, banked_tc.cu); this one is kept as an
+ * independent cross-check of it. */
+int cc_banked_attention_simt(const cc_bank_seq* seqs_dev, int32_t n_seqs, int32_t max_new,
+                             int64_t max_bank, const float* q, const float* k_new,
+                             const float* v_new, int32_t n_q_heads, int32_t n_kv_heads,
+                             int32_t head_dim, float factor, void* out, int32_t out_mode,
+                             float* weights_out, int64_t w_col0, int64_t w_ld, void* stream);
 
 /* ------------------------------------------------------------------------
  * (5) Importance reduction + grouped top-k — aux_score_tokens' head/query

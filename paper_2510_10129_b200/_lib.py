@@ -99,6 +99,7 @@ _SIGS = {
     "cc_lse_merge": ([vp, vp, i32, i64, i64, i32, i32, vp, i64, i32, vp], i32),
     "cc_sparse_row_attention_mma": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),
     "cc_banked_attention_f32": ([vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, f32, vp, i32, vp, i64, i64, vp], i32),
+    "cc_banked_attention_simt": ([vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, f32, vp, i32, vp, i64, i64, vp], i32),
     "cc_reduce_scores": ([vp, i32, i32, i32, i64, vp, vp, i64, vp, vp], i32),
     "cc_select_workspace_bytes": ([i64, i32], i64),
     "cc_select_topk_windows": ([vp, i64, vp, i32, i64, i64, i32, i32, i32, i64, vp, vp, vp, vp, vp, vp], i32),

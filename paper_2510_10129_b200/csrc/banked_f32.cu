@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kBkThreads) banked_f32_kernel(
 
 using namespace cc;
 
-extern "C" int cc_banked_attention_f32(const cc_bank_seq* seqs_dev, int32_t n_seqs, int32_t max_new,
+extern "C" int cc_banked_attention_simt(const cc_bank_seq* seqs_dev, int32_t n_seqs, int32_t max_new,
                                        int64_t max_bank, const float* q, const float* k_new, const float* v_new,
                                        int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim, float factor,
                                        void* out, int32_t out_mode, float* weights_out, int64_t w_col0,
@@ -243,7 +243,7 @@ extern "C" int cc_banked_attention_f32(const cc_bank_seq* seqs_dev, int32_t n_se
                (long long)(max_bank + max_new));
   dim3 grid((max_new + qpb - 1) / qpb, n_kv_heads, n_seqs);
   cudaStream_t st = as_stream(stream);
-  ProfScope ps(st, OP_BANKED, 0);
+  ProfScope ps(st, OP_OTHER, 0);
   if (head_dim == 64) {
     cudaFuncSetAttribute(banked_f32_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     banked_f32_kernel<64><<<grid, kBkThreads, smem, st>>>(seqs_dev, q, k_new, v_new, n_q_heads, n_kv_heads, factor,

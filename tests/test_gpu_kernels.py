@@ -223,13 +223,22 @@ def test_sparse_row_attention_row_factor():
     assert (out.double().view(m, Hq, D) - ref).abs().max().item() < 2e-2
 
 
-def test_banked_attention_f32_matches_reference_math():
+@pytest.mark.parametrize("fn", ["cc_banked_attention_f32", "cc_banked_attention_simt"])
+@pytest.mark.parametrize("Hq,Hkv,D,Q,nbs", [
+    (4, 2, 64, 8, (40, 3, 100)),
+    (14, 2, 64, 32, (544, 0, 37, 300)),   # the 0.5B scoring model's heads, a C3 chunk bank
+    (8, 8, 128, 20, (130, 1)),
+    (14, 2, 64, 150, (0, 260)),           # chunk precompute shape: no bank, many new rows
+])
+def test_banked_attention_f32_matches_reference_math(fn, Hq, Hkv, D, Q, nbs):
+    """cc_banked_attention_f32 (tcgen05 3xTF32) and the SIMT cross-check
+    against the oracle's attend (tensor_core.py:109-170 order) in float64-free
+    numpy fp32: context and last-layer weights at fp32-level tolerance."""
     from paper_2510_10129_b200 import _lib as L
     from paper_2510_10129_b200.runtime import bank_tables
-    rng = np.random.default_rng(2)
-    Hq, Hkv, D, Q = 4, 2, 64, 8
-    banks = [rng.standard_normal((1, nb, Hkv, D)).astype(np.float32) for nb in (40, 3, 100)]
-    vbanks = [rng.standard_normal((1, nb, Hkv, D)).astype(np.float32) for nb in (40, 3, 100)]
+    rng = np.random.default_rng(2 + Q)
+    banks = [rng.standard_normal((1, nb, Hkv, D)).astype(np.float32) for nb in nbs]
+    vbanks = [rng.standard_normal((1, nb, Hkv, D)).astype(np.float32) for nb in nbs]
     S = len(banks)
     q = rng.standard_normal((S * Q, Hq * D)).astype(np.float32)
     kn = rng.standard_normal((S * Q, Hkv * D)).astype(np.float32)
@@ -241,16 +250,23 @@ def test_banked_attention_f32_matches_reference_math():
     out = torch.empty(S * Q, Hq * D, device=DEV)
     factor = float(np.float32(1 / math.sqrt(D)))
     maxb = max(b.shape[1] for b in banks)
-    L.call("cc_banked_attention_f32", tables.data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
-           vd.data_ptr(), Hq, Hkv, D, factor, out.data_ptr(), L.CC_F32, None, 0, 0,
-           torch.cuda.current_stream().cuda_stream)
-    w = torch.zeros(S, Hq, Q, maxb, device=DEV)
-    L.call("cc_banked_attention_f32", tables.data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
-           vd.data_ptr(), Hq, Hkv, D, factor, out.data_ptr(), L.CC_F32, w.data_ptr(), 0, maxb,
-           torch.cuda.current_stream().cuda_stream)
+    st = torch.cuda.current_stream().cuda_stream
+    L.call(fn, tables.data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
+           vd.data_ptr(), Hq, Hkv, D, factor, out.data_ptr(), L.CC_F32, None, 0, 0, st)
+    w = torch.zeros(S, Hq, Q, max(maxb, 1), device=DEV)
+    L.call(fn, tables.data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
+           vd.data_ptr(), Hq, Hkv, D, factor, out.data_ptr(), L.CC_F32, w.data_ptr(), 0, max(maxb, 1), st)
+    split = torch.empty(S * Q, 3 * Hq * D, device=DEV)
+    L.call(fn, tables.data_ptr(), S, Q, maxb, qd.data_ptr(), kd.data_ptr(),
+           vd.data_ptr(), Hq, Hkv, D, factor, split.data_ptr(), L.CC_F32_SPLIT3, None, 0, 0, st)
     torch.cuda.synchronize()
     got = out.cpu().numpy()
     wg = w.cpu().numpy()
+    sp = split.cpu().numpy()
+    w_ = Hq * D
+    # split layout [hi | hi | lo]: hi + lo reproduces the context to ~2^-22
+    np.testing.assert_allclose(sp[:, :w_] + sp[:, 2 * w_:], got, rtol=1e-6, atol=1e-7)
+    assert np.array_equal(sp[:, :w_], sp[:, w_:2 * w_])
     for s in range(S):
         nb = banks[s].shape[1]
         bank_k = np.concatenate([banks[s][0], kn[s * Q:(s + 1) * Q].reshape(Q, Hkv, D)])
