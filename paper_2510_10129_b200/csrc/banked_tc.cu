@@ -11,16 +11,19 @@
 //
 // hi = x rounded to tf32, lo = tf32(x - hi): the dropped lo*lo term and the
 // tf32 rounding of lo leave ~2^-22 relative error per product (fp32 level).
-// The softmax keeps the reference's order exactly (tensor_core.py:88-96,
-// 165-170): logits = S * factor (one fp32 multiply), masked, row max, e =
-// exp(logit - max), row sum, p = e / sum, then p @ V. Since a row's 576
-// logits do not fit TMEM, the key tiles are swept three times — max, sum,
-// then p (stored as the last-layer weights, selector.py:157-165, or fed to
-// the PV product); recomputing Q K^T is cheap next to the softmax.
+// A row's 576 logits do not fit TMEM, so the key tiles are swept more than
+// once (recomputing Q K^T is cheap next to the softmax):
+//   - last (scoring) layer: the reference's order exactly (tensor_core.py:
+//     88-96, 165-170) — max of S * factor, then the sum of exp(x - max), then
+//     p = exp(x - max) / sum written as the weights (selector.py:157-165);
+//   - other layers: an online max / sum in the log2 domain (MUFU ex2), then
+//     P = 2^(y - max) / sum fed to O += P V.
 //
 // CTA = one sequence x one KV head x (128 / G) query rows; packed row r =
 // query i0 + r / G, head kvh*G + r % G, so the K/V tiles are read once for
-// all G heads. Thread r owns TMEM lane r (its packed row). K/V tiles are
+// all G heads. 8 warps: warp w owns TMEM lane quarter w % 4 (its packed rows)
+// and column half w / 4 of every 32-key tile; the two halves combine their
+// row statistics once per sweep through shared memory. K/V tiles are
 // register-prefetched from global one tile ahead, split hi/lo and written
 // into 128B-swizzled smem (V transposed: an MN-major tf32 B operand read back
 // as zeros on this part, K-major V^T is exact); one thread issues the MMAs.
@@ -30,13 +33,13 @@ namespace cc {
 
 constexpr int kBtRows = 128;   // packed rows per CTA = TMEM lanes
 constexpr int kBtKeys = 32;    // keys per tile
-constexpr int kBtThreads = 128;
+constexpr int kBtThreads = 256;  // 4 lane quarters x 2 column halves
 
 template <int HD>
 struct BtCfg {
   static constexpr int Q_BYTES = kBtRows * HD * 4;  // one of Q_hi / Q_lo
   static constexpr int K_BYTES = kBtKeys * HD * 4;  // one of K_hi / K_lo / V_hi / V_lo
-  static constexpr int SMEM = 2 * Q_BYTES + 4 * K_BYTES + 1024 + 64;
+  static constexpr int SMEM = 2 * Q_BYTES + 4 * K_BYTES + 4 * kBtRows * 4 + 1024 + 64;
   static constexpr int T_S = 0, T_PH = kBtKeys, T_PL = 2 * kBtKeys, T_O = 3 * kBtKeys;
   static constexpr int TMEM_COLS = (3 * kBtKeys + HD) <= 256 ? 256 : 512;
   static constexpr int F4 = kBtKeys * HD / 4 / kBtThreads;  // float4 per thread per K (or V) tile
@@ -96,12 +99,52 @@ __device__ __forceinline__ void tmem_st32_f(uint32_t taddr, const float* v) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st16_f(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// tf32 split without the non-finite guard (inputs are finite probabilities / values)
+__device__ __forceinline__ void split_tf32_finite(float x, float& hi, float& lo) {
+  const uint32_t u = __float_as_uint(x);
+  hi = __uint_as_float((u + 0xFFFu + ((u >> 13) & 1u)) & 0xFFFFE000u);
+  lo = __fsub_rn(x, hi);
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
     const cc_bank_seq* __restrict__ seqs, const float* __restrict__ q, const float* __restrict__ k_new,
     const float* __restrict__ v_new, int n_q_heads, int n_kv_heads, float factor, int qpb, void* __restrict__ out,
     int out_mode, float* __restrict__ weights_out, int64_t w_col0, int64_t w_ld) {
   using Cfg = BtCfg<HD>;
+  constexpr int HC = kBtKeys / 2;  // columns of a key tile per thread (two column halves)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sQh = smem;
@@ -110,7 +153,8 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
   uint8_t* sKl = sKh + Cfg::K_BYTES;
   uint8_t* sVh = sKl + Cfg::K_BYTES;
   uint8_t* sVl = sVh + Cfg::K_BYTES;
-  uint64_t* s_bar = reinterpret_cast<uint64_t*>(sVl + Cfg::K_BYTES);
+  float* red = reinterpret_cast<float*>(sVl + Cfg::K_BYTES);  // [2 halves][2][128 rows]
+  uint64_t* s_bar = reinterpret_cast<uint64_t*>(red + 4 * kBtRows);
   uint64_t* pv_bar = s_bar + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_bar + 2);
 
@@ -125,8 +169,10 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
   const int ncols = (int)(nb + i0 + nq);
   const int n_tiles = (ncols + kBtKeys - 1) / kBtKeys;
   const int64_t qw = (int64_t)n_q_heads * HD, kvw = (int64_t)n_kv_heads * HD;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const bool want_pv = weights_out == nullptr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int half = warp >> 2;                 // column half of every key tile
+  const int r = (warp & 3) * 32 + lane;       // packed row = TMEM lane
+  const bool scoring = weights_out != nullptr;
 
   if (tid == 0) {
     mbar_init(s_bar, 1);
@@ -135,8 +181,7 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
   }
   if (warp == 0) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
 
-  // ---- this thread's packed row: Q -> split hi/lo, swizzled K-major ----
-  const int r = tid;
+  // ---- packed row r: Q -> split hi/lo, swizzled K-major (each half stages half the dims) ----
   const bool live = r < nrows;
   const int qi = i0 + (live ? r / G : 0);
   const int head = kvh * G + (live ? r % G : 0);
@@ -144,7 +189,8 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
   {
     const float4* src = reinterpret_cast<const float4*>(q + (sq.row0 + qi) * qw + (int64_t)head * HD);
 #pragma unroll
-    for (int c4 = 0; c4 < HD / 4; ++c4) {
+    for (int c = 0; c < HD / 8; ++c) {
+      const int c4 = half * (HD / 8) + c;
       const float4 v = live ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
       float4 hi, lo;
       split4(v, hi, lo);
@@ -201,26 +247,22 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's TMEM lane quarter
+  const uint32_t t_s = tl + Cfg::T_S + half * HC;
 
   uint32_t s_phase = 0, pv_phase = 0;
-  float mx = -INFINITY, sum = 0.f;
-  float* wrow = nullptr;
-  if (!want_pv && live)
-    wrow = weights_out + (((int64_t)blockIdx.z * n_q_heads + head) * sq.n_new + qi) * w_ld - w_col0;
-
-  for (int pass = 0; pass < 3; ++pass) {
-    const bool pv = pass == 2 && want_pv;
-    fetch(0, pv);
+  // one sweep over the key tiles: S = Q K^T for tile j, then body(c0 + half*HC, s[HC])
+  auto sweep = [&](bool with_v, auto&& body) {
+    fetch(0, with_v);
     for (int j = 0; j < n_tiles; ++j) {
-      if (pv && j > 0) {  // PV(j-1) still reads V smem and P in TMEM
+      if (with_v && j > 0) {  // PV(j-1) still reads V smem and P in TMEM
         mbar_wait(pv_bar, pv_phase);
         pv_phase ^= 1;
       }
-      stage(pv);
+      stage(with_v);
       fence_proxy_async_bt();
       tc_fence_before();
-      __syncthreads();
+      __syncthreads();  // also: every thread has read S(j-1) before S(j) overwrites it
       tc_fence_after();
       if (tid == 0) {
         const uint32_t q0h = smem_u32(sQh), q0l = smem_u32(sQl), k0h = smem_u32(sKh), k0l = smem_u32(sKl);
@@ -235,77 +277,125 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
         }
         tc_commit(s_bar);
       }
-      if (j + 1 < n_tiles) fetch(j + 1, pv);  // in flight during the MMA and the softmax
+      if (j + 1 < n_tiles) fetch(j + 1, with_v);  // in flight during the MMA and the softmax
       mbar_wait(s_bar, s_phase);
       s_phase ^= 1;
       tc_fence_after();
-      float s[kBtKeys];
-      tmem_ld32(trow + Cfg::T_S, s);
-      const int c0 = j * kBtKeys;
-      if (pass == 0) {
+      float s[HC];
+      tmem_ld16(t_s, s);
+      body(j, j * kBtKeys + half * HC, s);
+    }
+  };
+  // combine a per-half row statistic (half 0 first: deterministic order)
+  auto exchange = [&](float a, float b, float& a1, float& b1) {
+    red[(half * 2 + 0) * kBtRows + r] = a;
+    red[(half * 2 + 1) * kBtRows + r] = b;
+    __syncthreads();
+    a1 = red[((half ^ 1) * 2 + 0) * kBtRows + r];
+    b1 = red[((half ^ 1) * 2 + 1) * kBtRows + r];
+    __syncthreads();
+  };
+
+  if (scoring) {
+    // Exact reference order for the weights that become importance scores:
+    // max of (S * factor), then sum of exp(x - max), then exp(x - max) / sum.
+    float mx = -INFINITY;
+    sweep(false, [&](int, int c0, float* s) {
 #pragma unroll
-        for (int t = 0; t < kBtKeys; ++t)
-          if (c0 + t < limit) mx = fmaxf(mx, __fmul_rn(s[t], factor));
-      } else if (pass == 1) {
+      for (int t = 0; t < HC; ++t)
+        if (c0 + t < limit) mx = fmaxf(mx, __fmul_rn(s[t], factor));
+    });
+    float o0, o1, unused;
+    exchange(mx, 0.f, o0, unused);
+    mx = fmaxf(mx, o0);
+    float sum = 0.f;
+    sweep(false, [&](int, int c0, float* s) {
 #pragma unroll
-        for (int t = 0; t < kBtKeys; ++t)
-          if (c0 + t < limit) sum = __fadd_rn(sum, expf(__fsub_rn(__fmul_rn(s[t], factor), mx)));
+      for (int t = 0; t < HC; ++t)
+        if (c0 + t < limit) sum = __fadd_rn(sum, expf(__fsub_rn(__fmul_rn(s[t], factor), mx)));
+    });
+    exchange(sum, 0.f, o1, unused);
+    sum = half == 0 ? __fadd_rn(sum, o1) : __fadd_rn(o1, sum);
+    float* wrow = live ? weights_out + (((int64_t)blockIdx.z * n_q_heads + head) * sq.n_new + qi) * w_ld - w_col0
+                       : nullptr;
+    sweep(false, [&](int, int c0, float* s) {
+      if (!wrow || c0 >= nb || c0 + HC <= w_col0) return;
+      float p[HC];
+#pragma unroll
+      for (int t = 0; t < HC; ++t)
+        p[t] = c0 + t < limit ? __fdiv_rn(expf(__fsub_rn(__fmul_rn(s[t], factor), mx)), sum) : 0.f;
+      float* dst = wrow + c0;
+      if (c0 >= w_col0 && c0 + HC <= nb && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+        for (int t = 0; t < HC / 4; ++t)
+          reinterpret_cast<float4*>(dst)[t] = make_float4(p[4 * t], p[4 * t + 1], p[4 * t + 2], p[4 * t + 3]);
       } else {
 #pragma unroll
-        for (int t = 0; t < kBtKeys; ++t)
-          s[t] = c0 + t < limit ? __fdiv_rn(expf(__fsub_rn(__fmul_rn(s[t], factor), mx)), sum) : 0.f;
-        if (!pv) {
-          if (wrow) {  // last-layer weights over bank columns [w_col0, nb)
+        for (int t = 0; t < HC; ++t)
+          if (c0 + t >= w_col0 && c0 + t < nb) dst[t] = p[t];
+      }
+    });
+  } else {
+    // Context rows: online max / sum in the log2 domain (MUFU ex2), then
+    // P = 2^(y - max) / sum fed to O += P V on the tensor core.
+    const float fl = factor * 1.4426950408889634f;
+    float m = -INFINITY, l = 0.f;
+    sweep(false, [&](int, int c0, float* s) {
+      float tm = m;
 #pragma unroll
-            for (int t = 0; t < kBtKeys; ++t)
-              if (c0 + t >= w_col0 && c0 + t < nb) wrow[c0 + t] = s[t];
-          }
-        } else {
-          float ph[kBtKeys];
+      for (int t = 0; t < HC; ++t) {
+        s[t] = c0 + t < limit ? s[t] * fl : -INFINITY;
+        tm = fmaxf(tm, s[t]);
+      }
+      if (tm == -INFINITY) return;
+      l *= ex2_approx(m - tm);
+      m = tm;
 #pragma unroll
-          for (int t = 0; t < kBtKeys; ++t) {
-            float lo;
-            split_tf32(s[t], ph[t], lo);
-            float l2;
-            split_tf32(lo, s[t], l2);
-          }
-          tmem_st32_f(trow + Cfg::T_PH, ph);
-          tmem_st32_f(trow + Cfg::T_PL, s);
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          tc_fence_before();
-          __syncthreads();
-          tc_fence_after();
-          if (tid == 0) {
-            const uint32_t v0h = smem_u32(sVh), v0l = smem_u32(sVl);
+      for (int t = 0; t < HC; ++t) l += ex2_approx(s[t] - m);
+    });
+    float m1, l1;
+    exchange(m, l, m1, l1);
+    const float M = fmaxf(m, m1);
+    const float L = (m == -INFINITY ? 0.f : l * ex2_approx(m - M)) + (m1 == -INFINITY ? 0.f : l1 * ex2_approx(m1 - M));
+    const float inv = L > 0.f ? 1.0f / L : 0.f;
+    sweep(true, [&](int j, int c0, float* s) {
+      float ph[HC];
 #pragma unroll
-            for (int k = 0; k < kBtKeys / 8; ++k) {
-              const uint64_t bh = umma_desc_sw128(v0h + k * 32), bl = umma_desc_sw128(v0l + k * 32);
-              tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PH + k * 8, bh, Cfg::IDESC_PV, (j > 0 || k > 0) ? 1u : 0u);
-              tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PH + k * 8, bl, Cfg::IDESC_PV, 1u);
-              tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PL + k * 8, bh, Cfg::IDESC_PV, 1u);
-            }
-            tc_commit(pv_bar);
-          }
+      for (int t = 0; t < HC; ++t) {
+        const float pv = c0 + t < limit ? ex2_approx(s[t] * fl - M) * inv : 0.f;
+        float lo;
+        split_tf32_finite(pv, ph[t], lo);
+        float l2;
+        split_tf32_finite(lo, s[t], l2);
+      }
+      tmem_st16_f(tl + Cfg::T_PH + half * HC, ph);
+      tmem_st16_f(tl + Cfg::T_PL + half * HC, s);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncthreads();
+      tc_fence_after();
+      if (tid == 0) {
+        const uint32_t v0h = smem_u32(sVh), v0l = smem_u32(sVl);
+#pragma unroll
+        for (int k = 0; k < kBtKeys / 8; ++k) {
+          const uint64_t bh = umma_desc_sw128(v0h + k * 32), bl = umma_desc_sw128(v0l + k * 32);
+          tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PH + k * 8, bh, Cfg::IDESC_PV, (j > 0 || k > 0) ? 1u : 0u);
+          tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PH + k * 8, bl, Cfg::IDESC_PV, 1u);
+          tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PL + k * 8, bh, Cfg::IDESC_PV, 1u);
         }
+        tc_commit(pv_bar);
       }
-      if (!pv) {  // the next tile's S MMA overwrites S and K smem: everyone has read S
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-      }
-    }
-  }
-
-  if (want_pv) {
+    });
     mbar_wait(pv_bar, pv_phase);
     tc_fence_after();
 #pragma unroll
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = 0; c < HD / 64; ++c) {
       float o[32];
-      tmem_ld32(trow + Cfg::T_O + c * 32, o);
+      const int d0 = half * (HD / 2) + c * 32;
+      tmem_ld32(tl + Cfg::T_O + d0, o);
       if (!live) continue;
       const int64_t row = sq.row0 + qi;
-      const int64_t col0 = (int64_t)head * HD + c * 32;
+      const int64_t col0 = (int64_t)head * HD + d0;
       if (out_mode == CC_F32) {
         float4* p = reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + row * qw + col0);
 #pragma unroll
