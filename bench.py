@@ -56,6 +56,8 @@ def parse_args():
     ap.add_argument("--sweep", action="store_true", help="also time ratios 5/10/20/40%%")
     ap.add_argument("--sharded", action="store_true",
                     help="one request sequence-sharded over the ranks (C4 path) instead of request-parallel")
+    ap.add_argument("--requests", type=int, default=0, help="c5: requests per step (default: the workload's 64)")
+    ap.add_argument("--pool", type=int, default=0, help="c5: shared chunk-pool size (default 4 x chunks/request)")
     return ap.parse_args()
 
 
@@ -114,6 +116,18 @@ def peaks() -> dict:
         return {"hbm": d["hbm_gbs"], "bf16": d["bf16_tflops"], "bf16_sustained": d.get("bf16_tflops_sustained"),
                 "source": "measured"}
     return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sustained": 1400.0, "source": "fallback"}
+
+
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/ncu_traffic.json, built by
+    scripts/profile_r1c.sh); None when that kernel was not captured."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f).get(kernel)
+    return None if d is None else d["bytes_per_launch"]
 
 
 # ---------------------------------------------------------------------------
@@ -341,7 +355,7 @@ def run_ours(args, rank: int, world: int):
     else:
         roof = {"bound": "tensor", "achieved": tv["work"] / (tv["ms"] * 1e-3) / 1e12, "peak": sust,
                 "unit": "TFLOP/s"}
-    roof.update(kernel=top, frac=roof["achieved"] / roof["peak"], traffic=None,
+    roof.update(kernel=top, frac=roof["achieved"] / roof["peak"], traffic=ncu_traffic(top),
                 share_of_step=tv["ms"] / args.steps / ttft,
                 peak_source=f"{pk['source']} ({'HBM copy' if roof['bound'] == 'hbm' else 'bf16 sustained'})")
     stages = None
@@ -535,6 +549,126 @@ def run_sharded(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def run_serving(args, rank: int, world: int):
+    """C5 batched serving: `requests` concurrent RAG requests (64 x 16K ctx)
+    spread round-robin over the ranks (request-parallel replicas, no data-path
+    collective; total work fixed -> strong scaling). Chunks come from a shared
+    corpus pool precomputed once per rank (chunk reuse across requests is the
+    point of CacheClip); each request draws `n_chunks` distinct pool chunks
+    and its own query. A step = all of this rank's requests, back to back;
+    per-request TTFT from CUDA events (p50/p99)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_10129_b200 as cc
+    from paper_2510_10129_b200 import _lib
+    from paper_2510_10129_b200.workloads import WORKLOADS
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _lib.require_device(local)
+    work = WORKLOADS[args.config]
+    n_req = args.requests or work.requests
+    mine = [r for r in range(n_req) if r % world == rank]
+    pool_n = args.pool or 4 * work.n_chunks
+    t0 = time.time()
+    primary = cc.init_model(work.primary, 0, device=dev, source="torch")
+    aux = cc.init_model(work.aux, 1, device=dev, source="torch")
+    v = min(work.primary.vocab_size, work.aux.vocab_size)
+    rng = np.random.default_rng(77)
+    prefix = rng.integers(0, v, work.prefix_len).tolist()
+    pool_ids = [rng.integers(0, v, work.chunk_len).tolist() for _ in range(pool_n)]
+    pool = [cc.prefill_chunk(primary, prefix, c) for c in pool_ids]
+    pool_aux = [cc.prefill_chunk(aux, prefix, c) for c in pool_ids]
+    reqs = []
+    for r in mine:
+        rr = np.random.default_rng(5000 + r)
+        pick = rr.choice(pool_n, work.n_chunks, replace=False)
+        reqs.append(([pool[i] for i in pick], [pool_aux[i] for i in pick],
+                     rr.integers(0, v, work.query_len).tolist()))
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    config = cc.SelectionConfig(args.ratio, 8, args.window_threshold)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step(record=None):
+        rows = 0
+        for ch, ach, q in reqs:
+            if record is not None:
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+            o = cc.cacheclip_prefill(primary, aux, ch, ach, q, config)
+            if record is not None:
+                b.record()
+                record.append((a, b))
+            rows += len(o.plan.indices)
+        return rows
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    barrier()
+    torch.cuda.synchronize()
+    evs, per_req, rows = [], [], 0
+    _lib.profile_collect()
+    with ClockSampler(local) as clocks:
+        _lib.profile_enable(True)
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            rows = step(per_req)
+            e1.record()
+            evs.append((e0, e1))
+        _lib.profile_enable(False)
+        torch.cuda.synchronize()
+    barrier()
+    recs = _lib.profile_collect()
+    step_ms = float(np.mean([a.elapsed_time(b) for a, b in evs]))
+    ttfts = np.array([a.elapsed_time(b) for a, b in per_req])
+    tot = torch.tensor([step_ms, float(rows)], device=dev, dtype=torch.float64)
+    if world > 1:
+        mx = tot.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tot.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        step_ms, all_rows = float(mx[0].item()), float(sm[1].item())
+    else:
+        all_rows = float(rows)
+    launches = sum(2 if op == "lm_head" else 1 for op, _, _ in recs) / args.steps
+    if rank != 0:
+        return
+    line = {
+        "metric": f"recomputed tok/s at recomp {args.ratio:.0%}, {work.name} batched RAG serving "
+                  f"({n_req} requests per step)",
+        "value": all_rows / (step_ms * 1e-3), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, uniform random token ids, shared chunk pool)",
+        "config": {"workload": f"{work.name}: {work.description}", "requests": n_req,
+                   "context_rows": work.context_rows, "chunk_pool": pool_n, "recomp_ratio": args.ratio,
+                   "recomputed_rows_per_step": all_rows,
+                   "window_rule": f"window_len=8, threshold={args.window_threshold}",
+                   "parallelism": f"request-parallel x{world}" if world > 1 else "1 GPU",
+                   "l2": "256 MB flush between timed steps; 1 GB of chunk caches per request > L2"},
+        "requests_per_s": n_req / (step_ms * 1e-3),
+        "ttft_ms": {"p50": float(np.percentile(ttfts, 50)), "p99": float(np.percentile(ttfts, 99)),
+                    "mean": float(ttfts.mean()), "rank0_requests": len(mine)},
+        "gpu_launches": launches, "clocks": clocks.summary(), "setup_s": setup_s,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def WORKLOADS_REQUESTS(name: str) -> int:
+    from paper_2510_10129_b200.workloads import WORKLOADS
+    return WORKLOADS[name].requests
+
+
 def main():
     args = parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -548,6 +682,8 @@ def main():
         run_reference(args, rank, world)
     elif args.sharded:
         run_sharded(args, rank, world)
+    elif WORKLOADS_REQUESTS(args.config) > 1:
+        run_serving(args, rank, world)
     else:
         run_ours(args, rank, world)
     if world > 1:
