@@ -21,7 +21,9 @@
 namespace cc {
 
 constexpr int kBM = 128;
-constexpr int kGemmThreads = 192;
+constexpr int kEpiWarps = 8;  // two per TMEM lane quarter (column halves)
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiStageBytes = 32 * 32 * 4;
 
 template <int BN, bool kTF32>
 struct GemmCfg {
@@ -34,8 +36,9 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN == 256) ? 4 : 6;
   static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + kEpiWarps * kEpiStageBytes + 1024 + 256;
   static constexpr uint32_t IDESC = umma_idesc(kBM, BN, kTF32);
+  static_assert(SMEM_BYTES <= 232448, "GEMM shared memory over the sm_100 per-CTA limit");
 };
 
 struct EpiParams {
@@ -65,157 +68,206 @@ __device__ __forceinline__ float act_apply(int act, float x) {
   return act == CC_ACT_SILU ? silu_f(x) : gelu_tanh_f(x);
 }
 
-// Store 32 consecutive values of one row (cols [col0, col0+32)) in `mode`.
-// `width` = logical row width (split layout uses a 3*width pitch).
-__device__ __forceinline__ void store_row32(void* base, int mode, int64_t row, int64_t ld, int64_t col0,
-                                            int64_t width, const float* v) {
-  const bool full = (col0 + 32 <= width);
+// Store 4 consecutive values of one row (cols [col, col+4)) in `mode`; the
+// split layout keeps a 3*ld row pitch with [hi | hi | lo] segments `width` apart.
+__device__ __forceinline__ void store4(void* base, int mode, int64_t row, int64_t ld, int64_t col, int64_t width,
+                                       float4 v) {
   if (mode == CC_BF16) {
-    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(base) + row * ld + col0;
-    if (full && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint4 u;
-        __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[q * 8 + 2 * i], v[q * 8 + 2 * i + 1]);
-        reinterpret_cast<uint4*>(p)[q] = u;
-      }
-    } else {
-      for (int j = 0; j < 32; ++j)
-        if (col0 + j < width) p[j] = __float2bfloat16_rn(v[j]);
-    }
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&a);
+    u.y = *reinterpret_cast<uint32_t*>(&b);
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(base) + row * ld + col) = u;
   } else if (mode == CC_F32) {
-    float* p = reinterpret_cast<float*>(base) + row * ld + col0;
-    if (full && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q)
-        reinterpret_cast<float4*>(p)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-    } else {
-      for (int j = 0; j < 32; ++j)
-        if (col0 + j < width) p[j] = v[j];
-    }
+    *reinterpret_cast<float4*>(reinterpret_cast<float*>(base) + row * ld + col) = v;
   } else {  // CC_F32_SPLIT3 : [hi | hi | lo]
-    float* p = reinterpret_cast<float*>(base) + row * ld * 3 + col0;
-    if (full && ((reinterpret_cast<uintptr_t>(p) & 15) == 0) && (width & 3) == 0) {
+    float* p = reinterpret_cast<float*>(base) + row * ld * 3 + col;
+    const float e[4] = {v.x, v.y, v.z, v.w};
+    float hi[4], lh[4];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        float hi[4], lh[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float lo, ll;
-          split_tf32(v[4 * q + e], hi[e], lo);
-          split_tf32(lo, lh[e], ll);
-        }
-        const float4 h4 = make_float4(hi[0], hi[1], hi[2], hi[3]);
-        reinterpret_cast<float4*>(p)[q] = h4;
-        reinterpret_cast<float4*>(p + width)[q] = h4;
-        reinterpret_cast<float4*>(p + 2 * width)[q] = make_float4(lh[0], lh[1], lh[2], lh[3]);
-      }
-      return;
+    for (int i = 0; i < 4; ++i) {
+      float lo, ll;
+      split_tf32(e[i], hi[i], lo);
+      split_tf32(lo, lh[i], ll);
     }
-    for (int j = 0; j < 32; ++j) {
-      if (col0 + j < width) {
-        float hi, lo, lh, ll;
-        split_tf32(v[j], hi, lo);
-        split_tf32(lo, lh, ll);
-        p[j] = hi;
-        p[width + j] = hi;
-        p[2 * width + j] = lh;
-      }
-    }
+    const float4 h4 = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<float4*>(p) = h4;
+    *reinterpret_cast<float4*>(p + width) = h4;
+    *reinterpret_cast<float4*>(p + 2 * width) = make_float4(lh[0], lh[1], lh[2], lh[3]);
   }
 }
 
-template <int BN>
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tbase, int c0, int64_t grow,
-                                               int64_t n0, bool row_ok) {
-  float v[32];
-  if (ep.epilogue == CC_EPI_GLU) {
-    float u[32];
-    tmem_ld32(tbase + c0, v);
-    tmem_ld32(tbase + c0 + BN / 2, u);
-    if (!row_ok) return;
-    const int64_t ocol0 = n0 / 2 + c0;  // output column
-    const int64_t gcol = n0 + c0;       // interleaved gate column
+__device__ __forceinline__ float4 ld_bias4(const float* b, int64_t col) {
+  return b ? *reinterpret_cast<const float4*>(b + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+// Epilogue staging: each epilogue warp owns a 32 x 32 fp32 tile in smem.
+// Element (r, c) lives at r*32 + ((c/4) ^ (r%8))*4 + c%4 — a 16-byte-granule
+// XOR swizzle, so both the row-per-lane writes (TMEM layout) and the
+// 8-lanes-per-row reads (coalesced global layout) are bank-conflict free.
+__device__ __forceinline__ void stage_row32(float* stg, int r, const float* v) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      float g = v[j], up = u[j];
-      if (ep.bias) {
-        g += ep.bias[gcol + j];
-        up += ep.bias[gcol + BN / 2 + j];
+  for (int g = 0; g < 8; ++g)
+    *reinterpret_cast<float4*>(stg + r * 32 + ((g ^ (r & 7)) << 2)) =
+        make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+}
+__device__ __forceinline__ float4 unstage4(const float* stg, int r, int g) {
+  return *reinterpret_cast<const float4*>(stg + r * 32 + ((g ^ (r & 7)) << 2));
+}
+
+// One 32-row x 32-column chunk of the accumulator: TMEM -> registers (lane =
+// row) -> swizzled smem -> 8 passes of 4 rows x 8 lanes x 4 columns, so every
+// global access is a contiguous 128-byte (fp32) / 64-byte (bf16) row segment.
+// Row-local math (GLU) runs in the lane-per-row layout; column-indexed math
+// (bias, RoPE pairs, residual) runs in the coalesced layout.
+template <int BN>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tbase, int c0, int64_t row0, int64_t n0,
+                                               float* stg, int lane) {
+  float v[32];
+  int64_t colbase;  // global output column of the chunk's column 0
+  int64_t width;    // logical output width (column bound)
+  if (ep.epilogue == CC_EPI_GLU) {
+    const int64_t gcol = n0 + c0;  // interleaved gate column
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {  // 16 columns at a time (register budget)
+      float u[16];
+      tmem_ld16(tbase + c0 + 16 * hh, v + 16 * hh);
+      tmem_ld16(tbase + c0 + 16 * hh + BN / 2, u);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float g = v[16 * hh + j], up = u[j];
+        if (ep.bias) {
+          g += ep.bias[gcol + 16 * hh + j];
+          up += ep.bias[gcol + BN / 2 + 16 * hh + j];
+        }
+        v[16 * hh + j] = __fmul_rn(act_apply(ep.act, g), up);
       }
-      v[j] = __fmul_rn(act_apply(ep.act, g), up);
     }
-    store_row32(ep.C, ep.c_mode, grow, ep.ldc, ocol0, ep.n_out, v);
+    colbase = n0 / 2 + c0;
+    width = ep.n_out;
+  } else {
+    tmem_ld32(tbase + c0, v);
+    colbase = n0 + c0;
+    width = ep.N;
+  }
+  stage_row32(stg, lane, v);
+  __syncwarp();
+  const int g = lane & 7;
+  const int64_t col = colbase + 4 * g;
+  if (col >= width) {
+    __syncwarp();
     return;
   }
-  tmem_ld32(tbase + c0, v);
-  if (!row_ok) return;
-  const int64_t col0 = n0 + c0;
-  if (col0 >= ep.N) return;
-  if (ep.bias) {
-#pragma unroll
-    for (int j = 0; j < 32; ++j)
-      if (col0 + j < ep.N) v[j] += ep.bias[col0 + j];
-  }
+  // pass p covers rows 4p + lane/8; every global load of the chunk is issued
+  // before the first dependent store (eight independent requests in flight)
+  const int rl = lane >> 3;
+  const int64_t m_left = ep.M - row0;
   switch (ep.epilogue) {
+    case CC_EPI_GLU:
+#pragma unroll
+      for (int ps = 0; ps < 8; ++ps)
+        if (ps * 4 + rl < m_left) store4(ep.C, ep.c_mode, row0 + ps * 4 + rl, ep.ldc, col, width,
+                                         unstage4(stg, ps * 4 + rl, g));
+      break;
     case CC_EPI_STORE:
-      store_row32(ep.C, ep.c_mode, grow, ep.ldc, col0, ep.N, v);
-      break;
-    case CC_EPI_ACT:
+    case CC_EPI_ACT: {
+      const float4 b = ld_bias4(ep.bias, col);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = act_apply(ep.act, v[j]);
-      store_row32(ep.C, ep.c_mode, grow, ep.ldc, col0, ep.N, v);
-      break;
-    case CC_EPI_RESIDUAL: {
-      float* h = reinterpret_cast<float*>(ep.C) + grow * ep.ldc + col0;
-      if (col0 + 32 <= ep.N && ((reinterpret_cast<uintptr_t>(h) & 15) == 0)) {
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          float4 o = reinterpret_cast<float4*>(h)[q];
-          o.x = __fadd_rn(o.x, v[4 * q]);
-          o.y = __fadd_rn(o.y, v[4 * q + 1]);
-          o.z = __fadd_rn(o.z, v[4 * q + 2]);
-          o.w = __fadd_rn(o.w, v[4 * q + 3]);
-          reinterpret_cast<float4*>(h)[q] = o;
+      for (int ps = 0; ps < 8; ++ps) {
+        const int r = ps * 4 + rl;
+        if (r >= m_left) continue;
+        float4 x = unstage4(stg, r, g);
+        x.x += b.x;
+        x.y += b.y;
+        x.z += b.z;
+        x.w += b.w;
+        if (ep.epilogue == CC_EPI_ACT) {
+          x.x = act_apply(ep.act, x.x);
+          x.y = act_apply(ep.act, x.y);
+          x.z = act_apply(ep.act, x.z);
+          x.w = act_apply(ep.act, x.w);
         }
-      } else {
-        for (int j = 0; j < 32; ++j)
-          if (col0 + j < ep.N) h[j] = __fadd_rn(h[j], v[j]);
+        store4(ep.C, ep.c_mode, row0 + r, ep.ldc, col, width, x);
+      }
+      break;
+    }
+    case CC_EPI_RESIDUAL: {
+      const float4 b = ld_bias4(ep.bias, col);
+      float* hb = reinterpret_cast<float*>(ep.C) + row0 * ep.ldc + col;
+      float4 o[8];
+#pragma unroll
+      for (int ps = 0; ps < 8; ++ps)
+        if (ps * 4 + rl < m_left) o[ps] = *reinterpret_cast<const float4*>(hb + (ps * 4 + rl) * ep.ldc);
+#pragma unroll
+      for (int ps = 0; ps < 8; ++ps) {
+        const int r = ps * 4 + rl;
+        if (r >= m_left) continue;
+        const float4 x = unstage4(stg, r, g);
+        float4 y = o[ps];
+        y.x = __fadd_rn(y.x, x.x + b.x);
+        y.y = __fadd_rn(y.y, x.y + b.y);
+        y.z = __fadd_rn(y.z, x.z + b.z);
+        y.w = __fadd_rn(y.w, x.w + b.w);
+        *reinterpret_cast<float4*>(hb + r * ep.ldc) = y;
       }
       break;
     }
     case CC_EPI_QKV_ROPE: {
+      const float4 b = ld_bias4(ep.bias, col);
       const int dh = ep.head_dim;
       const int64_t qw = (int64_t)ep.n_q_heads * dh, kw = (int64_t)ep.n_kv_heads * dh;
-      if (col0 < qw + kw) {  // q or k: rotate adjacent pairs
-        const int half = dh >> 1;
-        const int p0 = (int)(col0 % dh) >> 1;
-        const float* cs = ep.rope_cos + grow * half + p0;
-        const float* sn = ep.rope_sin + grow * half + p0;
-        float r[32];
+      const bool rot = col < qw + kw;
+      const int half = dh >> 1;
+      const int pr = (int)(col % dh) >> 1;
 #pragma unroll
-        for (int p = 0; p < 16; ++p) rope_pair(v[2 * p], v[2 * p + 1], cs[p], sn[p], r[2 * p], r[2 * p + 1]);
-        if (col0 < qw) {
-          store_row32(ep.q_out, ep.q_mode, grow, ep.ldq, col0, qw, r);
-        } else {
-          const int64_t drow = ep.dst_rows ? ep.dst_rows[grow] : grow;
-          store_row32(ep.k_cache, ep.cache_dtype, drow, kw, col0 - qw, kw, r);
-          if (ep.k_raw) {
-            const int64_t rrow = ep.raw_rows ? ep.raw_rows[grow] : grow;
-            store_row32(ep.k_raw, ep.cache_dtype, rrow, kw, col0 - qw, kw, v);
+      for (int half_p = 0; half_p < 2; ++half_p) {  // two batches of 4 passes (register budget)
+        float2 cs[4], sn[4];
+        int64_t drow[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = (half_p * 4 + q) * 4 + rl;
+          const int64_t grow = row0 + r;
+          if (r >= m_left) continue;
+          if (rot) {
+            cs[q] = *reinterpret_cast<const float2*>(ep.rope_cos + grow * half + pr);
+            sn[q] = *reinterpret_cast<const float2*>(ep.rope_sin + grow * half + pr);
+          }
+          if (col >= qw) drow[q] = ep.dst_rows ? ep.dst_rows[grow] : grow;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = (half_p * 4 + q) * 4 + rl;
+          if (r >= m_left) continue;
+          const int64_t grow = row0 + r;
+          float4 x = unstage4(stg, r, g);
+          x.x += b.x;
+          x.y += b.y;
+          x.z += b.z;
+          x.w += b.w;
+          if (rot) {
+            float4 r4;
+            rope_pair(x.x, x.y, cs[q].x, sn[q].x, r4.x, r4.y);
+            rope_pair(x.z, x.w, cs[q].y, sn[q].y, r4.z, r4.w);
+            if (col < qw) {
+              store4(ep.q_out, ep.q_mode, grow, ep.ldq, col, qw, r4);
+            } else {
+              store4(ep.k_cache, ep.cache_dtype, drow[q], kw, col - qw, kw, r4);
+              if (ep.k_raw) {
+                const int64_t rrow = ep.raw_rows ? ep.raw_rows[grow] : grow;
+                store4(ep.k_raw, ep.cache_dtype, rrow, kw, col - qw, kw, x);
+              }
+            }
+          } else {
+            store4(ep.v_cache, ep.cache_dtype, drow[q], kw, col - qw - kw, kw, x);
           }
         }
-      } else {
-        const int64_t drow = ep.dst_rows ? ep.dst_rows[grow] : grow;
-        store_row32(ep.v_cache, ep.cache_dtype, drow, kw, col0 - qw - kw, kw, v);
       }
       break;
     }
     default:
       break;
   }
+  __syncwarp();  // the staging tile is reused by the next chunk
 }
 
 template <int BN, bool kTF32>
@@ -228,7 +280,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
   uint8_t* smem_a = smem;
   uint8_t* smem_b = smem + Cfg::STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+  uint8_t* smem_epi = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + kEpiWarps * kEpiStageBytes);
   uint64_t* empty = full + Cfg::STAGES;
   uint64_t* tfull = empty + Cfg::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -246,7 +299,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], kEpiWarps);
     }
     fence_barrier_init();
   }
@@ -309,20 +362,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
   } else {
-    // epilogue warps 2..5: TMEM lane quarter = warp % 4
+    // epilogue warps 2..9: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
+    const int ew = warp - 2;
     const int quarter = warp & 3;
+    const int chalf = ew >> 2;
+    float* stg = reinterpret_cast<float*>(smem_epi + ew * kEpiStageBytes);
     int acc = 0;
     uint32_t acc_phase = 0;
+    // GLU tiles produce BN/2 output columns (gate/up pairs), others BN
+    const int cols = (ep.epilogue == CC_EPI_GLU) ? BN / 2 : BN;
+    const int c_begin = chalf * (cols / 2), c_end = c_begin + cols / 2;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int mb = t % num_m, nb = t / num_m;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(quarter * 32) << 16);
-      const int64_t grow = (int64_t)mb * kBM + quarter * 32 + lane;
-      const bool row_ok = grow < ep.M;
+      const int64_t row0 = (int64_t)mb * kBM + quarter * 32;
       const int64_t n0 = (int64_t)nb * BN;
-      const int cols = (ep.epilogue == CC_EPI_GLU) ? BN / 2 : BN;
-      for (int c0 = 0; c0 < cols; c0 += 32) epilogue_chunk<BN>(ep, tbase, c0, grow, n0, row_ok);
+      for (int c0 = c_begin; c0 < c_end; c0 += 32) epilogue_chunk<BN>(ep, tbase, c0, row0, n0, stg, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -413,6 +470,10 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   CC_CHECK_ARG(((uintptr_t)a->A % 16) == 0 && ((uintptr_t)a->B % 16) == 0, CC_ERR_UNSUPPORTED,
                "operands must be 16-byte aligned");
   CC_CHECK_ARG(a->N % 16 == 0, CC_ERR_UNSUPPORTED, "N=%lld must be a multiple of 16", (long long)a->N);
+  // the epilogue writes 4-column vectors (16 B fp32 / 8 B bf16)
+  CC_CHECK_ARG(a->ldc % 4 == 0 && a->ldq % 4 == 0 && a->n_out % 4 == 0 && ((uintptr_t)a->C % 16) == 0 &&
+                   ((uintptr_t)a->q_out % 16) == 0,
+               CC_ERR_UNSUPPORTED, "GEMM outputs must be 16-byte aligned with row pitches a multiple of 4");
   EpiParams ep{};
   ep.epilogue = a->epilogue;
   ep.M = a->M;
