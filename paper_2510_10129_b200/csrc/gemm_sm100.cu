@@ -7,8 +7,11 @@
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, fp32 in TMEM)
 //   warps 2..5  epilogue: tcgen05.ld 32x32b -> registers -> fused op -> global
 // Two TMEM accumulators (2 x BN columns) let the epilogue of tile i overlap the
-// MMAs of tile i+1. kind::f16 (bf16) for the primary model; kind::tf32 over
-// [hi|hi|lo]·[hi|lo|hi] operands (3xTF32, fp32-faithful) for the scoring model.
+// MMAs of tile i+1. kind::f16 (bf16) for the primary model; kind::tf32 for the
+// scoring model as 3xTF32 (fp32-faithful): operands are stored split, A' =
+// [hi|hi|lo] and B' = [hi|lo|hi]; a pipeline stage holds the hi and lo
+// sub-tiles of both (each loaded once) and feeds three MMAs: hi*hi into one
+// accumulator, hi*lo + lo*hi into a second; the epilogue adds the two in fp32.
 //
 // Replaces the numpy `x @ W` of attention_qkv / _attn_project_out / _mlp
 // (model.py:340-432) and fuses bias, RoPE + K/V scatter (model.py:709-714),
@@ -31,13 +34,25 @@ struct GemmCfg {
   static constexpr int BK = 128 / ELEM;  // one 128-byte swizzle row per tile row
   static constexpr int UK = kTF32 ? 8 : 16;
   static constexpr int KSTEPS = BK / UK;
-  static constexpr int A_BYTES = kBM * 128;
-  static constexpr int B_BYTES = BN * 128;
+  // 3xTF32: a stage holds the hi and lo sub-tiles of both operands (loaded
+  // once, consumed by the three MMAs hi*hi, hi*lo, lo*hi)
+  static constexpr int NSUB = kTF32 ? 2 : 1;
+  static constexpr int A_SUB = kBM * 128;
+  static constexpr int B_SUB = BN * 128;
+  static constexpr int A_BYTES = NSUB * A_SUB;
+  static constexpr int B_BYTES = NSUB * B_SUB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : 6;
-  static constexpr int TMEM_COLS = 2 * BN;  // two accumulators
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + kEpiWarps * kEpiStageBytes + 1024 + 256;
+  static constexpr int FIXED = kEpiWarps * kEpiStageBytes + 1024 + 256;
+  static constexpr int FIT = (232448 - FIXED) / STAGE_BYTES;
+  static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+  // two accumulator buffers; 3xTF32 keeps hi*hi and the hi*lo + lo*hi
+  // corrections in separate accumulators (summed in fp32 by the epilogue)
+  static constexpr int ACC_STRIDE = kTF32 ? 2 * BN : BN;
+  static constexpr int TMEM_COLS = 2 * ACC_STRIDE;
+  static_assert(TMEM_COLS <= 512, "TMEM holds 512 columns");
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
   static constexpr uint32_t IDESC = umma_idesc(kBM, BN, kTF32);
+  static_assert(STAGES >= 2, "GEMM pipeline needs two stages");
   static_assert(SMEM_BYTES <= 232448, "GEMM shared memory over the sm_100 per-CTA limit");
 };
 
@@ -49,6 +64,7 @@ struct EpiParams {
   int64_t ldc;
   int c_mode;
   int act;
+  int glu_block;
   int64_t n_out;
   int n_q_heads, n_kv_heads, head_dim;
   const float* rope_cos;
@@ -120,34 +136,58 @@ __device__ __forceinline__ float4 unstage4(const float* stg, int r, int g) {
 // global access is a contiguous 128-byte (fp32) / 64-byte (bf16) row segment.
 // Row-local math (GLU) runs in the lane-per-row layout; column-indexed math
 // (bias, RoPE pairs, residual) runs in the coalesced layout.
+// First weight row of half `h` (0: columns [0, BN/2), 1: [BN/2, BN)) of tile
+// column block nb. GLU weights interleave gate/up in blocks of glu_block rows;
+// a GLU tile holds BN/2 gate rows and the matching BN/2 up rows, so the
+// epilogue finds gate at accumulator column c and up at c + BN/2.
 template <int BN>
-__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tbase, int c0, int64_t row0, int64_t n0,
+__device__ __forceinline__ int b_row(const EpiParams& ep, int nb, int h) {
+  if (ep.epilogue != CC_EPI_GLU) return nb * BN + h * (BN / 2);
+  const int per_blk = 2 * ep.glu_block / BN;  // tiles per gate/up block pair
+  return (nb / per_blk) * 2 * ep.glu_block + (nb % per_blk) * (BN / 2) + h * ep.glu_block;
+}
+
+// accumulator columns [c, c+n) (+ the 3xTF32 correction accumulator)
+template <int BN, bool kTF32>
+__device__ __forceinline__ void acc_ld16(uint32_t taddr, float* v) {
+  tmem_ld16(taddr, v);
+  if constexpr (kTF32) {
+    float w[16];
+    tmem_ld16(taddr + BN, w);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = __fadd_rn(v[j], w[j]);
+  }
+}
+
+template <int BN, bool kTF32>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tbase, int c0, int64_t row0, int nb,
                                                float* stg, int lane) {
   float v[32];
   int64_t colbase;  // global output column of the chunk's column 0
   int64_t width;    // logical output width (column bound)
   if (ep.epilogue == CC_EPI_GLU) {
-    const int64_t gcol = n0 + c0;  // interleaved gate column
+    const int64_t gcol = b_row<BN>(ep, nb, 0) + c0;  // interleaved gate row of column c0
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {  // 16 columns at a time (register budget)
       float u[16];
-      tmem_ld16(tbase + c0 + 16 * hh, v + 16 * hh);
-      tmem_ld16(tbase + c0 + 16 * hh + BN / 2, u);
+      acc_ld16<BN, kTF32>(tbase + c0 + 16 * hh, v + 16 * hh);
+      acc_ld16<BN, kTF32>(tbase + c0 + 16 * hh + BN / 2, u);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         float g = v[16 * hh + j], up = u[j];
         if (ep.bias) {
           g += ep.bias[gcol + 16 * hh + j];
-          up += ep.bias[gcol + BN / 2 + 16 * hh + j];
+          up += ep.bias[gcol + ep.glu_block + 16 * hh + j];
         }
         v[16 * hh + j] = __fmul_rn(act_apply(ep.act, g), up);
       }
     }
-    colbase = n0 / 2 + c0;
+    colbase = (int64_t)nb * (BN / 2) + c0;
     width = ep.n_out;
   } else {
-    tmem_ld32(tbase + c0, v);
-    colbase = n0 + c0;
+    acc_ld16<BN, kTF32>(tbase + c0, v);
+    acc_ld16<BN, kTF32>(tbase + c0 + 16, v + 16);
+    colbase = (int64_t)nb * BN + c0;
     width = ep.N;
   }
   stage_row32(stg, lane, v);
@@ -273,7 +313,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tba
 template <int BN, bool kTF32>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
-                int num_m, int num_n, int num_kb) {
+                int num_m, int num_n, int num_kb, int k_orig) {
   using Cfg = GemmCfg<BN, kTF32>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -318,8 +358,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          tma_load_2d(smem_a + stage * Cfg::A_BYTES, &tmA, &full[stage], kb * Cfg::BK, mb * kBM);
-          tma_load_2d(smem_b + stage * Cfg::B_BYTES, &tmB, &full[stage], kb * Cfg::BK, nb * BN);
+          uint8_t* sa = smem_a + stage * Cfg::A_BYTES;
+          uint8_t* sb = smem_b + stage * Cfg::B_BYTES;
+          tma_load_2d(sa, &tmA, &full[stage], kb * Cfg::BK, mb * kBM);
+          const int br0 = b_row<BN>(ep, nb, 0), br1 = b_row<BN>(ep, nb, 1);
+          tma_load_2d(sb, &tmB, &full[stage], kb * Cfg::BK, br0);
+          tma_load_2d(sb + Cfg::B_SUB / 2, &tmB, &full[stage], kb * Cfg::BK, br1);
+          if constexpr (kTF32) {  // A' = [hi | hi | lo], B' = [hi | lo | hi]
+            tma_load_2d(sa + Cfg::A_SUB, &tmA, &full[stage], 2 * k_orig + kb * Cfg::BK, mb * kBM);
+            tma_load_2d(sb + Cfg::B_SUB, &tmB, &full[stage], k_orig + kb * Cfg::BK, br0);
+            tma_load_2d(sb + Cfg::B_SUB + Cfg::B_SUB / 2, &tmB, &full[stage], k_orig + kb * Cfg::BK, br1);
+          }
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -335,7 +384,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * BN;
+      const uint32_t d_tmem = tmem_base + acc * Cfg::ACC_STRIDE;
       for (int kb = 0; kb < num_kb; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
@@ -346,6 +395,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int k = 0; k < Cfg::KSTEPS; ++k) {
             tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
                           (kb | k) != 0 ? 1u : 0u);
+            if constexpr (kTF32) {  // corrections hi*lo + lo*hi into the second accumulator
+              tc_mma<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + Cfg::B_SUB + k * 32),
+                            Cfg::IDESC, (kb | k) != 0 ? 1u : 0u);
+              tc_mma<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + Cfg::A_SUB + k * 32), umma_desc_sw128(b0 + k * 32),
+                            Cfg::IDESC, 1u);
+            }
           }
           tc_commit(&empty[stage]);
           if (kb == num_kb - 1) tc_commit(&tfull[acc]);
@@ -376,10 +431,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int mb = t % num_m, nb = t / num_m;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(quarter * 32) << 16);
+      const uint32_t tbase = tmem_base + acc * Cfg::ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
       const int64_t row0 = (int64_t)mb * kBM + quarter * 32;
-      const int64_t n0 = (int64_t)nb * BN;
-      for (int c0 = c_begin; c0 < c_end; c0 += 32) epilogue_chunk<BN>(ep, tbase, c0, row0, n0, stg, lane);
+      for (int c0 = c_begin; c0 < c_end; c0 += 32)
+        epilogue_chunk<BN, kTF32>(ep, tbase, c0, row0, nb, stg, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -433,7 +488,7 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   CUtensorMap ta, tb;
   int rc = make_map(&ta, a->A, kTF32, kop, a->M, a->lda, Cfg::BK, kBM);
   if (rc) return rc;
-  rc = make_map(&tb, a->B, kTF32, kop, a->N, a->ldb, Cfg::BK, BN);
+  rc = make_map(&tb, a->B, kTF32, kop, a->N, a->ldb, Cfg::BK, BN / 2);
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
@@ -442,11 +497,12 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   }
   const int num_m = (int)((a->M + kBM - 1) / kBM);
   const int num_n = (int)((a->N + BN - 1) / BN);
-  const int num_kb = (int)((kop + Cfg::BK - 1) / Cfg::BK);
+  // 3xTF32 iterates the original K (hi/lo sub-tiles per stage)
+  const int num_kb = (int)(((kTF32 ? a->K : kop) + Cfg::BK - 1) / Cfg::BK);
   const int tiles = num_m * num_n;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
-  gemm_kernel<BN, kTF32><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb);
+  gemm_kernel<BN, kTF32><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb, (int)a->K);
   CC_LAUNCH_CHECK("gemm");
   return CC_OK;
 }
@@ -462,6 +518,8 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   if (a->M == 0) return CC_OK;
   const bool tf32 = a->kind == CC_GEMM_TF32X3;
   CC_CHECK_ARG(tf32 || a->kind == CC_GEMM_BF16, CC_ERR_UNSUPPORTED, "gemm kind %d", a->kind);
+  CC_CHECK_ARG(!tf32 || a->K % 32 == 0, CC_ERR_UNSUPPORTED, "3xTF32 GEMM needs K %% 32 == 0 (K=%lld)",
+               (long long)a->K);
   const int64_t kop = tf32 ? 3 * a->K : a->K;
   const int esz = tf32 ? 4 : 2;
   CC_CHECK_ARG(a->lda >= kop && a->ldb >= kop, CC_ERR_DIMENSION, "leading dimension smaller than K");
@@ -483,6 +541,7 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   ep.ldc = a->ldc;
   ep.c_mode = a->c_mode;
   ep.act = a->act;
+  ep.glu_block = a->glu_block;
   ep.n_out = a->n_out;
   ep.n_q_heads = a->n_q_heads;
   ep.n_kv_heads = a->n_kv_heads;
@@ -515,6 +574,7 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
     wide = t256 >= 2 * num_sms() || a->N % 128 != 0;
   }
   cudaStream_t st = as_stream(stream);
-  if (tf32) return wide ? launch<256, true>(a, ep, kop, st) : launch<128, true>(a, ep, kop, st);
+  // 3xTF32 runs 128-wide tiles: two accumulators (hi*hi, corrections) x two buffers fill TMEM
+  if (tf32) return launch<128, true>(a, ep, kop, st);
   return wide ? launch<256, false>(a, ep, kop, st) : launch<128, false>(a, ep, kop, st);
 }
