@@ -279,8 +279,8 @@ def run_ours(args, rank: int, world: int):
     primary = cc.init_model(work.primary, 0, device=dev, source="torch")
     aux = cc.init_model(work.aux, 1, device=dev, source="torch")
     prefix, chunk_ids, query = work.token_ids(1000 + rank)
-    chunks = [cc.prefill_chunk(primary, prefix, c) for c in chunk_ids]
-    aux_chunks = [cc.prefill_chunk(aux, prefix, c) for c in chunk_ids]
+    chunks = cc.prefill_chunks(primary, prefix, chunk_ids)
+    aux_chunks = cc.prefill_chunks(aux, prefix, chunk_ids)
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     config = cc.SelectionConfig(args.ratio, 8, args.window_threshold)
@@ -382,6 +382,37 @@ def run_ours(args, rank: int, world: int):
             torch_full_ms = None
             print(f"torch full-prefill baseline skipped: {exc}", file=sys.stderr)
 
+    # ---- chunk precompute: per-chunk loop vs one batched pass
+    precompute = None
+    if not args.skip_full:
+        from paper_2510_10129_b200.flops import layer_linear_macs
+
+        def pre_time(fn, reps=2):
+            fn()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(reps):
+                flush.fill_(1)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                fn()
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            return float(np.mean(ts))
+
+        n_rows = [len(prefix) + len(c) for c in chunk_ids]
+        precompute = {"chunks": len(chunk_ids), "rows": int(sum(n_rows))}
+        for tag, mdl in (("primary", primary), ("scoring", aux)):
+            c = mdl.config
+            fl = 2.0 * sum(c.n_layers * (layer_linear_macs(c, n) + 2 * c.n_heads * c.d_head * n * (n + 1) // 2)
+                           for n in n_rows)
+            t_one = pre_time(lambda: [cc.prefill_chunk(mdl, prefix, x) for x in chunk_ids])
+            t_bat = pre_time(lambda: cc.prefill_chunks(mdl, prefix, chunk_ids))
+            precompute[tag] = {"per_chunk_ms": t_one, "batched_ms": t_bat, "speedup": t_one / t_bat,
+                               "chunks_per_s": len(chunk_ids) / (t_bat * 1e-3),
+                               "tflops": fl / (t_bat * 1e-3) / 1e12}
+
     # ---- default 8/5 window rule (paper-faithful) effective ratio ----------
     dflt = step(cfg=cc.SelectionConfig(args.ratio))
     torch.cuda.synchronize()
@@ -467,6 +498,7 @@ def run_ours(args, rank: int, world: int):
                          "effective_ratio": dflt.plan.effective_ratio},
         "roofline": roof,
         "kernels": kernels,
+        "chunk_precompute": precompute,
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks.summary(), "sweep": sweep or None, "setup_s": setup_s,
     }
@@ -496,8 +528,8 @@ def run_sharded(args, rank: int, world: int):
     prefix, chunk_ids, query = work.token_ids(1000)  # one request, identical on every rank
     plan = plan_shards([len(c) for c in chunk_ids], len(prefix), len(query), world, rank)
     mine = plan.local_chunks()
-    chunks = [cc.prefill_chunk(primary, prefix, chunk_ids[c]) for c in mine]
-    aux_chunks = [cc.prefill_chunk(aux, prefix, chunk_ids[c]) for c in mine]
+    chunks = cc.prefill_chunks(primary, prefix, [chunk_ids[c] for c in mine])
+    aux_chunks = cc.prefill_chunks(aux, prefix, [chunk_ids[c] for c in mine])
     torch.cuda.synchronize()
     setup_s = time.time() - t0
     config = cc.SelectionConfig(args.ratio, 8, args.window_threshold)
@@ -579,8 +611,8 @@ def run_serving(args, rank: int, world: int):
     rng = np.random.default_rng(77)
     prefix = rng.integers(0, v, work.prefix_len).tolist()
     pool_ids = [rng.integers(0, v, work.chunk_len).tolist() for _ in range(pool_n)]
-    pool = [cc.prefill_chunk(primary, prefix, c) for c in pool_ids]
-    pool_aux = [cc.prefill_chunk(aux, prefix, c) for c in pool_ids]
+    pool = cc.prefill_chunks(primary, prefix, pool_ids)
+    pool_aux = cc.prefill_chunks(aux, prefix, pool_ids)
     reqs = []
     for r in mine:
         rr = np.random.default_rng(5000 + r)

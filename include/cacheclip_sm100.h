@@ -160,6 +160,15 @@ int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions
                             int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
                             float factor, const float* row_factor,
                             void* out, int64_t ldo, void* stream);
+/* Same with a per-row first key (key_start NULL: 0): row i attends bank rows
+ * [key_start[i], key_start[i] + positions[i]] — many independent sequences
+ * in one bank (batched prefill_chunk, model.py:538-565, one pass for all
+ * chunks). */
+int cc_sparse_row_attention_ranged(const void* q, int64_t ldq, const int64_t* positions,
+                                   const int64_t* key_start, int64_t m, const void* k_cache,
+                                   const void* v_cache, int64_t n_keys, int32_t n_q_heads,
+                                   int32_t n_kv_heads, int32_t head_dim, float factor,
+                                   const float* row_factor, void* out, int64_t ldo, void* stream);
 /* Split-KV partial attention for sequence-sharded caches:
  * same kernel, but row i attends local keys [0, limits[i]] (limits = local
  * index of its last visible key, -1 = none; cc_local_limits) and writes the
@@ -296,6 +305,11 @@ typedef struct {
   void* const* layer_ready;             /* optional host array of cudaEvent_t: layer l's
                                            QKV/attention wait for layer_ready[l] (a merge
                                            still streaming in on another stream) */
+  const int64_t* key_start;             /* optional first visible key per row (NULL: 0):
+                                           row r sees keys [key_start[r],
+                                           key_start[r] + positions[r] + 1) — one bank
+                                           holding many independent sequences (batched
+                                           chunk precompute) */
 } cc_kv_plan;
 
 /* Last-layer scoring (selector.py:157-165): weights workspace

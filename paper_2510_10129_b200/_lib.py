@@ -74,7 +74,7 @@ class KvPlan(ctypes.Structure):
     _fields_ = [("k_scatter", vp), ("k_scatter_stride", i64), ("v_scatter", vp), ("v_scatter_stride", i64),
                 ("dst_rows", vp), ("k_raw", vp), ("k_raw_stride", i64), ("raw_rows", vp),
                 ("attn_k", vp), ("attn_k_stride", i64), ("attn_v", vp), ("attn_v_stride", i64),
-                ("layer_ready", ctypes.POINTER(vp))]
+                ("layer_ready", ctypes.POINTER(vp)), ("key_start", vp)]
 
 
 class ScoreSpec(ctypes.Structure):
@@ -94,6 +94,8 @@ _SIGS = {
     "cc_convert_matrix": ([vp, i64, i64, vp, i32, i32, vp], i32),
     "cc_gemm": ([ctypes.POINTER(GemmArgs), vp], i32),
     "cc_sparse_row_attention": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),
+    "cc_sparse_row_attention_ranged": ([vp, i64, vp, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp],
+                                       i32),
     "cc_sparse_row_attention_partial": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, vp, vp], i32),
     "cc_local_limits": ([vp, i64, vp, i64, vp, vp], i32),
     "cc_lse_merge": ([vp, vp, i32, i64, i64, i32, i32, vp, i64, i32, vp], i32),

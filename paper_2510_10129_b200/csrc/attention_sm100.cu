@@ -181,7 +181,8 @@ constexpr int kFaPolyPairs = CC_FA_POLY;
 template <int D>
 __global__ void __launch_bounds__(kFaThreads, 1)
     fa_sparse_row_kernel(const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-                         const __nv_bfloat16* __restrict__ q, int64_t ldq, const int64_t* __restrict__ pos, int64_t m,
+                         const __nv_bfloat16* __restrict__ q, int64_t ldq, const int64_t* __restrict__ pos,
+                         const int64_t* __restrict__ kstart, int64_t m,
                          int64_t n_keys, int n_q_heads, int n_kv_heads, float factor,
                          const float* __restrict__ row_factor, __nv_bfloat16* __restrict__ out, int64_t ldo,
                          int n_ctas, float* __restrict__ o_part, float* __restrict__ lse_part) {
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   uint64_t* pv_done = bars + 10;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
   int* s_kmax = reinterpret_cast<int*>(bars + 12);
+  int* s_kmin = s_kmax + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = n_q_heads / n_kv_heads;
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     }
     mbar_init(pv_done, 1);
     *s_kmax = 0;
+    *s_kmin = 0x7fffffff;
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   const int tq = warp >= 4 ? (warp - 4) >> 2 : 0;  // query tile of this softmax warp
   const int quarter = warp & 3;                     // TMEM lane quarter
   const int r = quarter * 32 + lane;                // row within the tile
-  int lim = 0;
+  int lim = 0, ks = 0x7fffffff;  // this row sees keys [ks, lim)
   float scale2 = 0.f;
   int64_t out_off = -1, part_row = -1;
   if (warp >= 4) {
@@ -237,7 +240,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       const int64_t i = p / G;
       const int head = kvh * G + (int)(p % G);
       part_row = i * n_q_heads + head;
-      lim = (int)min(pos[i] + 1, n_keys);
+      ks = kstart ? (int)kstart[i] : 0;
+      lim = (int)min(ks + pos[i] + 1, n_keys);
       scale2 = (row_factor ? row_factor[i] : factor) * 1.4426950408889634f;
       src = reinterpret_cast<const uint4*>(q + i * ldq + (int64_t)head * D);
       out_off = i * ldo + (int64_t)head * D;
@@ -250,16 +254,25 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       *reinterpret_cast<uint4*>(qt + kb * (kFaTileRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
     }
     fence_proxy_async_smem();
-    int mx = lim;
+    int mx = lim, mn = ks;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0) atomicMax(s_kmax, mx);
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0) {
+      atomicMax(s_kmax, mx);
+      atomicMin(s_kmin, mn);
+    }
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int n_tiles = (*s_kmax + kFaKeys - 1) / kFaKeys;
+  // key tiles [j0, j0 + n_tiles) cover every row's range (rows are sorted, so a
+  // CTA's ranges are nearly contiguous; tiles outside a row's range are masked)
+  const int j0 = *s_kmax > 0 ? *s_kmin / kFaKeys : 0;
+  const int n_tiles = (*s_kmax + kFaKeys - 1) / kFaKeys - j0;
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kFaCtlRegs));
@@ -275,11 +288,11 @@ __global__ void __launch_bounds__(kFaThreads, 1)
           mbar_arrive_expect_tx(&k_full[s], Cfg::KT_BYTES);
   #pragma unroll
           for (int kb = 0; kb < Cfg::KB; ++kb)
-            tma_load_3d(sK + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmK, &k_full[s], kb * 64, kvh, j * kFaKeys);
+            tma_load_3d(sK + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmK, &k_full[s], kb * 64, kvh, (j0 + j) * kFaKeys);
           mbar_arrive_expect_tx(&v_full[s], Cfg::KT_BYTES);
   #pragma unroll
           for (int kb = 0; kb < Cfg::KB; ++kb)
-            tma_load_3d(sV + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmV, &v_full[s], kb * 64, kvh, j * kFaKeys);
+            tma_load_3d(sV + s * Cfg::KT_BYTES + kb * (kFaKeys * 128), &tmV, &v_full[s], kb * 64, kvh, (j0 + j) * kFaKeys);
         }
       }
     } else if (warp == 1) {
@@ -344,9 +357,12 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + Cfg::s_col(tq);
     const uint32_t o_addr = tmem + lane_base + Cfg::o_col(tq);
-    int warp_min = out_off >= 0 ? lim : 0x7fffffff;
+    int warp_min = out_off >= 0 ? lim : 0x7fffffff, warp_ks = out_off >= 0 ? ks : 0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) warp_min = min(warp_min, __shfl_xor_sync(0xffffffffu, warp_min, o));
+    for (int o = 16; o > 0; o >>= 1) {
+      warp_min = min(warp_min, __shfl_xor_sync(0xffffffffu, warp_min, o));
+      warp_ks = max(warp_ks, __shfl_xor_sync(0xffffffffu, warp_ks, o));
+    }
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(&s_full[tq], j & 1);
@@ -355,10 +371,10 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       float sv[kFaKeys];
 #pragma unroll
       for (int c = 0; c < kFaKeys / 32; ++c) tmem_ld32(s_addr + c * 32, sv + c * 32);
-      const int key0 = j * kFaKeys;
-      if (key0 + kFaKeys > warp_min) {  // boundary tile: apply the per-row causal limit
+      const int key0 = (j0 + j) * kFaKeys;
+      if (key0 + kFaKeys > warp_min || key0 < warp_ks) {  // boundary tile: apply the per-row key range
 #pragma unroll
-        for (int c = 0; c < kFaKeys; ++c) sv[c] = (key0 + c < lim) ? sv[c] : -INFINITY;
+        for (int c = 0; c < kFaKeys; ++c) sv[c] = (key0 + c < lim && key0 + c >= ks) ? sv[c] : -INFINITY;
       }
       // row max as four independent 3-input chains (FMNMX3), short dependency depth
       float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
@@ -486,7 +502,8 @@ static int make_kv_map(CUtensorMap* map, const void* base, int64_t n_keys, int h
 }
 
 template <int D>
-static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64_t m, const void* k_cache,
+static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const int64_t* kstart, int64_t m,
+                     const void* k_cache,
                      const void* v_cache, int64_t n_keys, int32_t hq, int32_t hkv, float factor,
                      const float* row_factor, void* out, int64_t ldo, cudaStream_t st, double flops,
                      float* o_part = nullptr, float* lse_part = nullptr) {
@@ -505,7 +522,7 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, int64
   dim3 grid(n_ctas, hkv);
   ProfScope ps(st, OP_ATTENTION, flops);
   fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
-      tk, tv, (const __nv_bfloat16*)q, ldq, positions, m, n_keys, hq, hkv, factor, row_factor,
+      tk, tv, (const __nv_bfloat16*)q, ldq, positions, kstart, m, n_keys, hq, hkv, factor, row_factor,
       (__nv_bfloat16*)out, ldo, n_ctas, o_part, lse_part);
   CC_LAUNCH_CHECK("fa_sparse_row");
   return CC_OK;
@@ -579,24 +596,35 @@ extern "C" int cc_debug_fa_trace(long long* out) {
 // knows sum(pos+1) on the host; 0 when unknown)
 double g_attn_flops = 0.0;
 
-extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions, int64_t m,
-                                       const void* k_cache, const void* v_cache, int64_t n_keys, int32_t n_q_heads,
-                                       int32_t n_kv_heads, int32_t head_dim, float factor, const float* row_factor,
-                                       void* out, int64_t ldo, void* stream) {
+extern "C" int cc_sparse_row_attention_ranged(const void* q, int64_t ldq, const int64_t* positions,
+                                              const int64_t* key_start, int64_t m, const void* k_cache,
+                                              const void* v_cache, int64_t n_keys, int32_t n_q_heads,
+                                              int32_t n_kv_heads, int32_t head_dim, float factor,
+                                              const float* row_factor, void* out, int64_t ldo, void* stream) {
   CC_CHECK_ARG(n_kv_heads > 0 && n_q_heads % n_kv_heads == 0, CC_ERR_DIMENSION,
                "query heads %d not a multiple of kv heads %d", n_q_heads, n_kv_heads);
   CC_CHECK_ARG(head_dim == 64 || head_dim == 128, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
   CC_CHECK_ARG(n_keys > 0, CC_ERR_VALUE, "attention row with no visible keys");
+  CC_CHECK_ARG(n_keys < (int64_t)1 << 31, CC_ERR_UNSUPPORTED, "key bank of %lld rows too large",
+               (long long)n_keys);
   CC_CHECK_ARG(((uintptr_t)k_cache % 16) == 0 && ((uintptr_t)v_cache % 16) == 0 && ((uintptr_t)q % 16) == 0 &&
                    (ldq % 8) == 0 && (ldo % 8) == 0,
                CC_ERR_UNSUPPORTED, "attention operands must be 16-byte aligned");
   if (m <= 0) return CC_OK;
   cudaStream_t st = as_stream(stream);
   if (head_dim == 128)
-    return fa_launch<128>(q, ldq, positions, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
-                          out, ldo, st, g_attn_flops);
-  return fa_launch<64>(q, ldq, positions, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
-                       out, ldo, st, g_attn_flops);
+    return fa_launch<128>(q, ldq, positions, key_start, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor,
+                          row_factor, out, ldo, st, g_attn_flops);
+  return fa_launch<64>(q, ldq, positions, key_start, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor,
+                       row_factor, out, ldo, st, g_attn_flops);
+}
+
+extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions, int64_t m,
+                                       const void* k_cache, const void* v_cache, int64_t n_keys, int32_t n_q_heads,
+                                       int32_t n_kv_heads, int32_t head_dim, float factor, const float* row_factor,
+                                       void* out, int64_t ldo, void* stream) {
+  return cc_sparse_row_attention_ranged(q, ldq, positions, nullptr, m, k_cache, v_cache, n_keys, n_q_heads,
+                                        n_kv_heads, head_dim, factor, row_factor, out, ldo, stream);
 }
 
 extern "C" int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const int64_t* limits, int64_t m,
@@ -616,9 +644,9 @@ extern "C" int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const
     return CC_OK;
   }
   if (head_dim == 128)
-    return fa_launch<128>(q, ldq, limits, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
+    return fa_launch<128>(q, ldq, limits, nullptr, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
                           nullptr, 0, st, g_attn_flops, o_part, lse);
-  return fa_launch<64>(q, ldq, limits, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
+  return fa_launch<64>(q, ldq, limits, nullptr, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
                        nullptr, 0, st, g_attn_flops, o_part, lse);
 }
 

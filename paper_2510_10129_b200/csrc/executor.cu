@@ -173,9 +173,10 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
     a.raw_rows = plan->raw_rows;
     CC_TRY(cc_gemm(&a, stream));
     g_attn_flops = 4.0 * md->n_heads * md->head_dim * attn_pairs;
-    CC_TRY(cc_sparse_row_attention(q, qw, positions, R, lp(plan->attn_k, plan->attn_k_stride, l),
-                                   lp(plan->attn_v, plan->attn_v_stride, l), n_keys, md->n_heads, md->n_kv_heads,
-                                   md->head_dim, factor, row_factor, ctx, qw, stream));
+    CC_TRY(cc_sparse_row_attention_ranged(q, qw, positions, plan->key_start, R,
+                                          lp(plan->attn_k, plan->attn_k_stride, l),
+                                          lp(plan->attn_v, plan->attn_v_stride, l), n_keys, md->n_heads,
+                                          md->n_kv_heads, md->head_dim, factor, row_factor, ctx, qw, stream));
     g_attn_flops = 0.0;
     CC_TRY(gemm_call(CC_GEMM_BF16, CC_EPI_RESIDUAL, R, d, qw, ctx, qw, lw.w_o, qw, lw.b_o, h, d, CC_F32, 0, 0,
                      stream));

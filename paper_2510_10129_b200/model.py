@@ -131,6 +131,76 @@ def prefill_chunk(model: Model, prefix_ids: Sequence[int], chunk_ids: Sequence[i
                       model.fingerprint)
 
 
+def _dense_batched(model: Model, seqs: list[list[int]]):
+    """Independent causal forwards of many sequences in ONE layer-wise pass
+    (every GEMM sees all rows). bf16: one key bank holding every sequence at a
+    128-row-aligned base, so each row attends [base, base + pos] over the same
+    key tiles a lone prefill would (bitwise-equal results); fp32: the banked
+    engine with one empty-bank sequence each. Returns per-sequence (K, V)."""
+    c = model.config
+    dev = model.device
+    lens = np.array([len(x) for x in seqs], dtype=np.int64)
+    R = int(lens.sum())
+    ids_h = np.concatenate([np.asarray(x, dtype=np.int64) for x in seqs])
+    if ids_h.min() < 0 or ids_h.max() >= c.vocab_size:
+        raise ValueError(f"token id outside vocab of size {c.vocab_size}")
+    pos_h = np.concatenate([np.arange(n, dtype=np.int64) for n in lens])
+    row0 = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    if c.dtype == "bf16":
+        padded = -(-lens // 128) * 128
+        base = np.concatenate([[0], np.cumsum(padded)[:-1]]).astype(np.int64)
+        n_bank = int(padded.sum())
+        kstart_h = np.repeat(base, lens)
+        dst_h = kstart_h + pos_h
+        buf = host_to_device(np.concatenate([ids_h, pos_h, kstart_h, dst_h]), dev)
+        ids, pos, kstart, dst = buf[:R], buf[R:2 * R], buf[2 * R:3 * R], buf[3 * R:]
+        K = torch.empty(c.n_layers, n_bank, c.kv_heads, c.d_head, dtype=torch.bfloat16, device=dev)
+        V = torch.zeros_like(K)  # padding rows are read (masked, P = 0) by attention: must be finite
+        bank = torch.zeros(n_bank, c.kv_heads, c.d_head, dtype=torch.bfloat16, device=dev)
+        plan = KvPlan(k_scatter=bank, v_scatter=V, attn_k=bank, attn_v=V, dst_rows=dst, k_raw=K, raw_rows=dst,
+                      key_start=kstart)
+        pairs = int(sum(visible_pairs(int(n)) for n in lens))
+        forward_rows(model, ids, pos, plan, n_bank, want_logits=False, pairs=pairs)
+        return [(K[:, b:b + n], V[:, b:b + n]) for b, n in zip(base.tolist(), lens.tolist())]
+    buf = host_to_device(np.concatenate([ids_h, pos_h]), dev)
+    ids, pos = buf[:R], buf[R:]
+    K = torch.empty(c.n_layers, R, c.kv_heads, c.d_head, dtype=torch.float32, device=dev)
+    V = torch.empty_like(K)
+    tables = bank_tables(c.n_layers, [(None, None, 0, int(r0), int(n)) for r0, n in zip(row0, lens)], dev)
+    forward_banked(model, ids, pos, tables, len(seqs), int(lens.max()), 0, v_dst=V, k_raw_dst=K)
+    return [(K[:, b:b + n], V[:, b:b + n]) for b, n in zip(row0.tolist(), lens.tolist())]
+
+
+def prefill_chunks(model: Model, prefix_ids: Sequence[int], chunks: Sequence[Sequence[int]], *,
+                   trace: PipelineTrace | None = None, max_rows: int = 65536) -> list[ChunkCache]:
+    """Batched ``prefill_chunk``: every chunk behind the shared prefix at local
+    positions, position-free keys, in as few layer-wise passes as fit
+    ``max_rows`` rows (model.py:538-565 applied to each chunk; the results are
+    the per-chunk ones). One pass feeds the GEMMs tens of thousands of rows
+    instead of a few hundred per chunk."""
+    prefix_ids = list(prefix_ids)
+    chunks = [list(x) for x in chunks]
+    if not chunks:
+        return []
+    if any(not x for x in chunks):
+        raise ValueError("chunk must contain at least one token")
+    out: list[ChunkCache] = []
+    i = 0
+    while i < len(chunks):
+        batch, rows = [], 0
+        while i < len(chunks) and (not batch or rows + len(prefix_ids) + len(chunks[i]) <= max_rows):
+            batch.append(prefix_ids + chunks[i])
+            rows += len(batch[-1])
+            i += 1
+        for seq, (k, v) in zip(batch, _dense_batched(model, batch)):
+            out.append(ChunkCache(k, v, seq, len(prefix_ids), model.config.tokenizer_id, model.fingerprint))
+            n = len(seq)
+            trace_layer(trace, model.config, "chunk_precompute", n, visible_pairs(n), times=model.config.n_layers)
+            if trace is not None:
+                trace.matmul("chunk_precompute", 1, model.config.d_model, model.config.vocab_size)
+    return out
+
+
 def _check_cache(model: Model, cache) -> None:
     if getattr(cache, "model_fingerprint", model.fingerprint) != model.fingerprint:
         raise ValueError("cache was built by a different model")

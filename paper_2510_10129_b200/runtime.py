@@ -115,6 +115,7 @@ class KvPlan:
     k_raw: torch.Tensor | None = None
     raw_rows: torch.Tensor | None = None
     layer_ready: list | None = None   # torch.cuda.Event per layer (streamed merge) or None
+    key_start: torch.Tensor | None = None  # int64 [rows]: first visible bank row (batched sequences)
 
     def to_c(self) -> _lib.KvPlan:
         ready = None
@@ -124,7 +125,7 @@ class KvPlan:
         return _lib.KvPlan(_p(self.k_scatter), _layer_stride(self.k_scatter), _p(self.v_scatter),
                            _layer_stride(self.v_scatter), _p(self.dst_rows), _p(self.k_raw),
                            _layer_stride(self.k_raw), _p(self.raw_rows), _p(self.attn_k), _layer_stride(self.attn_k),
-                           _p(self.attn_v), _layer_stride(self.attn_v), ready)
+                           _p(self.attn_v), _layer_stride(self.attn_v), ready, _p(self.key_start))
 
 
 @dataclass

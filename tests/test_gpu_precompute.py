@@ -1,0 +1,75 @@
+"""Batched chunk precompute (prefill_chunks) against the per-chunk path
+(prefill_chunk, model.py:538-565, itself pinned to the oracle in
+test_gpu_parity.py): the same caches, bit for bit, for ragged chunk lengths
+(tile-aligned, one row over, single token), several passes (max_rows), the
+bf16 primary engine (head_dim 64 and 128, GQA) and the fp32 scoring engine."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+LENS = (40, 57, 33, 128, 129, 1, 255)
+
+
+def _model(dtype, d_head, n_heads, kv, d_model, layers=2, vocab=512):
+    import paper_2510_10129_b200 as cc
+    cfg = cc.ModelConfig(n_layers=layers, n_heads=n_heads, n_kv_heads=kv, d_model=d_model, d_head=d_head,
+                         d_ff=4 * d_model, vocab_size=vocab, rope_base=1e4, norm_eps=1e-5, activation="silu",
+                         mlp_gated=True, attn_bias=True, tokenizer_id="tiny", dtype=dtype)
+    return cc.init_model(cfg, 3, device=torch.device("cuda", 0), source="torch")
+
+
+def _check(model, max_rows):
+    import paper_2510_10129_b200 as cc
+    rng = np.random.default_rng(11)
+    prefix = rng.integers(0, 512, 16).tolist()
+    chunks = [rng.integers(0, 512, n).tolist() for n in LENS]
+    one = [cc.prefill_chunk(model, prefix, c) for c in chunks]
+    many = cc.prefill_chunks(model, prefix, chunks, max_rows=max_rows)
+    torch.cuda.synchronize()
+    assert len(many) == len(one)
+    for a, b in zip(one, many):
+        assert a.token_ids == b.token_ids and a.prefix_len == b.prefix_len
+        assert a.model_fingerprint == b.model_fingerprint
+        assert a.k.shape == b.k.shape and b.k.is_contiguous()
+        assert torch.equal(a.k, b.k), (a.k.float() - b.k.float()).abs().max().item()
+        assert torch.equal(a.v, b.v), (a.v.float() - b.v.float()).abs().max().item()
+
+
+@pytest.mark.parametrize("d_head,n_heads,kv,d_model", [(64, 4, 2, 256), (128, 8, 2, 512)])
+@pytest.mark.parametrize("max_rows", [1 << 16, 300])
+def test_prefill_chunks_bf16_equals_per_chunk(d_head, n_heads, kv, d_model, max_rows):
+    _check(_model("bf16", d_head, n_heads, kv, d_model), max_rows)
+
+
+@pytest.mark.parametrize("max_rows", [1 << 16, 300])
+def test_prefill_chunks_fp32_equals_per_chunk(max_rows):
+    _check(_model("fp32", 64, 2, 2, 128), max_rows)
+
+
+def test_prefill_chunks_feeds_cacheclip_prefill():
+    """The batched caches drop into the hot path: same selection and logits."""
+    import paper_2510_10129_b200 as cc
+    primary = _model("bf16", 64, 4, 2, 256)
+    aux = _model("fp32", 64, 2, 2, 128)
+    rng = np.random.default_rng(4)
+    prefix = rng.integers(0, 512, 16).tolist()
+    chunks = [rng.integers(0, 512, 96).tolist() for _ in range(6)]
+    query = rng.integers(0, 512, 12).tolist()
+    cfg = cc.SelectionConfig(0.25, 8, 1)
+    ref = cc.cacheclip_prefill(primary, aux, [cc.prefill_chunk(primary, prefix, c) for c in chunks],
+                               [cc.prefill_chunk(aux, prefix, c) for c in chunks], query, cfg)
+    out = cc.cacheclip_prefill(primary, aux, cc.prefill_chunks(primary, prefix, chunks),
+                               cc.prefill_chunks(aux, prefix, chunks), query, cfg)
+    assert out.plan.indices == ref.plan.indices
+    assert np.array_equal(out.logits, ref.logits)
+
+
+def test_prefill_chunks_rejects_empty_chunk():
+    import paper_2510_10129_b200 as cc
+    model = _model("bf16", 64, 4, 2, 256)
+    with pytest.raises(ValueError):
+        cc.prefill_chunks(model, [1, 2], [[3, 4], []])
+    assert cc.prefill_chunks(model, [1, 2], []) == []
