@@ -230,6 +230,10 @@ int cc_banked_attention_simt(const cc_bank_seq* seqs_dev, int32_t n_seqs, int32_
  *     mean (selector.py:163-165), selection_budget/top_candidates
  *     (selector.py:113-129) and the per-chunk window rule (selector.py:182-214).
  * ---------------------------------------------------------------------- */
+/* CacheBlend discrepancy (selector.py:280-282): out[r] = || a[r] - b[r] ||_2
+ * over `width` columns; a and b each CC_BF16 or CC_F32 (row pitches lda, ldb). */
+int cc_row_l2_diff(const void* a, int32_t a_dtype, int64_t lda, const void* b, int32_t b_dtype, int64_t ldb,
+                   int64_t n, int32_t width, float* out, void* stream);
 /* weights [n_seqs][H][Q][w_ld] -> scores[col_offset[s] + j], j < chunk_len[s]:
  * in-order sum over heads / H, then in-order sum over queries / Q. */
 int cc_reduce_scores(const float* weights, int32_t n_seqs, int32_t n_heads, int32_t n_query,

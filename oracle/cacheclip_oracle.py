@@ -596,6 +596,41 @@ def cacheclip(primary: OracleModel, aux: OracleModel, chunks: Sequence[Chunk],
     return Outcome(merged, logits, plan, wins, s)
 
 
+def cacheblend_select(m: OracleModel, merged: Merged, ratio: float):
+    """CacheBlend-style discrepancy selection (selector.py:248-291): layer 0
+    recomputed for every merged row with global context, then the L2 drift
+    of layer 1's value projection against the cached values, top
+    ceil(ratio*N) with no windows. GQA: the L2 runs over the KV heads (the
+    reference's MHA-expanded values give sqrt(G) x this, same order).
+    Returns (indices, discrepancy)."""
+    if m.cfg.n_layers < 2:
+        raise ValueError("discrepancy selection needs at least two layers")
+    if not 0.0 <= ratio <= 1.0:
+        raise ValueError(f"ratio must be in [0, 1], got {ratio}")
+    sink, total = merged.sink_len, merged.total
+    n = total - sink
+    h = embed(m, merged.token_ids[:total])
+    h1 = block(m, 0, h, np.arange(total, dtype=np.int64), None)[0]
+    _, _, v1 = qkv_project(m, 1, h1)   # == value_projection (model.py:367-389)
+    diff = v1[sink:] - merged.values[1][sink:total]
+    disc = np.sqrt(np.sum(np.square(diff.reshape(n, -1)), axis=1))
+    chosen = top_k_stable(disc, budget(ratio, n))
+    return tuple(int(i) + sink for i in chosen), disc
+
+
+def cacheblend(m: OracleModel, chunks: Sequence[Chunk], query_ids, ratio: float) -> Outcome:
+    """cacheblend_prefill (pipeline.py:229-255): prefix-less chunk caches,
+    discrepancy selection, selective recompute, then the query."""
+    for i, c in enumerate(chunks):
+        if c.prefix_len != 0:
+            raise ValueError(f"chunk {i} carries a shared prefix; this baseline concatenates raw chunks")
+    merged = merge(chunks, m.cfg.d_head, m.cfg.rope_base)
+    plan, disc = cacheblend_select(m, merged, ratio)
+    selective(m, merged, plan)
+    logits = extend(m, merged, query_ids)
+    return Outcome(merged, logits, plan, (), disc)
+
+
 def full_prefill(m: OracleModel, ids) -> Prefill:
     """full_attention_prefill (pipeline.py:77-84)."""
     return prefill_full(m, ids)

@@ -18,10 +18,10 @@ from .kv_store import ChunkCache, MergedCache, MergeLayout, compute_positions, m
 from .model import (LayerCache, PrefillResult, decode_step, extend_cache, peek_forward, prefill_chunk, prefill_chunks,
                     prefill_full, selective_forward, visible_pairs)
 from .persist import CACHE_MAGIC, CACHE_VERSION, CACHE_VERSION_BF16, load_cache, save_cache
-from .pipeline import (STRATEGIES, ApeConfig, PrefillOutcome, ape_prefill, cacheclip_prefill,
+from .pipeline import (STRATEGIES, ApeConfig, PrefillOutcome, ape_prefill, cacheblend_prefill, cacheclip_prefill,
                        direct_reuse_prefill, full_attention_prefill, reuse_context_ids)
 from .selector import (AuxSelection, ImportanceScores, SelectionConfig, SelectionPlan, WindowRecord,
-                       aux_score_tokens, map_selection, random_select, select_tokens, selection_budget,
+                       aux_score_tokens, cacheblend_select, map_selection, random_select, select_tokens, selection_budget,
                        top_candidates)
 from .tokenizers import AlignmentMap, GreedyTokenizer, TokenSpan, align_spans, char_vocab
 from .weights import Model, from_params, init_model, reference_init_params

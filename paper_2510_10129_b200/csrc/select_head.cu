@@ -262,6 +262,29 @@ __global__ void argmax_finish_kernel(const unsigned long long* best, int64_t* ou
 
 using namespace cc;
 
+// CacheBlend discrepancy (selector.py:280-282): out[r] = ||a[r] - b[r]||_2,
+// a the recomputed layer-1 values, b the cached ones (each CC_BF16 or
+// CC_F32). One warp per row; each lane sums a fixed strided subset, then a
+// fixed xor-tree: deterministic.
+__device__ __forceinline__ float ld_any(const void* p, int dtype, int64_t i) {
+  return dtype == CC_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i])
+                          : reinterpret_cast<const float*>(p)[i];
+}
+__global__ void row_l2_diff_kernel(const void* __restrict__ a, int a_dtype, int64_t lda, const void* __restrict__ b,
+                                   int b_dtype, int64_t ldb, int64_t n, int width, float* __restrict__ out) {
+  const int64_t row = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (row >= n) return;
+  float acc = 0.f;
+  for (int j = lane; j < width; j += 32) {
+    const float d = __fsub_rn(ld_any(a, a_dtype, row * lda + j), ld_any(b, b_dtype, row * ldb + j));
+    acc = __fmaf_rn(d, d, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[row] = __fsqrt_rn(acc);
+}
+
 extern "C" {
 
 int cc_reduce_scores(const float* weights, int32_t n_seqs, int32_t n_heads, int32_t n_query, int64_t w_ld,
@@ -274,6 +297,18 @@ int cc_reduce_scores(const float* weights, int32_t n_seqs, int32_t n_heads, int3
   reduce_scores_kernel<<<grid, 256, 0, as_stream(stream)>>>(weights, n_heads, n_query, w_ld, chunk_lens_dev,
                                                              col_offset_dev, scores);
   CC_LAUNCH_CHECK("reduce_scores");
+  return CC_OK;
+}
+
+int cc_row_l2_diff(const void* a, int32_t a_dtype, int64_t lda, const void* b, int32_t b_dtype, int64_t ldb,
+                   int64_t n, int32_t width, float* out, void* stream) {
+  CC_CHECK_ARG(width > 0 && lda >= width && ldb >= width, CC_ERR_DIMENSION, "bad row width %d", width);
+  CC_CHECK_ARG((a_dtype == CC_BF16 || a_dtype == CC_F32) && (b_dtype == CC_BF16 || b_dtype == CC_F32),
+               CC_ERR_UNSUPPORTED, "dtypes %d / %d", a_dtype, b_dtype);
+  if (n <= 0) return CC_OK;
+  row_l2_diff_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(a, a_dtype, lda, b, b_dtype,
+                                                                                       ldb, n, width, out);
+  CC_LAUNCH_CHECK("row_l2_diff");
   return CC_OK;
 }
 

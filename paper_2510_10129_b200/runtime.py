@@ -136,13 +136,22 @@ class RowsResult:
 
 
 def forward_rows(model: Model, ids: torch.Tensor, positions: torch.Tensor, plan: KvPlan, n_keys: int, *,
-                 row_factor: torch.Tensor | None = None, want_logits: bool = True, pairs: int = 0) -> RowsResult:
+                 row_factor: torch.Tensor | None = None, want_logits: bool = True, pairs: int = 0,
+                 layers: int | None = None) -> RowsResult:
+    """``layers``: run only the first `layers` layers (no head); the residual
+    stream after them is returned (CacheBlend's layer-0 pass)."""
     c = model.config
     if c.dtype != "bf16":
         raise ValueError("forward_rows runs bf16 models; fp32 models use forward_banked")
     dev = ids.device
     R = ids.numel()
     md = model.desc()
+    if layers is not None:
+        if not 1 <= layers <= c.n_layers:
+            raise ValueError(f"layers={layers} outside 1..{c.n_layers}")
+        md = _lib.ModelDesc.from_buffer_copy(md)
+        md.n_layers = layers
+        want_logits = want_logits and layers == c.n_layers
     lib = _lib.load()
     ws = torch.empty(int(lib.cc_forward_rows_workspace_bytes(ctypes.byref(md), R)), dtype=torch.uint8, device=dev)
     logits = argmax = None

@@ -24,7 +24,7 @@ import torch
 from . import _lib
 from .flops import PipelineTrace, trace_layer
 from .kv_store import ChunkCache, host_to_device
-from .runtime import ScoreSpec, bank_tables, forward_banked
+from .runtime import KvPlan, ScoreSpec, bank_tables, forward_banked, forward_rows
 from .tokenizers import TokenSpan, align_spans
 from .weights import Model
 
@@ -276,6 +276,67 @@ def aux_score_tokens(aux_model: Model, aux_chunk_caches: Sequence[ChunkCache], q
         trace_layer(trace, c, "selection", Q * S, Q * rows_total + S * (Q * (Q + 1) // 2), times=c.n_layers)
         trace.matmul("selection", S, c.d_model, c.vocab_size)
     return ImportanceScores(scores, tuple(int(x) for x in chunk_lens))
+
+
+def cacheblend_select(primary_model: Model, merged, ratio: float, *, trace: PipelineTrace | None = None,
+                      return_scores: bool = False):
+    """selector.py:248-291 (see _cacheblend_device)."""
+    plan, _, disc = _cacheblend_device(primary_model, merged, ratio, trace)
+    if return_scores:
+        return plan, disc.cpu().numpy()
+    return plan
+
+
+def _cacheblend_device(primary_model: Model, merged, ratio: float, trace: PipelineTrace | None = None):
+    """CacheBlend-style discrepancy selection (selector.py:248-291) on the
+    device: layer 0 of every merged row recomputed with global context (one
+    dense causal pass, the cache untouched), layer 1's value projection of
+    those states (RMSNorm + the V rows of the fused QKV weight), the per-row
+    L2 drift against the cached layer-1 values (cc_row_l2_diff), then the
+    exact stable top-ceil(ratio*N) with no windows."""
+    c = primary_model.config
+    if c.n_layers < 2:
+        raise ValueError("discrepancy selection needs at least two layers")
+    if not 0.0 <= ratio <= 1.0:
+        raise ValueError(f"ratio must be in [0, 1], got {ratio}")
+    if c.dtype != "bf16":
+        raise ValueError("device CacheBlend runs the bf16 primary engine")
+    dev = primary_model.device
+    sink, total = merged.layout.sink_len, merged.layout.total
+    n = total - sink
+    if n <= 0:
+        return SelectionPlan((), (), float(ratio), 0.0), None, torch.zeros(0, device=dev)
+    ids = merged.token_ids_device()[:total]
+    pos = torch.arange(total, dtype=torch.int64, device=dev)
+    bank_k = torch.empty(total, c.kv_heads, c.d_head, dtype=torch.bfloat16, device=dev)
+    bank_v = torch.empty_like(bank_k)
+    res = forward_rows(primary_model, ids, pos, KvPlan(k_scatter=bank_k, v_scatter=bank_v, attn_k=bank_k,
+                                                       attn_v=bank_v), total, want_logits=False,
+                       pairs=total * (total + 1) // 2, layers=1)
+    lw = primary_model.layers[1]
+    s = torch.cuda.current_stream().cuda_stream
+    x = torch.empty(total, c.d_model, dtype=torch.bfloat16, device=dev)
+    _lib.call("cc_rmsnorm", res.h.data_ptr(), total, c.d_model, c.d_model, lw.attn_norm.data_ptr(), c.norm_eps,
+              x.data_ptr(), _lib.CC_BF16, s)
+    qw, kw = c.attn_width, c.kv_width
+    from .runtime import gemm
+    # values in the cache's own precision (bf16 rounding, as the QKV epilogue
+    # stores them), so a row whose context did not change drifts by exactly 0
+    cached = merged.v_store[1][sink:total]
+    v_global = torch.empty(total, kw, dtype=cached.dtype, device=dev)
+    vmode = _lib.CC_BF16 if cached.dtype == torch.bfloat16 else _lib.CC_F32
+    gemm(_lib.CC_GEMM_BF16, _lib.CC_EPI_STORE, total, kw, c.d_model, x, lw.w_qkv[qw + kw:qw + 2 * kw],
+         bias=None if lw.b_qkv is None else lw.b_qkv[qw + kw:qw + 2 * kw], C=v_global, ldc=kw, c_mode=vmode)
+    disc = torch.empty(n, dtype=torch.float32, device=dev)
+    _lib.call("cc_row_l2_diff", v_global[sink:].data_ptr(), vmode, kw, cached.data_ptr(), vmode, kw, n, kw,
+              disc.data_ptr(), s)
+    if trace is not None:
+        trace_layer(trace, c, "selection", total, total * (total + 1) // 2, times=1)
+        trace.matmul("selection", total, c.d_model, kw)
+    # one "chunk" and threshold 1: the window rule keeps exactly the candidates
+    dsel = select_tokens_device(ImportanceScores(disc, (n,)), SelectionConfig(ratio, 8, 1), index_offset=sink)
+    plan = SelectionPlan(tuple(dsel.idx_host.tolist()), (), float(ratio), dsel.count / n)
+    return plan, dsel, disc
 
 
 def random_select(n_tokens: int, ratio: float, seed: int, *, index_offset: int = 0) -> SelectionPlan:

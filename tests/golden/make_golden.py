@@ -119,6 +119,22 @@ def run(w: Workload, seed: int = 0) -> dict:
     )
 
 
+def run_cacheblend(w: Workload, seed: int = 0) -> dict:
+    """cacheblend_prefill (pipeline.py:229-255) on prefix-less chunk caches of
+    the workload's chunks (the baseline concatenates raw chunks)."""
+    p_params = orc.seeded_params(w.primary, w.primary_seed, w.bias_std)
+    primary = ref.Model(ref_config(w.primary, "chars"), orc.mha_expand(w.primary, p_params))
+    _, chunk_ids, query = w.token_ids(seed)
+    chunks = [ref.prefill_chunk(primary, [], c) for c in chunk_ids]
+    merged = ref.merge_caches(chunks, primary.config.rope)
+    plan, disc = ref.cacheblend_select(primary, merged, w.ratio, return_scores=True)
+    out = ref.cacheblend_prefill(primary, chunks, query, w.ratio)
+    return dict(cb_indices=np.asarray(out.plan.indices, dtype=np.int64),
+                cb_select_indices=np.asarray(plan.indices, dtype=np.int64),
+                cb_discrepancy=np.asarray(disc, dtype=np.float32), cb_logits=out.logits,
+                digest_cb_logits=np.array(digest([out.logits])))
+
+
 def write_reference_files() -> None:
     """Small .cclp files written by the reference's own save_cache (format v1)."""
     rng = np.random.default_rng(42)
@@ -151,6 +167,8 @@ def main() -> None:
     write_reference_files()
     for w in (C1, C1_EXACT, B1):
         out = run(w)
+        if w is not C1_EXACT:
+            out.update(run_cacheblend(w))
         path = os.path.join(HERE, f"{w.name}.npz")
         np.savez_compressed(path, **out)
         print(f"{w.name}: {len(out['indices'])} selected of {out['scores'].size}, "

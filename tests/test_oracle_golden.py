@@ -147,3 +147,31 @@ def test_full_selection_equals_full_prefill():
                                    orc.rope_rotate(full.keys[layer], pos, 64, w.primary.rope_base),
                                    rtol=0, atol=1e-4)
         np.testing.assert_allclose(merged.values[layer], full.values[layer], rtol=0, atol=1e-4)
+
+
+@pytest.mark.parametrize("w", [C1, B1], ids=lambda w: w.name)
+def test_cacheblend_matches_reference(w):
+    """cacheblend_select / cacheblend_prefill (selector.py:248-291,
+    pipeline.py:229-255) against the reference's own run (make_golden.py)."""
+    g = dict(np.load(os.path.join(GOLDEN, f"{w.name}.npz")))
+    prim = orc.OracleModel(w.primary, orc.seeded_params(w.primary, w.primary_seed, w.bias_std))
+    _, chunk_ids, query = w.token_ids(0)
+    chunks = [orc.prefill_chunk(prim, [], c) for c in chunk_ids]
+    out = orc.cacheblend(prim, chunks, query, w.ratio)
+    assert out.indices == tuple(int(i) for i in g["cb_indices"])
+    assert out.indices == tuple(int(i) for i in g["cb_select_indices"])
+    # the reference L2 runs over MHA-expanded values: sqrt(G) x the GQA norm
+    np.testing.assert_allclose(out.scores * np.sqrt(w.primary.group), g["cb_discrepancy"], rtol=1e-5, atol=1e-6)
+    if w.primary.group == 1:
+        assert _digest([out.logits]) == str(g["digest_cb_logits"])
+    np.testing.assert_allclose(out.logits, g["cb_logits"], rtol=0, atol=2e-5)
+
+
+def test_cacheblend_rejects_prefixed_chunks_and_shallow_models():
+    w = B1
+    prim = orc.OracleModel(w.primary, orc.seeded_params(w.primary, 0, w.bias_std))
+    chunks = [orc.prefill_chunk(prim, [1, 2], [3, 4, 5])]
+    with pytest.raises(ValueError):
+        orc.cacheblend(prim, chunks, [7], 0.5)
+    with pytest.raises(ValueError):
+        orc.cacheblend_select(prim, orc.merge(chunks, 64, w.primary.rope_base), 1.5)
