@@ -29,6 +29,7 @@ class Workload:
     primary_seed: int = 0
     aux_seed: int = 1
     bias_std: float = 0.0
+    chunk_lens: tuple = ()   # ragged chunks (overrides n_chunks x chunk_len)
 
     def token_ids(self, seed: int = 0):
         """(prefix, [chunk ids], query) drawn from one generator; aux shares
@@ -36,7 +37,8 @@ class Workload:
         v = min(self.primary.vocab_size, self.aux.vocab_size)
         rng = np.random.default_rng(seed)
         prefix = rng.integers(0, v, self.prefix_len).tolist()
-        chunks = [rng.integers(0, v, self.chunk_len).tolist() for _ in range(self.n_chunks)]
+        lens = self.chunk_lens or (self.chunk_len,) * self.n_chunks
+        chunks = [rng.integers(0, v, n).tolist() for n in lens]
         query = rng.integers(0, v, self.query_len).tolist()
         return prefix, chunks, query
 
@@ -67,6 +69,12 @@ B1_AUX = OracleConfig(n_layers=2, n_heads=2, n_kv_heads=1, d_model=128, d_head=6
 B1 = Workload("b1", B1_PRIMARY, B1_AUX, prefix_len=8, n_chunks=3, chunk_len=64, query_len=16,
               ratio=0.4, window_threshold=3, bias_std=0.05)
 
+# Ragged chunks (1-token, sub-window, tile-straddling lengths), GQA primary,
+# MHA aux with QKV bias, window threshold 3, ratio 0.3: pins partial windows
+# and per-chunk window restarts against the reference.
+R1 = Workload("r1", C1_PRIMARY, B1_AUX, prefix_len=5, n_chunks=6, chunk_len=0, query_len=9, ratio=0.3,
+              window_threshold=3, bias_std=0.05, chunk_lens=(37, 1, 130, 8, 64, 7))
+
 # Qwen2.5-7B / 0.5B shapes (BASELINE configs[1..2]); GPU-only sizes.
 QWEN7B = OracleConfig(n_layers=28, n_heads=28, n_kv_heads=4, d_model=3584, d_head=128,
                       d_ff=18944, vocab_size=152064, rope_base=1e6, norm_eps=1e-6,
@@ -82,4 +90,4 @@ C3 = Workload("c3", QWEN7B, QWEN05B, prefix_len=32, n_chunks=64, chunk_len=512, 
 C4 = Workload("c4", QWEN14B, QWEN05B, prefix_len=32, n_chunks=400, chunk_len=500, query_len=32)
 C5 = Workload("c5", QWEN7B, QWEN05B, prefix_len=32, n_chunks=32, chunk_len=512, query_len=32)
 
-WORKLOADS = {w.name: w for w in (C1, C1_EXACT, B1, C2, C3, C4, C5)}
+WORKLOADS = {w.name: w for w in (C1, C1_EXACT, B1, R1, C2, C3, C4, C5)}

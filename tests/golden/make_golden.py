@@ -30,7 +30,7 @@ sys.path.insert(0, REF_SRC)
 import cacheclip as ref  # noqa: E402  (the reference, read-only)
 
 from oracle import cacheclip_oracle as orc  # noqa: E402
-from oracle.synth import B1, C1, C1_EXACT, Workload  # noqa: E402
+from oracle.synth import B1, C1, C1_EXACT, R1, Workload  # noqa: E402
 
 ROW_STRIDE = 16  # sampled rows kept in the fixture (keeps files small)
 
@@ -165,7 +165,7 @@ def write_reference_files() -> None:
 
 def main() -> None:
     write_reference_files()
-    for w in (C1, C1_EXACT, B1):
+    for w in (C1, C1_EXACT, B1, R1):
         out = run(w)
         if w is not C1_EXACT:
             out.update(run_cacheblend(w))

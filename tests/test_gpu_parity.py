@@ -19,7 +19,7 @@ import pytest
 import torch
 
 from oracle import cacheclip_oracle as orc
-from oracle.synth import B1, C1, C1_EXACT
+from oracle.synth import B1, C1, C1_EXACT, R1
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
@@ -58,7 +58,7 @@ class Case:
         self.config = cc.SelectionConfig(w.ratio, w.window_len, w.window_threshold)
 
 
-@pytest.fixture(scope="module", params=[C1, C1_EXACT, B1], ids=lambda w: w.name)
+@pytest.fixture(scope="module", params=[C1, C1_EXACT, B1, R1], ids=lambda w: w.name)
 def case(request):
     return Case(request.param)
 
@@ -171,3 +171,31 @@ def test_full_prefill_and_ratio_identities(case):
     assert clip.plan.indices == tuple(int(i) for i in case.g["indices"])
     assert np.abs(clip.logits - case.g["clip_logits"]).max() < BF16_LOGIT_TOL * std
     assert clip.first_token == int(np.argmax(clip.logits))
+
+
+_SEED_CASES: dict = {}
+
+
+@pytest.mark.parametrize("wname", ["r1", "c1_exact"])
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+def test_selection_exact_across_seeds(wname, seed):
+    """SURVEY §8(d) seeds: for fresh inputs the device chain (chunk precompute
+    -> batched scoring -> top-k + windows) selects exactly the oracle chain's
+    tokens (the oracle being pinned to the reference above)."""
+    import paper_2510_10129_b200 as cc
+    from oracle.synth import WORKLOADS
+    w = WORKLOADS[wname]
+    if wname not in _SEED_CASES:
+        _SEED_CASES[wname] = Case(w)
+    case = _SEED_CASES[wname]
+    prefix, chunk_ids, query = w.token_ids(seed)
+    aux_chunks = cc.prefill_chunks(case.aux, prefix, chunk_ids)
+    scores = cc.aux_score_tokens(case.aux, aux_chunks, query)
+    o_aux = [orc.prefill_chunk(case.o_aux, prefix, c) for c in chunk_ids]
+    o_scores = orc.aux_scores(case.o_aux, o_aux, query)
+    np.testing.assert_allclose(scores.scores, o_scores, rtol=1e-5, atol=1e-9)
+    o_idx, o_win = orc.select(o_scores, [len(c) for c in chunk_ids], w.ratio, w.window_len, w.window_threshold)
+    sel = cc.select_tokens(scores, case.config)
+    assert sel.indices == o_idx
+    assert [(x.start, x.end, x.selected, x.kept, x.partial) for x in sel.windows] == \
+        [(x.start, x.end, x.selected, x.kept, x.partial) for x in o_win]

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from oracle import cacheclip_oracle as orc
-from oracle.synth import B1, C1, C1_EXACT
+from oracle.synth import B1, C1, C1_EXACT, R1
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -35,7 +35,7 @@ def _run(w, seed=0):
     return dict(prim=prim, chunks=chunks, direct=direct, direct_kv=direct_kv, out=out, full=full)
 
 
-@pytest.fixture(scope="module", params=[C1, C1_EXACT, B1], ids=lambda w: w.name)
+@pytest.fixture(scope="module", params=[C1, C1_EXACT, B1, R1], ids=lambda w: w.name)
 def case(request):
     w = request.param
     g = dict(np.load(os.path.join(GOLDEN, f"{w.name}.npz")))
@@ -149,7 +149,7 @@ def test_full_selection_equals_full_prefill():
         np.testing.assert_allclose(merged.values[layer], full.values[layer], rtol=0, atol=1e-4)
 
 
-@pytest.mark.parametrize("w", [C1, B1], ids=lambda w: w.name)
+@pytest.mark.parametrize("w", [C1, B1, R1], ids=lambda w: w.name)
 def test_cacheblend_matches_reference(w):
     """cacheblend_select / cacheblend_prefill (selector.py:248-291,
     pipeline.py:229-255) against the reference's own run (make_golden.py)."""
