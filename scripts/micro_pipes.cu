@@ -47,6 +47,14 @@ __global__ void pipe_kernel(float* out, long long* cyc, float seed) {
         __nv_bfloat162 b = __floats2bfloat162_rn(w[c].x, w[c].y);
         acc += *reinterpret_cast<uint32_t*>(&b);
         w[c] = __ffma2_rn(w[c], make_float2(0.999f, 0.999f), make_float2(1e-4f, 1e-4f));
+      } else if (OP == 9) {  // EX2 on packed bf16x2 (two exps per instruction)
+        uint32_t u = __float_as_uint(w[c].x);
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(u));
+        w[c].x = __uint_as_float(u);
+      } else if (OP == 10) {  // EX2 on packed f16x2
+        uint32_t u = __float_as_uint(w[c].y);
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(u));
+        w[c].y = __uint_as_float(u);
       } else if (OP == 8) {  // FMNMX3
         v[c] = fmaxf(v[c], fmaxf(w[c].x, w[c].y));
         w[c].x = -w[c].x;
@@ -90,6 +98,8 @@ int main() {
     run<6>("EX2+FFMA2", w);
     run<7>("F2FP+FFMA2", w);
     run<8>("FMNMX3", w);
+    run<9>("EX2.BF16X2", w);
+    run<10>("EX2.F16X2", w);
   }
   return 0;
 }
