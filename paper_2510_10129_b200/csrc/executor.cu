@@ -192,7 +192,7 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
 int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t R,
                       const cc_bank_seq* tables, int32_t n_seqs, int32_t max_new, int64_t max_bank, void* v_dst,
                       int64_t v_dst_stride, void* k_raw_dst, int64_t k_raw_stride, const cc_score_spec* score,
-                      void* workspace, void* stream) {
+                      void* const* layer_ready, void* workspace, void* stream) {
   CC_CHECK_ARG(md && tables && workspace, CC_ERR_VALUE, "null model / tables / workspace");
   CC_CHECK_ARG(md->dtype == CC_F32, CC_ERR_UNSUPPORTED, "cc_forward_banked runs fp32 (3xTF32) models");
   if (R <= 0) return CC_OK;
@@ -213,6 +213,10 @@ int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t
   const int L = md->n_layers;
   for (int l = 0; l < L; ++l) {
     const cc_layer_weights& lw = md->layers[l];
+    if (layer_ready && layer_ready[l]) {  // this layer's banks still streaming in on another stream
+      const cudaError_t e = cudaStreamWaitEvent(as_stream(stream), (cudaEvent_t)layer_ready[l], 0);
+      if (e != cudaSuccess) return fail(CC_ERR_CUDA, "cudaStreamWaitEvent: %s", cudaGetErrorString(e));
+    }
     if (l == 0)
       CC_TRY(cc_embed_rmsnorm(ids, R, md->embed, CC_F32, md->vocab, (int)d, h, lw.attn_norm, md->norm_eps, x,
                               CC_F32_SPLIT3, stream));

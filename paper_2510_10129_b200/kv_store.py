@@ -272,6 +272,51 @@ def compute_positions(chunk_lens: Sequence[int], prefix_len: int) -> np.ndarray:
     return np.arange(prefix_len + sum(chunk_lens), dtype=np.int64)
 
 
+def _stream_segments(spec, layers: int, dev) -> torch.Tensor:
+    """Per-layer copies of the segment table with layer-l host pointers."""
+    base = _segments(spec).view(np.int64).reshape(len(spec), 7)
+    per_layer = np.repeat(base[None], layers, axis=0)
+    for si, (c, *_rest) in enumerate(spec):
+        per_layer[:, si, 0] += np.arange(layers, dtype=np.int64) * c.k.stride(0) * c.k.element_size()
+        per_layer[:, si, 1] += np.arange(layers, dtype=np.int64) * c.v.stride(0) * c.v.element_size()
+    return host_to_device(per_layer.reshape(-1).view(np.uint8), dev)
+
+
+def stream_local_banks(chunks: Sequence[ChunkCache], rope: RopeParams, device):
+    """Host-resident (pinned) chunk caches -> one device bank per layer
+    holding every chunk's keys rotated at its LOCAL positions and its values
+    (what ChunkCache.local_rotated_keys + .v give per chunk), read straight
+    over PCIe by the assembly kernel one layer per launch on the current
+    stream; each layer records an event so the scoring pass can start on
+    layer l while later layers are still in flight. Returns (K [L,R,H,D],
+    V, row offsets per chunk, events)."""
+    first = chunks[0]
+    for i, c in enumerate(chunks):
+        if not (c.k.is_pinned() and c.v.is_pinned()):
+            raise CacheConsistencyError(f"chunk {i}: host caches must be in pinned memory")
+        if c.n_layers != first.n_layers or c.k.shape[2:] != first.k.shape[2:] or c.k.dtype != first.k.dtype:
+            raise CacheConsistencyError(f"chunk {i} has mismatched tensor geometry")
+    L, H, D = first.n_layers, first.k.shape[2], first.k.shape[3]
+    offs = np.concatenate([[0], np.cumsum([c.n_rows for c in chunks])]).astype(np.int64)
+    total = int(offs[-1])
+    dev = torch.device(device)
+    K = torch.empty(L, total, H, D, dtype=first.k.dtype, device=dev)
+    V = torch.empty_like(K)
+    spec = [(c, 0, int(o), c.n_rows, 0) for c, o in zip(chunks, offs[:-1])]  # pos0 = 0: local positions
+    segs = _stream_segments(spec, L, dev)
+    seg_bytes = len(spec) * 7 * 8
+    inv = rope.inv_freq
+    ready = []
+    for layer in range(L):
+        _lib.call("cc_assemble_kv_capped", segs.data_ptr() + layer * seg_bytes, len(spec), total, 1, H, D,
+                  _dtype_code(first.k.dtype), inv.ctypes.data, 0, K[layer].data_ptr(), V[layer].data_ptr(), total,
+                  STREAM_CTAS, _stream())
+        ev = torch.cuda.Event()
+        ev.record()
+        ready.append(ev)
+    return K, V, offs[:-1], ready
+
+
 def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: PipelineTrace | None = None,
                  *, capacity: int | None = None, device=None) -> MergedCache:
     """Concatenate chunk caches keeping only the first copy of the prefix and
@@ -332,12 +377,7 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
         for i, c in enumerate(chunks):
             if not (c.k.is_pinned() and c.v.is_pinned()):
                 raise CacheConsistencyError(f"chunk {i}: host caches must be in pinned memory")
-        base = _segments(spec).view(np.int64).reshape(len(spec), 7)
-        per_layer = np.repeat(base[None], L, axis=0)
-        for si, (c, *_rest) in enumerate(spec):
-            per_layer[:, si, 0] += np.arange(L, dtype=np.int64) * c.k.stride(0) * c.k.element_size()
-            per_layer[:, si, 1] += np.arange(L, dtype=np.int64) * c.v.stride(0) * c.v.element_size()
-        segs = host_to_device(per_layer.reshape(-1).view(np.uint8), dev)
+        segs = _stream_segments(spec, L, dev)
         seg_bytes = len(spec) * 7 * 8
         inv = rope.inv_freq
         layer_ready = []

@@ -196,7 +196,8 @@ class ScoreSpec:
 
 def forward_banked(model: Model, ids: torch.Tensor, positions: torch.Tensor, tables: torch.Tensor,
                    n_seqs: int, max_new: int, max_bank: int, *, v_dst: torch.Tensor | None = None,
-                   k_raw_dst: torch.Tensor | None = None, score: ScoreSpec | None = None) -> torch.Tensor:
+                   k_raw_dst: torch.Tensor | None = None, score: ScoreSpec | None = None,
+                   layer_ready: list | None = None) -> torch.Tensor:
     """fp32 engine. tables: device cc_bank_seq[n_layers][n_seqs]. v_dst /
     k_raw_dst: optional [L, rows, Hkv, D] destinations of the new rows' values
     and position-free keys (dense precompute). Returns the residual stream."""
@@ -215,9 +216,13 @@ def forward_banked(model: Model, ids: torch.Tensor, positions: torch.Tensor, tab
         w = torch.empty(n_seqs, c.n_heads, max_new, score.max_chunk, dtype=torch.float32, device=dev)
         spec_c = _lib.ScoreSpec(score.col0, score.chunk_lens.data_ptr(), score.col_off.data_ptr(), score.max_chunk,
                                 w.data_ptr(), score.scores.data_ptr())
+    ready = None
+    if layer_ready:
+        ready = (ctypes.c_void_p * len(layer_ready))(*[e.cuda_event for e in layer_ready])
     _lib.check(lib.cc_forward_banked(ctypes.byref(md), ids.data_ptr(), positions.data_ptr(), R, tables.data_ptr(),
                                      n_seqs, max_new, max_bank, _p(v_dst), _layer_stride(v_dst), _p(k_raw_dst),
                                      _layer_stride(k_raw_dst), ctypes.byref(spec_c) if spec_c is not None else None,
+                                     ctypes.cast(ready, ctypes.POINTER(ctypes.c_void_p)) if ready else None,
                                      ws.data_ptr(), _s()))
     return ws[: R * c.d_model * 4].view(torch.float32).view(R, c.d_model)
 

@@ -231,7 +231,7 @@ def _same_spans(a, b) -> bool:
 
 # ---------------------------------------------------------------------------
 def aux_score_tokens(aux_model: Model, aux_chunk_caches: Sequence[ChunkCache], query_ids: Sequence[int], *,
-                     trace: PipelineTrace | None = None, workers: int = 1) -> ImportanceScores:
+                     trace: PipelineTrace | None = None, workers: int = 1, _banks=None) -> ImportanceScores:
     """Score chunk tokens by last-layer query attention (selector.py:132-179).
 
     All chunks run as one batch of sequences; ``workers`` is accepted for
@@ -265,11 +265,18 @@ def aux_score_tokens(aux_model: Model, aux_chunk_caches: Sequence[ChunkCache], q
     R = S * Q
     ids_d, pos_d = buf[:R], buf[R:2 * R]
     lens_d, off_d = buf[2 * R:2 * R + S], buf[2 * R + S:]
-    seqs = [(ch.local_rotated_keys(c.rope), ch.v, ch.n_rows, si * Q, Q) for si, ch in enumerate(aux_chunk_caches)]
+    ready = None
+    if _banks is not None:  # host caches streamed in per layer (kv_store.stream_local_banks)
+        kb, vb, offs, ready = _banks
+        seqs = [(kb[:, o:o + ch.n_rows], vb[:, o:o + ch.n_rows], ch.n_rows, si * Q, Q)
+                for si, (ch, o) in enumerate(zip(aux_chunk_caches, offs.tolist()))]
+    else:
+        seqs = [(ch.local_rotated_keys(c.rope), ch.v, ch.n_rows, si * Q, Q)
+                for si, ch in enumerate(aux_chunk_caches)]
     tables = bank_tables(c.n_layers, seqs, dev)
     scores = torch.empty(int(chunk_lens.sum()), dtype=torch.float32, device=dev)
     spec = ScoreSpec(prefix, lens_d, off_d, int(chunk_lens.max()), scores)
-    forward_banked(aux_model, ids_d, pos_d, tables, S, Q, int(n_rows.max()), score=spec)
+    forward_banked(aux_model, ids_d, pos_d, tables, S, Q, int(n_rows.max()), score=spec, layer_ready=ready)
     if trace is not None:  # the reference's per-chunk peek events, folded (linear counts)
         rows_total = int(n_rows.sum())
         trace.rope("selection", c.n_layers * rows_total * c.kv_heads, c.d_head)

@@ -73,3 +73,36 @@ def test_prefill_chunks_rejects_empty_chunk():
     with pytest.raises(ValueError):
         cc.prefill_chunks(model, [1, 2], [[3, 4], []])
     assert cc.prefill_chunks(model, [1, 2], []) == []
+
+
+def test_host_pinned_caches_equal_device_caches():
+    """e2e path: pinned host chunk caches (scoring caches streamed in per
+    layer and rotated on the way, primary caches streamed into the merge)
+    give bit-identical scores, selection and logits to device caches."""
+    import paper_2510_10129_b200 as cc
+    primary = _model("bf16", 64, 4, 2, 256)
+    aux = _model("fp32", 64, 2, 2, 128)
+    rng = np.random.default_rng(8)
+    prefix = rng.integers(0, 512, 16).tolist()
+    chunks_ids = [rng.integers(0, 512, n).tolist() for n in (96, 40, 130, 7)]
+    query = rng.integers(0, 512, 12).tolist()
+    cfg = cc.SelectionConfig(0.3, 8, 2)
+    pc = cc.prefill_chunks(primary, prefix, chunks_ids)
+    ac = cc.prefill_chunks(aux, prefix, chunks_ids)
+
+    def host(c, m):
+        return cc.ChunkCache(c.k.cpu().pin_memory(), c.v.cpu().pin_memory(), c.token_ids, c.prefix_len,
+                             m.config.tokenizer_id, m.fingerprint)
+
+    dev_out = cc.cacheclip_prefill(primary, aux, pc, ac, query, cfg)
+    host_out = cc.cacheclip_prefill(primary, aux, [host(c, primary) for c in pc], [host(c, aux) for c in ac],
+                                    query, cfg)
+    torch.cuda.synchronize()
+    assert host_out.plan.indices == dev_out.plan.indices
+    assert host_out.plan.windows == dev_out.plan.windows
+    assert np.array_equal(host_out.logits, dev_out.logits)
+    s_dev = cc.aux_score_tokens(aux, ac, query).scores
+    from paper_2510_10129_b200.kv_store import stream_local_banks
+    banks = stream_local_banks([host(c, aux) for c in ac], aux.config.rope, aux.device)
+    s_host = cc.aux_score_tokens(aux, [host(c, aux) for c in ac], query, _banks=banks).scores
+    assert np.array_equal(s_dev, s_host)
