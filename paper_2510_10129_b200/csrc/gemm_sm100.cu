@@ -20,6 +20,7 @@
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 namespace cc {
 
@@ -452,6 +453,211 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair (cta_group::2) variant for large bf16 GEMMs: a cluster of two CTAs
+// on one TPC owns a 256 x BN tile. Each CTA TMA-loads its own 128 rows of A
+// and one BN/2-row half of B; the leader issues M=256 tcgen05.mma for the
+// pair, which reads both CTAs' shared memory, so each SM moves half the B
+// bytes (64 instead of 96 bytes of operand per clock at full rate). Each
+// CTA's TMEM holds the accumulator of its own 128 rows; both CTAs run the
+// same epilogue on their rows.
+//   barriers: full[s] (leader; expects both CTAs' bytes), empty[s] and
+//   tfull[a] (both CTAs; multicast tcgen05.commit from the leader),
+//   tempty[a] (leader; both CTAs' epilogue warps arrive, the peer remotely)
+// ---------------------------------------------------------------------------
+template <int BN>
+struct Gemm2Cfg {
+  static constexpr int BK = 64;
+  static constexpr int KSTEPS = BK / 16;
+  static constexpr int A_BYTES = 128 * 128;        // own 128 rows x 64 K
+  static constexpr int B_BYTES = (BN / 2) * 128;   // own half of B
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int FIXED = kEpiWarps * kEpiStageBytes + 1024 + 256;
+  static constexpr int FIT = (232448 - FIXED) / STAGE_BYTES;
+  static constexpr int STAGES = FIT > 6 ? 6 : FIT;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
+  static constexpr uint32_t IDESC = umma_idesc(256, BN, false);
+  static_assert(TMEM_COLS <= 512 && SMEM_BYTES <= 232448, "pair GEMM resources");
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* desc, uint32_t leader_bar, int32_t x,
+                                                 int32_t y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(desc), "r"(leader_bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+template <int BN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
+                 int num_m2, int num_n, int num_kb) {
+  using Cfg = Gemm2Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + Cfg::STAGES * Cfg::A_BYTES;
+  uint8_t* smem_epi = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + kEpiWarps * kEpiStageBytes);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+  const int tiles = num_m2 * num_n;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int st = 0; st < Cfg::STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(Cfg::TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // both CTAs: own A rows and own B half, completion counted on the leader's barrier
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster_id; t < tiles; t += n_clusters) {
+        const int mb = t % num_m2, nb = t / num_m2;
+        const int arow = mb * 256 + (int)rank * 128;
+        const int brow = b_row<BN>(ep, nb, (int)rank);
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
+          const uint32_t lbar = map_to_rank(&full[stage], 0);
+          tma_load_2d_pair(smem_a + stage * Cfg::A_BYTES, &tmA, lbar, kb * Cfg::BK, arow);
+          tma_load_2d_pair(smem_b + stage * Cfg::B_BYTES, &tmB, lbar, kb * Cfg::BK, brow);
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {  // the pair's single MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster_id; t < tiles; t += n_clusters) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(smem_a + stage * Cfg::A_BYTES);
+            const uint32_t b0 = smem_u32(smem_b + stage * Cfg::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < Cfg::KSTEPS; ++k)
+              tc_mma_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
+                          (kb | k) != 0 ? 1u : 0u);
+            tc_commit_pair(&empty[stage]);
+            if (kb == num_kb - 1) tc_commit_pair(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == Cfg::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int quarter = warp & 3;
+    const int chalf = ew >> 2;
+    float* stg = reinterpret_cast<float*>(smem_epi + ew * kEpiStageBytes);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    const int cols = (ep.epilogue == CC_EPI_GLU) ? BN / 2 : BN;
+    const int c_begin = chalf * (cols / 2), c_end = c_begin + cols / 2;
+    for (int t = cluster_id; t < tiles; t += n_clusters) {
+      const int mb = t % num_m2, nb = t / num_m2;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(quarter * 32) << 16);
+      const int64_t row0 = (int64_t)mb * 256 + (int64_t)rank * 128 + quarter * 32;
+      for (int c0 = c_begin; c0 < c_end; c0 += 32) epilogue_chunk<BN, false>(ep, tbase, c0, row0, nb, stg, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(map_to_rank(&tempty[acc], 0));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // no CTA leaves while its peer may still arrive on / read from it
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(Cfg::TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -505,6 +711,40 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   gemm_kernel<BN, kTF32><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb, (int)a->K);
   CC_LAUNCH_CHECK("gemm");
   return CC_OK;
+}
+
+template <int BN>
+static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, cudaStream_t st) {
+  using Cfg = Gemm2Cfg<BN>;
+  CUtensorMap ta, tb;
+  int rc = make_map(&ta, a->A, false, a->K, a->M, a->lda, Cfg::BK, 128);
+  if (rc) return rc;
+  rc = make_map(&tb, a->B, false, a->K, a->N, a->ldb, Cfg::BK, BN / 2);
+  if (rc) return rc;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    attr_set = true;
+  }
+  const int num_m2 = (int)((a->M + 255) / 256);
+  const int num_n = (int)((a->N + BN - 1) / BN);
+  const int num_kb = (int)((a->K + Cfg::BK - 1) / Cfg::BK);
+  const int tiles = num_m2 * num_n;
+  const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+  ProfScope ps(st, OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
+  gemm2_kernel<BN><<<2 * clusters, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m2, num_n, num_kb);
+  CC_LAUNCH_CHECK("gemm (CTA pair)");
+  return CC_OK;
+}
+
+// CC_GEMM_PAIR=0 in the environment keeps every bf16 GEMM on single-CTA tiles (A/B runs)
+static bool pair_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CC_GEMM_PAIR");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 }  // namespace cc
@@ -576,5 +816,7 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   cudaStream_t st = as_stream(stream);
   // 3xTF32 runs 128-wide tiles: two accumulators (hi*hi, corrections) x two buffers fill TMEM
   if (tf32) return launch<128, true>(a, ep, kop, st);
+  // large bf16 GEMMs on CTA pairs: 256-row tiles, half the B traffic per SM
+  if (pair_enabled() && a->M >= 512 && a->N % 256 == 0) return launch_pair<256>(a, ep, st);
   return wide ? launch<256, false>(a, ep, kop, st) : launch<128, false>(a, ep, kop, st);
 }
