@@ -98,6 +98,31 @@ int cc_assemble_kv_capped(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t
                           const double* inv_freq_host, int64_t pos_offset,
                           void* dst_k, void* dst_v, int64_t dst_rows_cap, int32_t max_ctas, void* stream);
 
+/* Small host -> device upload (tables, ids) read by the SMs straight from
+ * pinned host memory (src_pinned: a pinned host pointer, 16-byte aligned),
+ * stream-ordered. Keeps such uploads off the copy engines, which may be busy
+ * with bulk cache DMA (cc_h2d_segments) for tens of milliseconds. */
+int cc_upload(void* dst_dev, const void* src_pinned, int64_t bytes, void* stream);
+
+/* Host-resident (pinned) chunk caches, transfer half: copy-engine DMA of
+ * layers [layer0, layer0 + n_layers) of every segment (segs_host: a HOST
+ * array whose k/v are pinned host pointers) into dst_k / dst_v
+ * ([layers][dst_rows_cap][H][D]) at the segments' destination rows, keys still
+ * position-free. One cudaMemcpy2DAsync per (segment, K|V): no SM is occupied
+ * by the transfer, so it overlaps scoring and recompute kernels at full PCIe
+ * rate. Replaces the per-chunk array reads of merge_caches / attention_banks
+ * (kv_store.py:237-248, :106-116) when the caches live in host memory. */
+int cc_h2d_segments(const cc_kv_segment* segs_host, int32_t n_segs, int32_t layer0, int32_t n_layers,
+                    int32_t kv_heads, int32_t head_dim, int32_t dtype, void* dst_k, void* dst_v,
+                    int64_t dst_rows_cap, void* stream);
+/* Rotation half: rotate the keys of rows [0, n_rows) in place over n_layers
+ * layers (k points at the first layer; layer stride rows_cap rows); row r of
+ * the segment containing it (by dst_row0) sits at position pos0 + r - dst_row0.
+ * Same float64-angle / separately-rounded arithmetic as cc_assemble_kv. */
+int cc_rope_rows_inplace(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_rows, int32_t n_layers,
+                         int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
+                         void* k, int64_t rows_cap, void* stream);
+
 /* Per-row float32 cos/sin tables [n][head_dim/2] for arbitrary positions
  * (float64 angle formation, tensor_core.py:41-51). */
 int cc_rope_table(const int64_t* positions, int64_t n, const double* inv_freq_host,

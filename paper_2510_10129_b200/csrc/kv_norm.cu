@@ -185,6 +185,70 @@ __global__ void __launch_bounds__(256) assemble_kernel(const cc_kv_segment* __re
   }
 }
 
+// In-place RoPE of keys that the copy engines already placed at their
+// destination rows (host-resident caches, cc_h2d_segments): one thread per
+// 16-byte vector of one (row, kv head), angles formed once and reused over the
+// layer group. Each thread reads and writes only its own vector.
+template <typename T>
+__global__ void __launch_bounds__(256) rope_inplace_kernel(const cc_kv_segment* __restrict__ segs, int n_segs,
+                                                           int64_t n_rows, int n_layers, int kv_heads, int head_dim,
+                                                           InvFreq inv, T* k, int64_t rows_cap) {
+  constexpr int V = Vec16<T>::N;
+  const int vecs_per_row = kv_heads * head_dim / V;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= n_rows * vecs_per_row) return;
+  const int64_t row = gid / vecs_per_row;
+  const int col = (int)(gid - row * vecs_per_row) * V;
+  const int pair0 = (col % head_dim) / 2;
+  int lo = 0, hi = n_segs - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (segs[mid].dst_row0 <= row) lo = mid; else hi = mid - 1;
+  }
+  const double pos = (double)(segs[lo].pos0 + (row - segs[lo].dst_row0));
+  float c[V / 2], s[V / 2];
+#pragma unroll
+  for (int p = 0; p < V / 2; ++p) {
+    double sd, cd;
+    sincos(pos * inv.v[pair0 + p], &sd, &cd);
+    c[p] = (float)cd;
+    s[p] = (float)sd;
+  }
+  const int64_t row_elems = (int64_t)kv_heads * head_dim;
+  T* base = k + row * row_elems + col;
+  for (int l = 0; l < n_layers; ++l) {
+    T* p = base + l * rows_cap * row_elems;
+    const uint4 raw = *reinterpret_cast<const uint4*>(p);
+    float x[V], y[V];
+    if constexpr (V == 4) {
+      const float4 f = *reinterpret_cast<const float4*>(&raw);
+      x[0] = f.x; x[1] = f.y; x[2] = f.z; x[3] = f.w;
+    } else {
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int i = 0; i < V / 2; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        x[2 * i] = f.x;
+        x[2 * i + 1] = f.y;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < V / 2; ++q) rope_pair(x[2 * q], x[2 * q + 1], c[q], s[q], y[2 * q], y[2 * q + 1]);
+    store_vec<T>(p, y);
+  }
+}
+
+// Small host -> device uploads (index tables, token ids, segment tables) read
+// straight from pinned host memory by the SMs: they never queue behind bulk
+// cache DMA on the copy engines.
+__global__ void upload_kernel(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int64_t bytes) {
+  const int64_t n16 = bytes >> 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  const int64_t tail = (n16 << 4) + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tail < bytes) dst[tail] = src[tail];
+}
+
 static bool fill_inv(InvFreq& inv, const double* host, int head_dim) {
   if (head_dim <= 0 || head_dim % 2 || head_dim / 2 > kMaxPairs || !host) return false;
   for (int i = 0; i < head_dim / 2; ++i) inv.v[i] = host[i];
@@ -535,6 +599,77 @@ int cc_assemble_kv_capped(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t
     return fail(CC_ERR_UNSUPPORTED, "cache dtype %d unsupported", dtype);
   }
   CC_LAUNCH_CHECK("assemble_kv");
+  return CC_OK;
+}
+
+int cc_upload(void* dst_dev, const void* src_pinned, int64_t bytes, void* stream) {
+  CC_CHECK_ARG(bytes >= 0, CC_ERR_VALUE, "negative upload size");
+  if (bytes == 0) return CC_OK;
+  CC_CHECK_ARG(dst_dev && src_pinned && ((reinterpret_cast<uintptr_t>(dst_dev) | reinterpret_cast<uintptr_t>(src_pinned)) % 16) == 0,
+               CC_ERR_UNSUPPORTED, "upload buffers must be 16-byte aligned");
+  const int64_t n16 = bytes >> 4;
+  const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>((n16 + 255) / 256, 1), 64);
+  upload_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<uint8_t*>(dst_dev),
+                                                     static_cast<const uint8_t*>(src_pinned), bytes);
+  CC_LAUNCH_CHECK("upload");
+  return CC_OK;
+}
+
+int cc_h2d_segments(const cc_kv_segment* segs_host, int32_t n_segs, int32_t layer0, int32_t n_layers,
+                    int32_t kv_heads, int32_t head_dim, int32_t dtype, void* dst_k, void* dst_v,
+                    int64_t dst_rows_cap, void* stream) {
+  CC_CHECK_ARG(segs_host && n_segs > 0, CC_ERR_CONSISTENCY, "nothing to copy");
+  CC_CHECK_ARG(layer0 >= 0 && n_layers > 0 && kv_heads > 0 && head_dim > 0, CC_ERR_DIMENSION, "bad geometry");
+  CC_CHECK_ARG(dtype == CC_BF16 || dtype == CC_F32, CC_ERR_UNSUPPORTED, "cache dtype %d unsupported", dtype);
+  CC_CHECK_ARG(dst_k && dst_v, CC_ERR_VALUE, "null destination");
+  const size_t row_bytes = (size_t)kv_heads * head_dim * (dtype == CC_BF16 ? 2 : 4);
+  cudaStream_t st = as_stream(stream);
+  for (int i = 0; i < n_segs; ++i) {
+    const cc_kv_segment& s = segs_host[i];
+    CC_CHECK_ARG(s.dst_row0 >= 0 && s.dst_row0 + s.n_rows <= dst_rows_cap && s.src_row0 >= 0 &&
+                     s.src_row0 + s.n_rows <= s.src_rows,
+                 CC_ERR_DIMENSION, "segment %d out of range", i);
+    if (s.n_rows == 0) continue;
+    const size_t src_off = ((size_t)layer0 * s.src_rows + s.src_row0) * row_bytes;
+    const size_t dst_off = ((size_t)layer0 * dst_rows_cap + s.dst_row0) * row_bytes;
+    const size_t width = (size_t)s.n_rows * row_bytes;
+    const void* srcs[2] = {s.k, s.v};
+    void* dsts[2] = {dst_k, dst_v};
+    for (int t = 0; t < 2; ++t) {
+      cudaError_t e = cudaMemcpy2DAsync(static_cast<uint8_t*>(dsts[t]) + dst_off, dst_rows_cap * row_bytes,
+                                        static_cast<const uint8_t*>(srcs[t]) + src_off, s.src_rows * row_bytes,
+                                        width, n_layers, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return fail(CC_ERR_CUDA, "cudaMemcpy2DAsync (segment %d): %s", i, cudaGetErrorString(e));
+    }
+  }
+  return CC_OK;
+}
+
+int cc_rope_rows_inplace(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_rows, int32_t n_layers,
+                         int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host, void* k,
+                         int64_t rows_cap, void* stream) {
+  CC_CHECK_ARG(segs_dev && n_segs > 0, CC_ERR_CONSISTENCY, "no segments");
+  CC_CHECK_ARG(n_layers > 0 && kv_heads > 0 && n_rows <= rows_cap, CC_ERR_DIMENSION, "bad geometry");
+  InvFreq inv;
+  CC_CHECK_ARG(fill_inv(inv, inv_freq_host, head_dim), CC_ERR_DIMENSION, "rotary head_dim %d unsupported",
+               head_dim);
+  if (n_rows == 0) return CC_OK;
+  const int V = dtype == CC_BF16 ? 8 : 4;
+  CC_CHECK_ARG(head_dim % V == 0, CC_ERR_UNSUPPORTED, "head_dim %d not a multiple of %d", head_dim, V);
+  CC_CHECK_ARG(k && reinterpret_cast<uintptr_t>(k) % 16 == 0, CC_ERR_UNSUPPORTED, "keys not 16-byte aligned");
+  const int64_t threads = n_rows * (int64_t)(kv_heads * head_dim / V);
+  const unsigned grid = (unsigned)((threads + 255) / 256);
+  ProfScope ps(as_stream(stream), OP_ROPE, 2.0 * n_rows * n_layers * kv_heads * head_dim * (dtype == CC_BF16 ? 2 : 4));
+  if (dtype == CC_BF16)
+    rope_inplace_kernel<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>(
+        segs_dev, n_segs, n_rows, n_layers, kv_heads, head_dim, inv, reinterpret_cast<__nv_bfloat16*>(k), rows_cap);
+  else if (dtype == CC_F32)
+    rope_inplace_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(segs_dev, n_segs, n_rows, n_layers, kv_heads,
+                                                                    head_dim, inv, reinterpret_cast<float*>(k),
+                                                                    rows_cap);
+  else
+    return fail(CC_ERR_UNSUPPORTED, "cache dtype %d unsupported", dtype);
+  CC_LAUNCH_CHECK("rope_rows_inplace");
   return CC_OK;
 }
 

@@ -30,12 +30,66 @@ def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+class _PinnedRing:
+    """Pinned host staging for small uploads, reused round-robin: a region is
+    rewritten only after the upload that last read it has run (its event)."""
+
+    SIZE = 16 << 20
+
+    def __init__(self) -> None:
+        self.buf = torch.empty(self.SIZE, dtype=torch.uint8, pin_memory=True)
+        self.np = self.buf.numpy()
+        self.ptr = self.buf.data_ptr()
+        self.head = 0
+        self.pending: list = []  # (start, end, event) in allocation order
+
+    def alloc(self, n: int) -> int:
+        n = (n + 255) & ~255
+        if self.head + n > self.SIZE:
+            self.head = 0
+        start, end = self.head, self.head + n
+        keep = []
+        for a, b, ev in self.pending:
+            if a < end and start < b:
+                ev.synchronize()  # long done in practice: uploads run within microseconds
+            else:
+                keep.append((a, b, ev))
+        self.pending = keep
+        self.head = end
+        return start
+
+    def release(self, start: int, n: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record()
+        self.pending.append((start, start + n, ev))
+
+
+_ring: _PinnedRing | None = None
+
+
 def host_to_device(data: np.ndarray, device) -> torch.Tensor:
-    """Small host table -> device via pinned staging (stream-ordered copy)."""
-    t = torch.from_numpy(np.ascontiguousarray(data))
+    """Small host table -> device, stream-ordered. The bytes are staged in a
+    pinned ring and read by the SMs (cc_upload), not the copy engines, so a
+    table never waits behind streamed cache DMA (cc_h2d_segments)."""
+    global _ring
+    arr = np.ascontiguousarray(data)
+    t = torch.from_numpy(arr)
+    if torch.device(device).type != "cuda":
+        return t.clone()
     if t.numel() == 0:
         return torch.empty(0, dtype=t.dtype, device=device)
-    return t.pin_memory().to(device, non_blocking=True)
+    n = arr.nbytes
+    if n > _PinnedRing.SIZE // 4:
+        return t.pin_memory().to(device, non_blocking=True)
+    if _ring is None:
+        _ring = _PinnedRing()
+    off = _ring.alloc(n)
+    _ring.np[off:off + n] = arr.reshape(-1).view(np.uint8)
+    out = torch.empty((n + 15) & ~15, dtype=torch.uint8, device=device)
+    with torch.cuda.device(out.device):
+        _lib.call("cc_upload", out.data_ptr(), _ring.ptr + off, n, _stream())
+        _ring.release(off, n)
+    return out[:n].view(t.dtype).view(t.shape)
 
 
 def _as_layers(x, device=None) -> torch.Tensor:
@@ -118,12 +172,6 @@ class ChunkCache:
     def attention_banks(self, rope: RopeParams, trace: PipelineTrace | None = None, stage: str = "decode"):
         k = self.local_rotated_keys(rope)
         return list(zip(k.unbind(0), self.v.unbind(0)))
-
-
-# CTAs of the zero-copy (host -> device) streamed merge: ~24 x 256 threads x
-# 32 B keeps > 150 KB in flight (PCIe Gen5 x16 latency-bandwidth product)
-# while leaving the other SMs to the scoring / recompute kernels.
-STREAM_CTAS = 24
 
 
 def _dtype_code(dt: torch.dtype) -> int:
@@ -272,24 +320,96 @@ def compute_positions(chunk_lens: Sequence[int], prefix_len: int) -> np.ndarray:
     return np.arange(prefix_len + sum(chunk_lens), dtype=np.int64)
 
 
-def _stream_segments(spec, layers: int, dev) -> torch.Tensor:
-    """Per-layer copies of the segment table with layer-l host pointers."""
-    base = _segments(spec).view(np.int64).reshape(len(spec), 7)
-    per_layer = np.repeat(base[None], layers, axis=0)
-    for si, (c, *_rest) in enumerate(spec):
-        per_layer[:, si, 0] += np.arange(layers, dtype=np.int64) * c.k.stride(0) * c.k.element_size()
-        per_layer[:, si, 1] += np.arange(layers, dtype=np.int64) * c.v.stride(0) * c.v.element_size()
-    return host_to_device(per_layer.reshape(-1).view(np.uint8), dev)
+def _layer_groups(n_layers: int, ramp=(1, 2, 3), cap: int = 6, taper=(4, 2)) -> list[tuple[int, int]]:
+    """[l0, l1) layer groups for streamed caches: ``ramp`` first (the consumer
+    starts on layer 0 early), then groups of ``cap``, then ``taper`` (a
+    transfer-bound consumer finishes soon after the last byte). Every group
+    costs one 2-D copy per (chunk, K|V): tall groups keep the DMA efficient
+    (~4 us fixed cost per copy) and the copy queue short (the driver blocks the
+    host beyond ~1,000 queued copies)."""
+    sizes, left = [], n_layers
+    for s in ramp:
+        if left <= 0:
+            break
+        sizes.append(min(s, left))
+        left -= sizes[-1]
+    tail = []
+    for s in reversed(taper):
+        if left <= 0:
+            break
+        tail.insert(0, min(s, left))
+        left -= tail[0]
+    while left > 0:
+        sizes.append(min(cap, left))
+        left -= sizes[-1]
+    out, l0 = [], 0
+    for s in sizes + tail:
+        out.append((l0, l0 + s))
+        l0 += s
+    return out
+
+
+# scoring caches gate the scoring pass layer by layer (transfer-bound): small
+# first and last groups; primary caches are needed only after the selection
+SCORING_GROUPS = dict(ramp=(1, 2, 3), cap=6, taper=(4, 2))
+PRIMARY_GROUPS = dict(ramp=(1, 3, 6), cap=8, taper=())
+
+
+_copy_streams: dict = {}
+
+
+def _copy_stream(dev: torch.device) -> torch.cuda.Stream:
+    key = dev.index if dev.index is not None else torch.cuda.current_device()
+    if key not in _copy_streams:
+        _copy_streams[key] = torch.cuda.Stream(device=dev)
+    return _copy_streams[key]
+
+
+def _stream_in(spec, rot: np.ndarray, n_rows: int, k_store: torch.Tensor, v_store: torch.Tensor,
+               rope: RopeParams, groups: dict) -> list:
+    """Host-resident (pinned) chunk caches -> k_store / v_store
+    ([L][cap][H][D]): per layer group, the copy engines DMA every segment's
+    rows (cc_h2d_segments, on a dedicated copy stream, so no SM is spent on the
+    transfer), then the current stream rotates the group's keys in place
+    (cc_rope_rows_inplace, segments ``rot`` give each row's position). Returns
+    one event per layer, recorded on the current stream after its rotation."""
+    for i, item in enumerate(spec):
+        c = item[0]
+        if not (c.k.is_pinned() and c.v.is_pinned()):
+            raise CacheConsistencyError(f"chunk {i}: host caches must be in pinned memory")
+    L, cap, H, D = k_store.shape
+    dt = _dtype_code(k_store.dtype)
+    host_segs = np.ascontiguousarray(_segments(spec))
+    rot_dev = host_to_device(rot, k_store.device)
+    cur = torch.cuda.current_stream()
+    cp = _copy_stream(k_store.device)
+    cp.wait_stream(cur)  # destination allocated / previous users done
+    k_store.record_stream(cp)
+    v_store.record_stream(cp)
+    inv = rope.inv_freq
+    row_bytes = H * D * k_store.element_size()
+    ready = []
+    for l0, l1 in _layer_groups(L, **groups):
+        _lib.call("cc_h2d_segments", host_segs.ctypes.data, len(spec), l0, l1 - l0, H, D, dt, k_store.data_ptr(),
+                  v_store.data_ptr(), cap, cp.cuda_stream)
+        copied = torch.cuda.Event()
+        copied.record(cp)
+        cur.wait_event(copied)
+        _lib.call("cc_rope_rows_inplace", rot_dev.data_ptr(), len(rot) // (7 * 8), n_rows, l1 - l0, H, D, dt,
+                  inv.ctypes.data, k_store.data_ptr() + l0 * cap * row_bytes, cap, _stream())
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        ready.extend([ev] * (l1 - l0))
+    return ready
 
 
 def stream_local_banks(chunks: Sequence[ChunkCache], rope: RopeParams, device):
     """Host-resident (pinned) chunk caches -> one device bank per layer
     holding every chunk's keys rotated at its LOCAL positions and its values
-    (what ChunkCache.local_rotated_keys + .v give per chunk), read straight
-    over PCIe by the assembly kernel one layer per launch on the current
-    stream; each layer records an event so the scoring pass can start on
-    layer l while later layers are still in flight. Returns (K [L,R,H,D],
-    V, row offsets per chunk, events)."""
+    (what ChunkCache.local_rotated_keys + .v give per chunk). The copy engines
+    bring the caches in layer group by layer group (_stream_in); each layer
+    has an event so the scoring pass starts on layer l while later layers are
+    still in flight. Returns (K [L,R,H,D], V, row offsets per chunk, events)."""
     first = chunks[0]
     for i, c in enumerate(chunks):
         if not (c.k.is_pinned() and c.v.is_pinned()):
@@ -303,17 +423,7 @@ def stream_local_banks(chunks: Sequence[ChunkCache], rope: RopeParams, device):
     K = torch.empty(L, total, H, D, dtype=first.k.dtype, device=dev)
     V = torch.empty_like(K)
     spec = [(c, 0, int(o), c.n_rows, 0) for c, o in zip(chunks, offs[:-1])]  # pos0 = 0: local positions
-    segs = _stream_segments(spec, L, dev)
-    seg_bytes = len(spec) * 7 * 8
-    inv = rope.inv_freq
-    ready = []
-    for layer in range(L):
-        _lib.call("cc_assemble_kv_capped", segs.data_ptr() + layer * seg_bytes, len(spec), total, 1, H, D,
-                  _dtype_code(first.k.dtype), inv.ctypes.data, 0, K[layer].data_ptr(), V[layer].data_ptr(), total,
-                  STREAM_CTAS, _stream())
-        ev = torch.cuda.Event()
-        ev.record()
-        ready.append(ev)
+    ready = _stream_in(spec, _segments(spec), total, K, V, rope, SCORING_GROUPS)
     return K, V, offs[:-1], ready
 
 
@@ -370,24 +480,12 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
         _lib.call("cc_assemble_kv", segs.data_ptr(), len(spec), total, L, H, D, _dtype_code(first.k.dtype),
                   inv.ctypes.data, 0, k_store.data_ptr(), v_store.data_ptr(), cap, _stream())
     elif total:
-        # Host-resident (pinned) chunk caches: the assembly kernel reads them
-        # straight over PCIe (zero-copy), one layer per launch, and each layer
+        # Host-resident (pinned) chunk caches: copy-engine DMA straight into
+        # the merged stores, keys rotated in place per layer group; each layer
         # records an event so a consumer can start on layer l while later
         # layers are still streaming in.
-        for i, c in enumerate(chunks):
-            if not (c.k.is_pinned() and c.v.is_pinned()):
-                raise CacheConsistencyError(f"chunk {i}: host caches must be in pinned memory")
-        segs = _stream_segments(spec, L, dev)
-        seg_bytes = len(spec) * 7 * 8
-        inv = rope.inv_freq
-        layer_ready = []
-        for layer in range(L):
-            _lib.call("cc_assemble_kv_capped", segs.data_ptr() + layer * seg_bytes, len(spec), total, 1, H, D,
-                      _dtype_code(first.k.dtype), inv.ctypes.data, 0, k_store[layer].data_ptr(),
-                      v_store[layer].data_ptr(), cap, STREAM_CTAS, _stream())
-            ev = torch.cuda.Event()
-            ev.record()
-            layer_ready.append(ev)
+        rot = _segments([(first, 0, 0, total, 0)])  # merged row r sits at position r
+        layer_ready = _stream_in(spec, rot, total, k_store, v_store, rope, PRIMARY_GROUPS)
     if trace is not None:  # one rotation per merged row per layer (kv_store.py:245-248), folded
         trace.rope("merge_overhead", L * total * H, D)
     # source map is derived lazily from the layout (MergedCache.source)

@@ -241,4 +241,5 @@ def bank_tables(layers: int, seqs: list[tuple], device) -> torch.Tensor:
     lidx = np.arange(layers, dtype=np.int64)[:, None]
     arr[:, :, 0] += lidx * stride[None, :, 0] * (per[None, :, 0] != 0)
     arr[:, :, 1] += lidx * stride[None, :, 1] * (per[None, :, 1] != 0)
-    return torch.from_numpy(arr.reshape(-1).view(np.uint8)).pin_memory().to(device, non_blocking=True)
+    from .kv_store import host_to_device
+    return host_to_device(arr.reshape(-1).view(np.uint8), device)

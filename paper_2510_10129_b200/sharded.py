@@ -210,7 +210,7 @@ def cacheclip_prefill_sharded(compute: ShardCompute, exchange: Exchange, plan: S
         w = c % W
         order.append(np.arange(w * l_max + offs[w], w * l_max + offs[w] + lens[c]))
         offs[w] += int(lens[c])
-    perm = torch.from_numpy(np.concatenate(order)).to(gathered.device)
+    perm = host_to_device(np.concatenate(order).astype(np.int64), gathered.device)
     scores = gathered.index_select(0, perm)
     selected = compute.select(scores, plan.chunk_lens, config, plan.prefix_len)
     # 3. row plan (same on every rank) and the recompute + query pass

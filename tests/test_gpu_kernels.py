@@ -338,7 +338,8 @@ def test_lm_head_argmax():
 
 def test_streamed_merge_from_pinned_host_matches_device_merge():
     """Host-resident (pinned) chunk caches are merged straight from host memory
-    layer by layer (zero-copy reads, per-layer events) — bitwise equal to the
+    by the copy engines layer group by layer group, keys rotated in place
+    (per-layer events) — bitwise equal to the
     device-resident merge; the pipeline result is identical too."""
     import paper_2510_10129_b200 as cc
     from oracle.synth import C1_EXACT as w

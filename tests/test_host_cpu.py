@@ -127,3 +127,14 @@ def test_rope_inv_freq_matches_reference_formula():
     from paper_2510_10129_b200 import RopeParams
     r = RopeParams(128, 1e6)
     np.testing.assert_array_equal(r.inv_freq, 1e6 ** (-np.arange(0, 128, 2, dtype=np.float64) / 128))
+
+
+def test_streamed_layer_groups_cover_every_layer_once():
+    from paper_2510_10129_b200.kv_store import PRIMARY_GROUPS, SCORING_GROUPS, _layer_groups
+    for n in (1, 2, 3, 5, 11, 24, 28, 48):
+        for kw in (SCORING_GROUPS, PRIMARY_GROUPS):
+            g = _layer_groups(n, **kw)
+            assert g[0][0] == 0 and g[-1][1] == n
+            assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(g, g[1:]))
+    assert [l1 - l0 for l0, l1 in _layer_groups(24, **SCORING_GROUPS)] == [1, 2, 3, 6, 6, 4, 2]
+    assert [l1 - l0 for l0, l1 in _layer_groups(28, **PRIMARY_GROUPS)] == [1, 3, 6, 8, 8, 2]
