@@ -372,6 +372,10 @@ int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t
  * reduction, 9 lm_head, 10 rope table. */
 void cc_profile_enable(int32_t on);
 int64_t cc_profile_collect(int32_t* ops, double* work, float* ms, int64_t cap);
+/* Set the algorithmic work of pending records of `op` launched with an
+ * unknown (negative) work: cc_forward_rows with attn_pairs < 0, i.e. launched
+ * before the host has read the selected positions. */
+void cc_profile_fill_work(int32_t op, double work);
 
 #ifdef __cplusplus
 }

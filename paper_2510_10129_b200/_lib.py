@@ -121,6 +121,7 @@ _SIGS = {
                            ctypes.POINTER(ScoreSpec), ctypes.POINTER(vp), vp, vp], i32),
     "cc_profile_enable": ([i32], None),
     "cc_profile_collect": ([vp, vp, vp, i64], i64),
+    "cc_profile_fill_work": ([i32, ctypes.c_double], None),
 }
 
 PROFILE_OPS = ("gemm_bf16", "gemm_3xtf32", "attention_tcgen05", "attention_mma", "banked_attention_f32",

@@ -541,6 +541,12 @@ int64_t cc_profile_collect(int32_t* ops, double* work, float* ms, int64_t cap) {
   g_prof.clear();
   return n;
 }
+void cc_profile_fill_work(int32_t op, double work) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (auto& r : g_prof)
+    if (r.op == op && r.work < 0.0) r.work = work;
+}
+
 const char* cc_last_error(void) { return g_err; }
 
 int cc_device_check(int dev) {

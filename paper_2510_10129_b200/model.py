@@ -226,14 +226,21 @@ def _row_factor(model: Model, knobs, n: int, n_plain: int = 0, device=None):
 def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | None, sel_idx_dev,
                       query_ids: Sequence[int] | None, *, knobs=None, append: bool = True,
                       want_logits: bool = True, trace: PipelineTrace | None = None,
-                      sel_stage: str = "recompute", query_stage: str = "decode"):
+                      sel_stage: str = "recompute", query_stage: str = "decode", n_sel: int | None = None):
     """One layer-wise pass over selected rows (recomputed in place, causal by
     global position) followed by query rows appended at n_rows.. — the fused
     form of selective_forward + extend_cache (bit-identical composition in the
-    reference's algebra: selected rows never see query positions)."""
+    reference's algebra: selected rows never see query positions).
+
+    ``n_sel``: the selected rows are known only on the device (``sel_idx`` is
+    None, ``sel_idx_dev`` holds ``n_sel`` sorted indices still being written
+    by the selection kernel on this stream): the pass is launched without a
+    host sync and the caller completes the host bookkeeping with
+    ``finish_selection`` once the indices are read back."""
     c = model.config
     dev = model.device
-    m = 0 if sel_idx is None else int(sel_idx.size)
+    deferred = sel_idx is None and n_sel is not None
+    m = int(n_sel) if deferred else (0 if sel_idx is None else int(sel_idx.size))
     nq = 0 if query_ids is None else len(query_ids)
     base = cache.n_rows
     R = m + nq
@@ -256,24 +263,40 @@ def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | No
               nq, base, ids.data_ptr(), pos.data_ptr(), torch.cuda.current_stream().cuda_stream)
     rf = _row_factor(model, knobs, nq, m, dev)
     ks, vs = cache.k_store, cache.v_store
-    pairs = (int(np.sum(sel_idx + 1)) if m else 0) + (visible_pairs(nq, base) if nq else 0)
+    # attention work, for the launch profiler only: unknown (-1) until the
+    # deferred indices are read back (finish_selection fills it in)
+    pairs = -1 if deferred and m else (int(np.sum(sel_idx + 1)) if m else 0) + (visible_pairs(nq, base) if nq else 0)
     plan = KvPlan(k_scatter=ks, v_scatter=vs, attn_k=ks, attn_v=vs, dst_rows=pos,
                   layer_ready=getattr(cache, "layer_ready", None))
     res = forward_rows(model, ids, pos, plan, base + nq, row_factor=rf, want_logits=want_logits and nq > 0,
                        pairs=pairs)
     cache.layer_ready = None  # every layer is now ordered before this stream's work
     if trace is not None:
-        if m:
-            trace_layer(trace, c, sel_stage, m, int(np.sum(sel_idx + 1)), times=c.n_layers)
         if nq:
             trace_layer(trace, c, query_stage, nq, visible_pairs(nq, base), times=c.n_layers)
         if nq and want_logits:
             trace.matmul(query_stage, 1, c.d_model, c.vocab_size)
     if append and nq:
         cache._append_rows(query_ids, q_dev)
-    if m:
-        cache.recomputed_rows = tuple(np.asarray(sel_idx, dtype=np.int64).tolist())
+    if m and not deferred:
+        finish_selection(model, cache, sel_idx, base, nq, trace=trace, sel_stage=sel_stage)
     return res.logits, res.argmax
+
+
+def finish_selection(model: Model, cache: MergedCache, sel_idx: np.ndarray, base: int, nq: int, *,
+                     trace: PipelineTrace | None = None, sel_stage: str = "recompute", deferred: bool = False):
+    """Host bookkeeping of a recompute pass once the selected indices are on
+    the host: recomputed_rows, the reference's MAC trace and (deferred
+    launches) the attention work of the launch profiler."""
+    c = model.config
+    pairs_sel = int(np.sum(np.asarray(sel_idx, dtype=np.int64) + 1))
+    if trace is not None:
+        trace_layer(trace, c, sel_stage, int(sel_idx.size), pairs_sel, times=c.n_layers)
+    cache.recomputed_rows = tuple(np.asarray(sel_idx, dtype=np.int64).tolist())
+    if deferred:
+        pairs = pairs_sel + (visible_pairs(nq, base) if nq else 0)
+        _lib.load().cc_profile_fill_work(_lib.PROFILE_OPS.index("attention_tcgen05"),
+                                         4.0 * c.n_heads * c.d_head * pairs)
 
 
 last_device_logits: torch.Tensor | None = None

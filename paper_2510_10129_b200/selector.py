@@ -193,18 +193,64 @@ class DeviceSelection:
         return AuxSelection(aux_idx, self.windows(), self.n_tokens, self.config.recomp_ratio)
 
 
-def select_tokens_device(scores: ImportanceScores, config: SelectionConfig, index_offset: int = 0) -> DeviceSelection:
+@dataclass
+class PendingSelection:
+    """The selection kernel's device outputs, launched but not yet read back."""
+    idx: torch.Tensor
+    cnt: torch.Tensor
+    win_sel: torch.Tensor
+    win_kept: torch.Tensor
+    budget: int
+    n_tokens: int
+    chunk_lens: tuple[int, ...]
+    config: SelectionConfig
+    index_offset: int
+    done: torch.cuda.Event  # recorded right behind the selection kernel
+
+    @property
+    def count_known(self) -> bool:
+        """With threshold <= 1 and no expansion every candidate's window is
+        kept (count >= 1 >= threshold), so exactly `budget` rows are selected
+        (selector.py:199-207): the host knows the count without reading it."""
+        return self.config.window_threshold <= 1 and not self.config.expand_full_window
+
+    def read_back(self, stream: torch.cuda.Stream | None = None) -> DeviceSelection:
+        """One D2H read: count | window counts | kept flags | indices. On a
+        side `stream` (waiting for the kernel) it does not wait for work
+        queued on the launching stream after the selection."""
+        if stream is None:
+            flags = torch.cat([self.cnt, self.win_sel.long(), self.win_kept.long(), self.idx]).cpu().numpy()
+        else:
+            stream.wait_event(self.done)
+            with torch.cuda.stream(stream):
+                dev = torch.cat([self.cnt, self.win_sel.long(), self.win_kept.long(), self.idx])
+                host = torch.empty(dev.shape, dtype=dev.dtype, pin_memory=True)
+                host.copy_(dev, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record()
+            for t in (self.cnt, self.win_sel, self.win_kept, self.idx):
+                t.record_stream(stream)
+            ev.synchronize()
+            flags = host.numpy()
+        k = int(flags[0])
+        n_win = self.win_sel.numel()
+        return DeviceSelection(k, self.idx[:k], flags[1 + 2 * n_win:1 + 2 * n_win + k].astype(np.int64),
+                               flags[1:1 + n_win], flags[1 + n_win:1 + 2 * n_win], self.n_tokens, self.chunk_lens,
+                               self.config, self.index_offset)
+
+
+def launch_select(scores: ImportanceScores, config: SelectionConfig, index_offset: int = 0) -> PendingSelection:
     n = int(scores.device_scores.numel())
     budget = selection_budget(config.recomp_ratio, n)
     idx, cnt, wsel, wkept = _run_select(scores.device_scores, scores.chunk_lens, budget, config.window_len,
                                         config.window_threshold, config.expand_full_window, index_offset)
-    n_win = wsel.numel()
-    # one D2H read: count | window counts | kept flags | indices
-    flags = torch.cat([cnt, wsel.long(), wkept.long(), idx]).cpu().numpy()
-    k = int(flags[0])
-    return DeviceSelection(k, idx[:k], flags[1 + 2 * n_win:1 + 2 * n_win + k].astype(np.int64),
-                           flags[1:1 + n_win], flags[1 + n_win:1 + 2 * n_win], n, tuple(scores.chunk_lens), config,
-                           index_offset)
+    done = torch.cuda.Event()
+    done.record()
+    return PendingSelection(idx, cnt, wsel, wkept, budget, n, tuple(scores.chunk_lens), config, index_offset, done)
+
+
+def select_tokens_device(scores: ImportanceScores, config: SelectionConfig, index_offset: int = 0) -> DeviceSelection:
+    return launch_select(scores, config, index_offset).read_back()
 
 
 def map_selection(aux_selection: AuxSelection, aux_spans: Sequence[TokenSpan], primary_spans: Sequence[TokenSpan],
