@@ -75,6 +75,37 @@ B1 = Workload("b1", B1_PRIMARY, B1_AUX, prefix_len=8, n_chunks=3, chunk_len=64, 
 R1 = Workload("r1", C1_PRIMARY, B1_AUX, prefix_len=5, n_chunks=6, chunk_len=0, query_len=9, ratio=0.3,
               window_threshold=3, bias_std=0.05, chunk_lens=(37, 1, 130, 8, 64, 7))
 
+# Cross-tokenizer pair (selector.py:217-245 +
+# tokenizers.py:151-177): the primary tokenizes single characters, the
+# scoring model's tokenizer adds 64 two-character merges, so an aux token may
+# cover two primary tokens and the plan is projected through the spans.
+X1_AUX = OracleConfig(n_layers=2, n_heads=2, n_kv_heads=2, d_model=128, d_head=64,
+                      d_ff=512, vocab_size=512 + 64, rope_base=1e4, norm_eps=1e-5,
+                      activation="silu", mlp_gated=True)
+X1_RATIO, X1_WINDOW_THRESHOLD = 0.25, 2
+
+
+def cross_tokenizer_case(seed: int = 0, n_chunks: int = 5, chunk_chars: int = 96, prefix_chars: int = 11,
+                         query_chars: int = 20):
+    """(primary vocab, aux vocab, prefix text, [chunk texts], query text).
+    Texts are random characters of the primary vocab with frequent merge
+    pairs, so both tokenizations differ in length and alignment."""
+    base = [chr(0x4E00 + i) for i in range(C1_PRIMARY.vocab_size)]
+    merges = [base[2 * k] + base[2 * k + 1] for k in range(X1_AUX.vocab_size - len(base))]
+    rng = np.random.default_rng(seed)
+
+    def text(n):
+        out = []
+        while len(out) < n:
+            if rng.random() < 0.4:
+                out.extend(merges[int(rng.integers(0, len(merges)))])
+            else:
+                out.append(base[int(rng.integers(0, len(base)))])
+        return "".join(out[:n])
+
+    return base, base + merges, text(prefix_chars), [text(chunk_chars) for _ in range(n_chunks)], text(query_chars)
+
+
 # Qwen2.5-7B / 0.5B shapes (BASELINE configs[1..2]); GPU-only sizes.
 QWEN7B = OracleConfig(n_layers=28, n_heads=28, n_kv_heads=4, d_model=3584, d_head=128,
                       d_ff=18944, vocab_size=152064, rope_base=1e6, norm_eps=1e-6,

@@ -30,7 +30,8 @@ sys.path.insert(0, REF_SRC)
 import cacheclip as ref  # noqa: E402  (the reference, read-only)
 
 from oracle import cacheclip_oracle as orc  # noqa: E402
-from oracle.synth import B1, C1, C1_EXACT, R1, Workload  # noqa: E402
+from oracle.synth import (B1, C1, C1_EXACT, C1_PRIMARY, R1, X1_AUX, X1_RATIO,  # noqa: E402
+                          X1_WINDOW_THRESHOLD, Workload, cross_tokenizer_case)
 
 ROW_STRIDE = 16  # sampled rows kept in the fixture (keeps files small)
 
@@ -135,6 +136,30 @@ def run_cacheblend(w: Workload, seed: int = 0) -> dict:
                 digest_cb_logits=np.array(digest([out.logits])))
 
 
+def run_cross_tokenizer(seed: int = 0) -> dict:
+    """cacheclip_prefill with two different tokenizers (pipeline.py:118-226):
+    chunk texts re-encoded by both, the aux selection projected onto primary
+    tokens through the character spans (selector.py:217-245)."""
+    pv, av, prefix_t, chunk_ts, query_t = cross_tokenizer_case(seed)
+    tp, ta = ref.GreedyTokenizer(pv, "chars"), ref.GreedyTokenizer(av, "chars+merges")
+    p_params = orc.seeded_params(C1_PRIMARY, 0)
+    a_params = orc.seeded_params(X1_AUX, 1)
+    primary = ref.Model(ref_config(C1_PRIMARY, "chars"), orc.mha_expand(C1_PRIMARY, p_params))
+    aux = ref.Model(ref_config(X1_AUX, "chars+merges"), orc.mha_expand(X1_AUX, a_params))
+    chunks = [ref.prefill_chunk(primary, tp.encode(prefix_t), tp.encode(t)) for t in chunk_ts]
+    aux_chunks = [ref.prefill_chunk(aux, ta.encode(prefix_t), ta.encode(t)) for t in chunk_ts]
+    cfg = ref.SelectionConfig(recomp_ratio=X1_RATIO, window_threshold=X1_WINDOW_THRESHOLD)
+    scores = ref.aux_score_tokens(aux, aux_chunks, ta.encode(query_t))
+    aux_sel = ref.select_tokens(scores, cfg)
+    clip = ref.cacheclip_prefill(primary, aux, chunks, aux_chunks, query_t, cfg,
+                                 primary_tokenizer=tp, aux_tokenizer=ta)
+    return dict(x_scores=scores.scores, x_aux_indices=np.asarray(aux_sel.indices, dtype=np.int64),
+                x_indices=np.asarray(clip.plan.indices, dtype=np.int64),
+                x_effective_ratio=np.float64(clip.plan.effective_ratio), x_clip_logits=clip.logits,
+                x_n_aux=np.int64(scores.scores.size),
+                x_n_primary=np.int64(sum(len(tp.encode(t)) for t in chunk_ts)))
+
+
 def write_reference_files() -> None:
     """Small .cclp files written by the reference's own save_cache (format v1)."""
     rng = np.random.default_rng(42)
@@ -169,6 +194,8 @@ def main() -> None:
         out = run(w)
         if w is not C1_EXACT:
             out.update(run_cacheblend(w))
+        if w is C1:
+            out.update(run_cross_tokenizer())
         path = os.path.join(HERE, f"{w.name}.npz")
         np.savez_compressed(path, **out)
         print(f"{w.name}: {len(out['indices'])} selected of {out['scores'].size}, "

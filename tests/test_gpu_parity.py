@@ -28,12 +28,12 @@ BF16_KV_RTOL = 2e-2
 BF16_LOGIT_TOL = 5e-2
 
 
-def _cfg(oc: orc.OracleConfig, dtype: str):
+def _cfg(oc: orc.OracleConfig, dtype: str, tokenizer_id: str = "chars"):
     from paper_2510_10129_b200 import ModelConfig
     return ModelConfig(n_layers=oc.n_layers, n_heads=oc.n_heads, d_model=oc.d_model, d_head=oc.d_head,
                        d_ff=oc.d_ff, vocab_size=oc.vocab_size, rope_base=oc.rope_base, norm_eps=oc.norm_eps,
                        activation=oc.activation, mlp_gated=oc.mlp_gated, attn_bias=oc.attn_bias,
-                       mlp_bias=oc.mlp_bias, tokenizer_id="chars", n_kv_heads=oc.kv_heads, dtype=dtype)
+                       mlp_bias=oc.mlp_bias, tokenizer_id=tokenizer_id, n_kv_heads=oc.kv_heads, dtype=dtype)
 
 
 def _bf16_params(p):
@@ -166,6 +166,14 @@ def test_full_prefill_and_ratio_identities(case):
                                  cc.SelectionConfig(1.0))
     assert clip1.plan.indices == tuple(range(w.prefix_len, clip1.cache.layout.total))
     assert np.abs(clip1.logits - full.logits).max() < BF16_LOGIT_TOL * std
+    # the same two edges through the exact-budget (threshold 1, no host sync)
+    # launch: identical results to the synced launch
+    for ratio, ref in ((0.0, clip0), (1.0, clip1)):
+        d = cc.cacheclip_prefill(case.primary, case.aux, chunks, aux_chunks, case.query,
+                                 cc.SelectionConfig(ratio, 8, 1))
+        assert d.plan.indices == ref.plan.indices and d.plan.windows == ref.plan.windows
+        assert d.cache.recomputed_rows == ref.cache.recomputed_rows
+        np.testing.assert_array_equal(d.logits, ref.logits)
     # the CacheClip strategy vs the reference's own first-token logits
     clip = cc.cacheclip_prefill(case.primary, case.aux, chunks, aux_chunks, case.query, case.config)
     assert clip.plan.indices == tuple(int(i) for i in case.g["indices"])
@@ -199,3 +207,31 @@ def test_selection_exact_across_seeds(wname, seed):
     assert sel.indices == o_idx
     assert [(x.start, x.end, x.selected, x.kept, x.partial) for x in sel.windows] == \
         [(x.start, x.end, x.selected, x.kept, x.partial) for x in o_win]
+
+
+def test_cross_tokenizer_prefill_matches_reference():
+    """cacheclip_prefill with different primary / scoring tokenizers
+    (pipeline.py:118-226): chunk texts re-encoded by both, the device
+    selection projected onto primary rows through the character spans
+    (selector.py:217-245). Plan: exact vs the reference's own run; logits:
+    bf16 tolerance."""
+    import paper_2510_10129_b200 as cc
+    from oracle.synth import C1_PRIMARY, X1_AUX, X1_RATIO, X1_WINDOW_THRESHOLD, cross_tokenizer_case
+    g = dict(np.load(os.path.join(GOLDEN, "c1.npz")))
+    pv, av, prefix_t, chunk_ts, query_t = cross_tokenizer_case(0)
+    tp, ta = cc.GreedyTokenizer(pv, "chars"), cc.GreedyTokenizer(av, "chars+merges")
+    primary = cc.from_params(_cfg(C1_PRIMARY, "bf16"), orc.seeded_params(C1_PRIMARY, 0))
+    aux = cc.from_params(_cfg(X1_AUX, "fp32", "chars+merges"), orc.seeded_params(X1_AUX, 1))
+    chunks = [cc.prefill_chunk(primary, tp.encode(prefix_t), tp.encode(t)) for t in chunk_ts]
+    aux_chunks = [cc.prefill_chunk(aux, ta.encode(prefix_t), ta.encode(t)) for t in chunk_ts]
+    cfg = cc.SelectionConfig(X1_RATIO, 8, X1_WINDOW_THRESHOLD)
+    scores = cc.aux_score_tokens(aux, aux_chunks, ta.encode(query_t))
+    np.testing.assert_allclose(scores.scores, g["x_scores"], rtol=1e-5, atol=1e-9)
+    out = cc.cacheclip_prefill(primary, aux, chunks, aux_chunks, query_t, cfg,
+                               primary_tokenizer=tp, aux_tokenizer=ta)
+    assert out.plan.indices == tuple(int(i) for i in g["x_indices"])
+    assert out.plan.effective_ratio == float(g["x_effective_ratio"])
+    assert out.cache.recomputed_rows == out.plan.indices
+    ref = g["x_clip_logits"]
+    assert np.abs(out.logits - ref).max() < BF16_LOGIT_TOL * ref.std()
+    assert out.first_token == int(np.argmax(out.logits))

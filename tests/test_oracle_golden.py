@@ -175,3 +175,39 @@ def test_cacheblend_rejects_prefixed_chunks_and_shallow_models():
         orc.cacheblend(prim, chunks, [7], 0.5)
     with pytest.raises(ValueError):
         orc.cacheblend_select(prim, orc.merge(chunks, 64, w.primary.rope_base), 1.5)
+
+
+def _cross_spans(tok_p, tok_a, chunk_texts):
+    """pipeline.py:118-153: per-chunk spans shifted by the running offset."""
+    p_spans, a_spans, off = [], [], 0
+    for t in chunk_texts:
+        p_spans += [type(s)(s.token_id, s.start + off, s.end + off) for s in tok_p.encode_with_offsets(t)]
+        a_spans += [type(s)(s.token_id, s.start + off, s.end + off) for s in tok_a.encode_with_offsets(t)]
+        off += len(t)
+    return p_spans, a_spans
+
+
+def test_cross_tokenizer_selection_and_projection():
+    """Two tokenizers (selector.py:217-245, tokenizers.py:151-177): the
+    oracle's aux scores / selection and the package's host-side span
+    projection reproduce the reference's own run (tests/golden/c1.npz x_*)."""
+    from oracle.synth import C1_PRIMARY, X1_AUX, X1_RATIO, X1_WINDOW_THRESHOLD, cross_tokenizer_case
+    from paper_2510_10129_b200 import AuxSelection, GreedyTokenizer
+    from paper_2510_10129_b200.selector import map_selection
+
+    g = np.load(os.path.join(GOLDEN, "c1.npz"))
+    pv, av, prefix_t, chunk_ts, query_t = cross_tokenizer_case(0)
+    tp, ta = GreedyTokenizer(pv, "chars"), GreedyTokenizer(av, "chars+merges")
+    aux = orc.OracleModel(X1_AUX, orc.seeded_params(X1_AUX, 1))
+    aux_chunks = [orc.prefill_chunk(aux, ta.encode(prefix_t), ta.encode(t)) for t in chunk_ts]
+    scores = orc.aux_scores(aux, aux_chunks, ta.encode(query_t))
+    np.testing.assert_allclose(scores, g["x_scores"], rtol=1e-6, atol=0)
+    idx, _ = orc.select(scores, [len(ta.encode(t)) for t in chunk_ts], X1_RATIO, 8, X1_WINDOW_THRESHOLD)
+    assert idx == tuple(int(i) for i in g["x_aux_indices"])
+    p_spans, a_spans = _cross_spans(tp, ta, chunk_ts)
+    assert len(a_spans) == int(g["x_n_aux"]) and len(p_spans) == int(g["x_n_primary"])
+    assert len(a_spans) < len(p_spans)  # merges make the aux tokenization shorter
+    plan = map_selection(AuxSelection(idx, (), len(a_spans), X1_RATIO), a_spans, p_spans,
+                         index_offset=len(tp.encode(prefix_t)))
+    assert plan.indices == tuple(int(i) for i in g["x_indices"])
+    assert plan.effective_ratio == float(g["x_effective_ratio"])
