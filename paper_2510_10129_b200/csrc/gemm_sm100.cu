@@ -464,20 +464,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 //   tfull[a] (both CTAs; multicast tcgen05.commit from the leader),
 //   tempty[a] (leader; both CTAs' epilogue warps arrive, the peer remotely)
 // ---------------------------------------------------------------------------
-template <int BN>
+template <int BN, bool kTF32>
 struct Gemm2Cfg {
-  static constexpr int BK = 64;
-  static constexpr int KSTEPS = BK / 16;
-  static constexpr int A_BYTES = 128 * 128;        // own 128 rows x 64 K
-  static constexpr int B_BYTES = (BN / 2) * 128;   // own half of B
+  static constexpr int ELEM = kTF32 ? 4 : 2;
+  static constexpr int BK = 128 / ELEM;            // one 128-byte swizzle row per tile row
+  static constexpr int UK = kTF32 ? 8 : 16;
+  static constexpr int KSTEPS = BK / UK;
+  static constexpr int NSUB = kTF32 ? 2 : 1;       // 3xTF32: hi and lo sub-tiles per stage
+  static constexpr int A_SUB = 128 * 128;          // own 128 rows x one 128-byte K row
+  static constexpr int B_SUB = (BN / 2) * 128;     // own half of B
+  static constexpr int A_BYTES = NSUB * A_SUB;
+  static constexpr int B_BYTES = NSUB * B_SUB;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int FIXED = kEpiWarps * kEpiStageBytes + 1024 + 256;
   static constexpr int FIT = (232448 - FIXED) / STAGE_BYTES;
   static constexpr int STAGES = FIT > 6 ? 6 : FIT;
-  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int ACC_STRIDE = kTF32 ? 2 * BN : BN;  // 3xTF32: hi*hi | corrections
+  static constexpr int TMEM_COLS = 2 * ACC_STRIDE;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
-  static constexpr uint32_t IDESC = umma_idesc(256, BN, false);
-  static_assert(TMEM_COLS <= 512 && SMEM_BYTES <= 232448, "pair GEMM resources");
+  static constexpr uint32_t IDESC = umma_idesc(256, BN, kTF32);
+  static_assert(TMEM_COLS <= 512 && SMEM_BYTES <= 232448 && STAGES >= 2, "pair GEMM resources");
 };
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -505,13 +511,22 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* desc, ui
       "l"(desc), "r"(leader_bar), "r"(x), "r"(y)
       : "memory");
 }
+template <bool kTF32>
 __device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                             uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+  if constexpr (kTF32) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+  }
 }
 __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `bar` in both CTAs
   asm volatile(
@@ -521,11 +536,11 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `b
       : "memory");
 }
 
-template <int BN>
+template <int BN, bool kTF32>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
-                 int num_m2, int num_n, int num_kb) {
-  using Cfg = Gemm2Cfg<BN>;
+                 int num_m2, int num_n, int num_kb, int k_orig) {
+  using Cfg = Gemm2Cfg<BN, kTF32>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* smem_a = smem;
@@ -579,8 +594,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_arrive_expect_tx(&full[stage], 2 * Cfg::STAGE_BYTES);
           const uint32_t lbar = map_to_rank(&full[stage], 0);
-          tma_load_2d_pair(smem_a + stage * Cfg::A_BYTES, &tmA, lbar, kb * Cfg::BK, arow);
-          tma_load_2d_pair(smem_b + stage * Cfg::B_BYTES, &tmB, lbar, kb * Cfg::BK, brow);
+          uint8_t* sa = smem_a + stage * Cfg::A_BYTES;
+          uint8_t* sb = smem_b + stage * Cfg::B_BYTES;
+          tma_load_2d_pair(sa, &tmA, lbar, kb * Cfg::BK, arow);
+          tma_load_2d_pair(sb, &tmB, lbar, kb * Cfg::BK, brow);
+          if constexpr (kTF32) {  // A' = [hi | hi | lo], B' = [hi | lo | hi]
+            tma_load_2d_pair(sa + Cfg::A_SUB, &tmA, lbar, 2 * k_orig + kb * Cfg::BK, arow);
+            tma_load_2d_pair(sb + Cfg::B_SUB, &tmB, lbar, k_orig + kb * Cfg::BK, brow);
+          }
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -597,7 +618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       for (int t = cluster_id; t < tiles; t += n_clusters) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * Cfg::ACC_STRIDE;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full[stage], phase);
           tc_fence_after();
@@ -605,9 +626,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             const uint32_t a0 = smem_u32(smem_a + stage * Cfg::A_BYTES);
             const uint32_t b0 = smem_u32(smem_b + stage * Cfg::B_BYTES);
 #pragma unroll
-            for (int k = 0; k < Cfg::KSTEPS; ++k)
-              tc_mma_pair(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
-                          (kb | k) != 0 ? 1u : 0u);
+            for (int k = 0; k < Cfg::KSTEPS; ++k) {
+              tc_mma_pair<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
+                                 (kb | k) != 0 ? 1u : 0u);
+              if constexpr (kTF32) {  // corrections hi*lo + lo*hi into the second accumulator
+                tc_mma_pair<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + k * 32),
+                                   umma_desc_sw128(b0 + Cfg::B_SUB + k * 32), Cfg::IDESC, (kb | k) != 0 ? 1u : 0u);
+                tc_mma_pair<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + Cfg::A_SUB + k * 32),
+                                   umma_desc_sw128(b0 + k * 32), Cfg::IDESC, 1u);
+              }
+            }
             tc_commit_pair(&empty[stage]);
             if (kb == num_kb - 1) tc_commit_pair(&tfull[acc]);
           }
@@ -636,9 +664,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int mb = t % num_m2, nb = t / num_m2;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(quarter * 32) << 16);
+      const uint32_t tbase = tmem_base + acc * Cfg::ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
       const int64_t row0 = (int64_t)mb * 256 + (int64_t)rank * 128 + quarter * 32;
-      for (int c0 = c_begin; c0 < c_end; c0 += 32) epilogue_chunk<BN, false>(ep, tbase, c0, row0, nb, stg, lane);
+      for (int c0 = c_begin; c0 < c_end; c0 += 32) epilogue_chunk<BN, kTF32>(ep, tbase, c0, row0, nb, stg, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(map_to_rank(&tempty[acc], 0));
@@ -713,26 +741,28 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   return CC_OK;
 }
 
-template <int BN>
-static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, cudaStream_t st) {
-  using Cfg = Gemm2Cfg<BN>;
+template <int BN, bool kTF32>
+static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaStream_t st) {
+  using Cfg = Gemm2Cfg<BN, kTF32>;
   CUtensorMap ta, tb;
-  int rc = make_map(&ta, a->A, false, a->K, a->M, a->lda, Cfg::BK, 128);
+  int rc = make_map(&ta, a->A, kTF32, kop, a->M, a->lda, Cfg::BK, 128);
   if (rc) return rc;
-  rc = make_map(&tb, a->B, false, a->K, a->N, a->ldb, Cfg::BK, BN / 2);
+  rc = make_map(&tb, a->B, kTF32, kop, a->N, a->ldb, Cfg::BK, BN / 2);
   if (rc) return rc;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm2_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+    cudaFuncSetAttribute(gemm2_kernel<BN, kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
     attr_set = true;
   }
   const int num_m2 = (int)((a->M + 255) / 256);
   const int num_n = (int)((a->N + BN - 1) / BN);
-  const int num_kb = (int)((a->K + Cfg::BK - 1) / Cfg::BK);
+  // 3xTF32 iterates the original K (hi/lo sub-tiles per stage)
+  const int num_kb = (int)(((kTF32 ? a->K : kop) + Cfg::BK - 1) / Cfg::BK);
   const int tiles = num_m2 * num_n;
   const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  ProfScope ps(st, OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
-  gemm2_kernel<BN><<<2 * clusters, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m2, num_n, num_kb);
+  ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
+  gemm2_kernel<BN, kTF32><<<2 * clusters, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m2, num_n, num_kb,
+                                                                               (int)a->K);
   CC_LAUNCH_CHECK("gemm (CTA pair)");
   return CC_OK;
 }
@@ -743,6 +773,18 @@ static bool pair_enabled() {
   if (on < 0) {
     const char* e = getenv("CC_GEMM_PAIR");
     on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+// CC_GEMM_PAIR_TF32=1 runs the large 3xTF32 GEMMs on CTA pairs. Off by default:
+// bitwise equal to the single-CTA kernel but measured no faster (C3 scoring
+// GEMMs 11.29 vs 10.98 ms/step), so operand traffic is not what bounds them.
+static bool tf32_pair_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CC_GEMM_PAIR_TF32");
+    on = (e && e[0] == '1') ? 1 : 0;
   }
   return on == 1;
 }
@@ -815,8 +857,11 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   }
   cudaStream_t st = as_stream(stream);
   // 3xTF32 runs 128-wide tiles: two accumulators (hi*hi, corrections) x two buffers fill TMEM
-  if (tf32) return launch<128, true>(a, ep, kop, st);
+  if (tf32) {
+    if (tf32_pair_enabled() && a->M >= 1024 && a->N % 128 == 0) return launch_pair<128, true>(a, ep, kop, st);
+    return launch<128, true>(a, ep, kop, st);
+  }
   // large bf16 GEMMs on CTA pairs: 256-row tiles, half the B traffic per SM
-  if (pair_enabled() && a->M >= 512 && a->N % 256 == 0) return launch_pair<256>(a, ep, st);
+  if (pair_enabled() && a->M >= 512 && a->N % 256 == 0) return launch_pair<256, false>(a, ep, kop, st);
   return wide ? launch<256, false>(a, ep, kop, st) : launch<128, false>(a, ep, kop, st);
 }

@@ -68,6 +68,60 @@ def test_gemm_tf32x3_is_fp32_faithful(M, N, K):
     assert err < 5 * (3 * K / 8) * 2.0 ** -23, (err, err32)
 
 
+_PAIR_SCRIPT = r"""
+import math, sys, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2510_10129_b200 import _lib as L, runtime
+L.load()
+DEV = "cuda"
+M, K = 2048, 896
+for epi in ("store", "glu", "residual"):
+    N = 2 * 1024 if epi == "glu" else 1152
+    n_out = N // 2 if epi == "glu" else N
+    g = torch.Generator(device=DEV).manual_seed(11)
+    a = torch.randn(M, K, device=DEV, generator=g)
+    b = torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)
+    A = torch.empty(M, 3 * K, device=DEV)
+    B = torch.empty(N, 3 * K, device=DEV)
+    s = torch.cuda.current_stream().cuda_stream
+    L.call("cc_convert_matrix", a.data_ptr(), M, K, A.data_ptr(), L.CC_F32_SPLIT3, 0, s)
+    L.call("cc_convert_matrix", b.data_ptr(), N, K, B.data_ptr(), L.CC_F32_SPLIT3, 1, s)
+    h0 = torch.randn(M, n_out, device=DEV, generator=g)
+
+    def run(r0, r1):
+        C = h0[r0:r1].clone()
+        kw = dict(C=C, ldc=n_out, c_mode=L.CC_F32)
+        e = {"store": L.CC_EPI_STORE, "residual": L.CC_EPI_RESIDUAL, "glu": L.CC_EPI_GLU}[epi]
+        if epi == "glu":
+            kw.update(act=L.CC_ACT_SILU, n_out=n_out)
+        runtime.gemm(L.CC_GEMM_TF32X3, e, r1 - r0, N, K, A[r0:r1], B, **kw)
+        return C
+
+    whole = run(0, M)                                           # CTA-pair kernel (M >= 1024)
+    blocks = torch.cat([run(r, r + 512) for r in range(0, M, 512)])  # single-CTA kernel
+    torch.cuda.synchronize()
+    assert torch.equal(whole, blocks), epi
+print("pair == single")
+"""
+
+
+def test_gemm_tf32x3_pair_bitwise_equals_single_cta():
+    """With CC_GEMM_PAIR_TF32=1, M >= 1024 runs the 3xTF32 GEMM on CTA pairs
+    (cta_group::2; off by default, measured no faster). Every output element
+    accumulates the same MMAs in the same order as the single-CTA kernel, so
+    the pair result must equal the stacked 512-row blocks bitwise (store,
+    GLU and residual epilogues). The env var is read once per process: the
+    check runs in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CC_GEMM_PAIR_TF32="1")
+    r = subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "pair == single" in r.stdout, r.stderr[-2000:]
+
+
 def test_gemm_residual_and_glu():
     from paper_2510_10129_b200 import _lib as L
     from paper_2510_10129_b200.weights import _interleave_glu, _interleave_bias
