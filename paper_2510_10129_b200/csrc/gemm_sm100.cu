@@ -53,6 +53,8 @@ struct GemmCfg {
   static_assert(TMEM_COLS <= 512, "TMEM holds 512 columns");
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + FIXED;
   static constexpr uint32_t IDESC = umma_idesc(kBM, BN, kTF32);
+  static constexpr uint32_t IDESC2 = umma_idesc(kBM, 2 * BN, kTF32);  // 3xTF32: [B_hi; B_lo] in one MMA
+  static_assert(!kTF32 || 2 * BN <= 256, "3xTF32 fused hi*[hi;lo] MMA needs N = 2*BN <= 256");
   static_assert(STAGES >= 2, "GEMM pipeline needs two stages");
   static_assert(SMEM_BYTES <= 232448, "GEMM shared memory over the sm_100 per-CTA limit");
 };
@@ -394,13 +396,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t b0 = smem_u32(smem_b + stage * Cfg::B_BYTES);
 #pragma unroll
           for (int k = 0; k < Cfg::KSTEPS; ++k) {
-            tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
-                          (kb | k) != 0 ? 1u : 0u);
-            if constexpr (kTF32) {  // corrections hi*lo + lo*hi into the second accumulator
-              tc_mma<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + Cfg::B_SUB + k * 32),
-                            Cfg::IDESC, (kb | k) != 0 ? 1u : 0u);
+            if constexpr (kTF32) {
+              // hi*hi and hi*lo as ONE N = 2*BN MMA: B_hi and B_lo are adjacent
+              // 128-byte-row sub-tiles (one 2*BN-row operand) and the two
+              // accumulators adjacent TMEM columns, so A_hi is read once; then
+              // lo*hi into the correction accumulator
+              tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC2,
+                            (kb | k) != 0 ? 1u : 0u);
               tc_mma<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + Cfg::A_SUB + k * 32), umma_desc_sw128(b0 + k * 32),
                             Cfg::IDESC, 1u);
+            } else {
+              tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
+                            (kb | k) != 0 ? 1u : 0u);
             }
           }
           tc_commit(&empty[stage]);
@@ -629,7 +636,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
             for (int k = 0; k < Cfg::KSTEPS; ++k) {
               tc_mma_pair<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
                                  (kb | k) != 0 ? 1u : 0u);
-              if constexpr (kTF32) {  // corrections hi*lo + lo*hi into the second accumulator
+              if constexpr (kTF32) {  // corrections hi*lo + lo*hi into the second accumulator (each CTA holds
+                                      // half of B_hi and of B_lo, so hi*[hi;lo] cannot be one N=2*BN MMA here)
                 tc_mma_pair<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + k * 32),
                                    umma_desc_sw128(b0 + Cfg::B_SUB + k * 32), Cfg::IDESC, (kb | k) != 0 ? 1u : 0u);
                 tc_mma_pair<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + Cfg::A_SUB + k * 32),
