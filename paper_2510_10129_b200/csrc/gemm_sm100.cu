@@ -867,6 +867,10 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   // 3xTF32 runs 128-wide tiles: two accumulators (hi*hi, corrections) x two buffers fill TMEM
   if (tf32) {
     if (tf32_pair_enabled() && a->M >= 1024 && a->N % 128 == 0) return launch_pair<128, true>(a, ep, kop, st);
+    // small-M scoring GEMMs (few chunks): 64-wide tiles double the CTAs when
+    // 128-wide tiles would leave over half the SMs idle (GLU tiles need >= 128)
+    const int64_t t128 = ((a->M + kBM - 1) / kBM) * ((a->N + 127) / 128);
+    if (a->epilogue != CC_EPI_GLU && 2 * t128 <= num_sms()) return launch<64, true>(a, ep, kop, st);
     return launch<128, true>(a, ep, kop, st);
   }
   // large bf16 GEMMs on CTA pairs: 256-row tiles, half the B traffic per SM

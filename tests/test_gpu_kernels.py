@@ -122,6 +122,31 @@ def test_gemm_tf32x3_pair_bitwise_equals_single_cta():
     assert r.returncode == 0 and "pair == single" in r.stdout, r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("epi", ["store", "residual"])
+def test_gemm_tf32x3_narrow_tiles_bitwise_equal(epi):
+    """Small-M 3xTF32 GEMMs (128-wide tiles would leave half the SMs idle) run
+    64-wide tiles; per element the same MMAs accumulate in the same order, so
+    rows of an M=512 GEMM (64-wide) equal the same rows of an M=2048 GEMM
+    (128-wide) bitwise."""
+    from paper_2510_10129_b200 import _lib as L
+    M, N, K = 2048, 1152, 896
+    g = torch.Generator(device=DEV).manual_seed(5)
+    a = torch.randn(M, K, device=DEV, generator=g)
+    b = torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)
+    A = torch.empty(M, 3 * K, device=DEV)
+    B = torch.empty(N, 3 * K, device=DEV)
+    s = torch.cuda.current_stream().cuda_stream
+    L.call("cc_convert_matrix", a.data_ptr(), M, K, A.data_ptr(), L.CC_F32_SPLIT3, 0, s)
+    L.call("cc_convert_matrix", b.data_ptr(), N, K, B.data_ptr(), L.CC_F32_SPLIT3, 1, s)
+    h0 = torch.randn(M, N, device=DEV, generator=g)
+    e = L.CC_EPI_STORE if epi == "store" else L.CC_EPI_RESIDUAL
+    wide = h0.clone()
+    _gemm(L.CC_GEMM_TF32X3, e, A, B, C=wide, ldc=N, c_mode=L.CC_F32)
+    narrow = h0[:512].clone()
+    _gemm(L.CC_GEMM_TF32X3, e, A[:512], B, C=narrow, ldc=N, c_mode=L.CC_F32)
+    assert torch.equal(wide[:512], narrow)
+
+
 def test_gemm_residual_and_glu():
     from paper_2510_10129_b200 import _lib as L
     from paper_2510_10129_b200.weights import _interleave_glu, _interleave_bias
