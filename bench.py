@@ -454,15 +454,21 @@ def run_ours(args, rank: int, world: int):
     # ---- end to end through the public API from host-resident caches -------
     e2e = None
     if not args.skip_e2e:
-        host_p = [(c.k.cpu().pin_memory(), c.v.cpu().pin_memory(), c.token_ids, c.prefix_len) for c in chunks]
-        host_a = [(c.k.cpu().pin_memory(), c.v.cpu().pin_memory(), c.token_ids, c.prefix_len) for c in aux_chunks]
-        h2d = sum(k.numel() * k.element_size() * 2 for k, *_ in host_p + host_a) + 8 * len(query)
+        # host-resident chunk caches, as the reference holds them in memory:
+        # a layer-major pinned HostCachePool per model (the request's chunks
+        # in consecutive slots); the pipeline streams them in with the copy
+        # engines, scoring caches first, primary caches under the scoring pass
+        def to_pool(caches):
+            L, _, H, D = caches[0].k.shape
+            pool = cc.HostCachePool(len(caches), max(c.n_rows for c in caches), L, H, D, caches[0].k.dtype)
+            return [pool.store(c) for c in caches]
 
-        # host-resident (pinned) chunk caches, as the reference holds them in
-        # memory; the pipeline uploads them (primary overlapped with scoring)
-        pc = [cc.ChunkCache(k, v, ids, pl, primary.config.tokenizer_id, primary.fingerprint)
-              for k, v, ids, pl in host_p]
-        ac = [cc.ChunkCache(k, v, ids, pl, aux.config.tokenizer_id, aux.fingerprint) for k, v, ids, pl in host_a]
+        pc, ac = to_pool(chunks), to_pool(aux_chunks)
+        row_b = lambda c: c.k.shape[2] * c.k.shape[3] * c.k.element_size() * c.n_layers * 2  # noqa: E731  K+V
+        # bytes actually moved: the primary's shared prefix once (the merge
+        # dedups it), every scoring cache whole, the query ids
+        h2d = (row_b(pc[0]) * (pc[0].prefix_len + sum(c.chunk_len for c in pc))
+               + sum(row_b(c) * c.n_rows for c in ac) + 8 * len(query))
 
         def e2e_step():
             o = cc.cacheclip_prefill(primary, aux, pc, ac, list(query), config)

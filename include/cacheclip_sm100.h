@@ -115,6 +115,15 @@ int cc_upload(void* dst_dev, const void* src_pinned, int64_t bytes, void* stream
 int cc_h2d_segments(const cc_kv_segment* segs_host, int32_t n_segs, int32_t layer0, int32_t n_layers,
                     int32_t kv_heads, int32_t head_dim, int32_t dtype, void* dst_k, void* dst_v,
                     int64_t dst_rows_cap, void* stream);
+/* Same transfer for a run of chunks stored at a constant host stride (slots of
+ * a layer-major HostCachePool) that land back to back: one cudaMemcpy2DAsync
+ * per (layer, K|V) moves `width` bytes of every chunk (rows = chunks, source
+ * pitch src_chunk_pitch, destination pitch dst_chunk_pitch), layers
+ * [layer0, layer0 + n_layers) at the given layer pitches. All sizes in bytes;
+ * src pointers are pinned host, dst device. */
+int cc_h2d_uniform(const void* src_k, const void* src_v, int64_t src_chunk_pitch, int64_t src_layer_pitch,
+                   void* dst_k, void* dst_v, int64_t width, int64_t dst_layer_pitch, int64_t dst_chunk_pitch,
+                   int32_t n_chunks, int32_t layer0, int32_t n_layers, void* stream);
 /* Rotation half: rotate the keys of rows [0, n_rows) in place over n_layers
  * layers (k points at the first layer; layer stride rows_cap rows); row r of
  * the segment containing it (by dst_row0) sits at position pos0 + r - dst_row0.

@@ -14,7 +14,7 @@ from .errors import (BadMagicError, CacheConsistencyError, CacheFormatError, Che
                      UnknownCharacterError, VersionMismatchError, VocabFormatError, WeightFormatError)
 from .flops import (STAGES, FlopReport, PipelineTrace, count_flops, event_macs, extend_macs,
                     full_prefill_macs)
-from .kv_store import ChunkCache, MergedCache, MergeLayout, compute_positions, merge_caches
+from .kv_store import ChunkCache, HostCachePool, MergedCache, MergeLayout, compute_positions, merge_caches
 from .model import (LayerCache, PrefillResult, decode_step, extend_cache, peek_forward, prefill_chunk, prefill_chunks,
                     prefill_full, selective_forward, visible_pairs)
 from .persist import CACHE_MAGIC, CACHE_VERSION, CACHE_VERSION_BF16, load_cache, save_cache

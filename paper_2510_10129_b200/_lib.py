@@ -89,6 +89,7 @@ _SIGS = {
     "cc_assemble_kv": ([vp, i32, i64, i32, i32, i32, i32, vp, i64, vp, vp, i64, vp], i32),
     "cc_assemble_kv_capped": ([vp, i32, i64, i32, i32, i32, i32, vp, i64, vp, vp, i64, i32, vp], i32),
     "cc_upload": ([vp, vp, i64, vp], i32),
+    "cc_h2d_uniform": ([vp, vp, i64, i64, vp, vp, i64, i64, i64, i32, i32, i32, vp], i32),
     "cc_h2d_segments": ([vp, i32, i32, i32, i32, i32, i32, vp, vp, i64, vp], i32),
     "cc_rope_rows_inplace": ([vp, i32, i64, i32, i32, i32, i32, vp, vp, i64, vp], i32),
     "cc_rope_table": ([vp, i64, vp, i32, vp, vp, vp], i32),

@@ -651,6 +651,28 @@ int cc_h2d_segments(const cc_kv_segment* segs_host, int32_t n_segs, int32_t laye
   return CC_OK;
 }
 
+int cc_h2d_uniform(const void* src_k, const void* src_v, int64_t src_chunk_pitch, int64_t src_layer_pitch,
+                   void* dst_k, void* dst_v, int64_t width, int64_t dst_layer_pitch, int64_t dst_chunk_pitch,
+                   int32_t n_chunks, int32_t layer0, int32_t n_layers, void* stream) {
+  CC_CHECK_ARG(src_k && src_v && dst_k && dst_v, CC_ERR_VALUE, "null pointer");
+  CC_CHECK_ARG(n_chunks > 0 && layer0 >= 0 && n_layers > 0 && width > 0, CC_ERR_DIMENSION, "bad geometry");
+  CC_CHECK_ARG(src_chunk_pitch >= width && dst_chunk_pitch >= width, CC_ERR_DIMENSION,
+               "chunk pitch smaller than the copied rows");
+  cudaStream_t st = as_stream(stream);
+  for (int l = layer0; l < layer0 + n_layers; ++l) {
+    const void* srcs[2] = {src_k, src_v};
+    void* dsts[2] = {dst_k, dst_v};
+    for (int t = 0; t < 2; ++t) {
+      cudaError_t e = cudaMemcpy2DAsync(static_cast<uint8_t*>(dsts[t]) + (size_t)l * dst_layer_pitch,
+                                        dst_chunk_pitch,
+                                        static_cast<const uint8_t*>(srcs[t]) + (size_t)l * src_layer_pitch,
+                                        src_chunk_pitch, width, n_chunks, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return fail(CC_ERR_CUDA, "cudaMemcpy2DAsync (layer %d): %s", l, cudaGetErrorString(e));
+    }
+  }
+  return CC_OK;
+}
+
 int cc_rope_rows_inplace(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_rows, int32_t n_layers,
                          int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host, void* k,
                          int64_t rows_cap, void* stream) {

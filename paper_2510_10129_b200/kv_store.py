@@ -107,6 +107,16 @@ def _as_layers(x, device=None) -> torch.Tensor:
     raise CacheConsistencyError("cache needs matching per-layer key/value lists")
 
 
+def _rows_contiguous(t: torch.Tensor) -> bool:
+    """[L, rows, H, D] with each layer's rows contiguous (any layer stride)."""
+    L, R, H, D = t.shape
+    return t.stride(3) == 1 and t.stride(2) == D and t.stride(1) == H * D and (L == 1 or t.stride(0) >= R * H * D)
+
+
+def _layer_stride_rows(t: torch.Tensor) -> int:
+    return t.stride(0) // (t.shape[2] * t.shape[3]) if t.shape[0] > 1 else t.shape[1]
+
+
 class ChunkCache:
     """One chunk processed against the shared prefix, keys position-free."""
 
@@ -120,7 +130,12 @@ class ChunkCache:
             raise CacheConsistencyError(f"layer shape {tuple(v.shape)} != {tuple(k.shape)}")
         if k.dtype not in (torch.float32, torch.bfloat16) or v.dtype != k.dtype:
             raise CacheConsistencyError(f"cache tensors must be float32 or bfloat16, got {k.dtype}")
-        self.k, self.v = k.contiguous(), v.contiguous()
+        # pinned host views into a layer-major HostCachePool keep their layer
+        # stride (the streaming copies read each layer through it); anything
+        # else is stored contiguous
+        pool_view = (not k.is_cuda and k.is_pinned() and v.is_pinned() and _rows_contiguous(k)
+                     and v.stride() == k.stride())
+        self.k, self.v = (k, v) if pool_view else (k.contiguous(), v.contiguous())
         self.token_ids = list(int(t) for t in token_ids)
         self.prefix_len = int(prefix_len)
         self.tokenizer_id = tokenizer_id
@@ -179,12 +194,13 @@ def _dtype_code(dt: torch.dtype) -> int:
 
 
 def _segments(spec) -> np.ndarray:
-    """[(chunk, src_row0, dst_row0, n_rows)] -> packed cc_kv_segment bytes."""
+    """[(chunk, src_row0, dst_row0, n_rows)] -> packed cc_kv_segment bytes
+    (src_rows = the chunk tensors' layer stride in rows)."""
     arr = np.empty((len(spec), 7), dtype=np.int64)  # == cc_kv_segment (7 x 8 bytes)
     for i, item in enumerate(spec):
         c, s0, d0, n = item[:4]
         pos0 = item[4] if len(item) > 4 else d0  # RoPE position of the first row
-        arr[i] = (c.k.data_ptr(), c.v.data_ptr(), c.n_rows, s0, d0, n, pos0)
+        arr[i] = (c.k.data_ptr(), c.v.data_ptr(), _layer_stride_rows(c.k), s0, d0, n, pos0)
     return arr.view(np.uint8).reshape(-1)
 
 
@@ -365,21 +381,62 @@ def _copy_stream(dev: torch.device) -> torch.cuda.Stream:
     return _copy_streams[key]
 
 
+_MAX_PITCH = 1 << 30  # cudaMemcpy2DAsync rejects larger row pitches
+
+
+def _same_storage(a, b) -> bool:
+    """One 2-D copy must stay inside one host allocation (a pool tensor)."""
+    try:
+        return a.untyped_storage().data_ptr() == b.untyped_storage().data_ptr()
+    except AttributeError:  # pointer stand-ins in host-logic tests
+        return True
+
+
+def _uniform_runs(spec, row_bytes: int) -> list[tuple[int, int]]:
+    """Split spec into runs [i, j) whose chunks sit at a constant host stride
+    inside one allocation (HostCachePool slots), copy the same rows (s0, n)
+    and land back to back: a run moves as one 2-D copy per (layer, K|V)."""
+    runs, i = [], 0
+    while i < len(spec):
+        j = i + 1
+        c0, s0, d0, n = spec[i][:4]
+        if j < len(spec):
+            step = spec[j][0].k.data_ptr() - c0.k.data_ptr()
+            while j < len(spec):
+                c, s, d, m = spec[j][:4]
+                prev = spec[j - 1][0]
+                if (s != s0 or m != n or d != d0 + (j - i) * n or c.k.stride() != c0.k.stride()
+                        or not (_same_storage(c.k, c0.k) and _same_storage(c.v, c0.v))
+                        or c.k.data_ptr() - prev.k.data_ptr() != step
+                        or c.v.data_ptr() - prev.v.data_ptr() != step or not n * row_bytes <= step <= _MAX_PITCH):
+                    break
+                j += 1
+        runs.append((i, j))
+        i = j
+    return runs
+
+
 def _stream_in(spec, rot: np.ndarray, n_rows: int, k_store: torch.Tensor, v_store: torch.Tensor,
                rope: RopeParams, groups: dict) -> list:
     """Host-resident (pinned) chunk caches -> k_store / v_store
     ([L][cap][H][D]): per layer group, the copy engines DMA every segment's
-    rows (cc_h2d_segments, on a dedicated copy stream, so no SM is spent on the
-    transfer), then the current stream rotates the group's keys in place
-    (cc_rope_rows_inplace, segments ``rot`` give each row's position). Returns
-    one event per layer, recorded on the current stream after its rotation."""
+    rows on a dedicated copy stream (no SM is spent on the transfer) — runs of
+    chunks stored at a constant stride (HostCachePool slots) as one 2-D copy
+    per (layer, K|V) (cc_h2d_uniform), other chunks one 2-D copy per
+    (chunk, K|V) over the group's layers (cc_h2d_segments) — then the current
+    stream rotates the group's keys in place (cc_rope_rows_inplace, segments
+    ``rot`` give each row's position). Returns one event per layer, recorded
+    on the current stream after its rotation."""
     for i, item in enumerate(spec):
         c = item[0]
         if not (c.k.is_pinned() and c.v.is_pinned()):
             raise CacheConsistencyError(f"chunk {i}: host caches must be in pinned memory")
     L, cap, H, D = k_store.shape
     dt = _dtype_code(k_store.dtype)
-    host_segs = np.ascontiguousarray(_segments(spec))
+    row_bytes = H * D * k_store.element_size()
+    runs = _uniform_runs(spec, row_bytes)
+    singles = [spec[i] for i, j in runs if j - i == 1]
+    host_segs = np.ascontiguousarray(_segments(singles)) if singles else None
     rot_dev = host_to_device(rot, k_store.device)
     cur = torch.cuda.current_stream()
     cp = _copy_stream(k_store.device)
@@ -387,11 +444,20 @@ def _stream_in(spec, rot: np.ndarray, n_rows: int, k_store: torch.Tensor, v_stor
     k_store.record_stream(cp)
     v_store.record_stream(cp)
     inv = rope.inv_freq
-    row_bytes = H * D * k_store.element_size()
     ready = []
     for l0, l1 in _layer_groups(L, **groups):
-        _lib.call("cc_h2d_segments", host_segs.ctypes.data, len(spec), l0, l1 - l0, H, D, dt, k_store.data_ptr(),
-                  v_store.data_ptr(), cap, cp.cuda_stream)
+        if singles:
+            _lib.call("cc_h2d_segments", host_segs.ctypes.data, len(singles), l0, l1 - l0, H, D, dt,
+                      k_store.data_ptr(), v_store.data_ptr(), cap, cp.cuda_stream)
+        for i, j in runs:
+            if j - i == 1:
+                continue
+            c, s0, d0, n = spec[i][:4]
+            step = spec[i + 1][0].k.data_ptr() - c.k.data_ptr()
+            lstride = c.k.stride(0) * c.k.element_size()
+            _lib.call("cc_h2d_uniform", c.k.data_ptr() + s0 * row_bytes, c.v.data_ptr() + s0 * row_bytes, step,
+                      lstride, k_store.data_ptr() + d0 * row_bytes, v_store.data_ptr() + d0 * row_bytes,
+                      n * row_bytes, cap * row_bytes, n * row_bytes, j - i, l0, l1 - l0, cp.cuda_stream)
         copied = torch.cuda.Event()
         copied.record(cp)
         cur.wait_event(copied)
@@ -401,6 +467,44 @@ def _stream_in(spec, rot: np.ndarray, n_rows: int, k_store: torch.Tensor, v_stor
         ev.record(cur)
         ready.extend([ev] * (l1 - l0))
     return ready
+
+
+class HostCachePool:
+    """Pinned host storage for chunk caches, LAYER-MAJOR across slots:
+    ``k``, ``v`` = [layers][slots][rows_max][kv_heads][head_dim]. A chunk
+    stored in slot s is the view k[:, s, :rows] (a ChunkCache like any other).
+    The caches of chunks in consecutive slots form one pitched region per
+    layer, so streaming a request's caches to the GPU (merge_caches /
+    aux_score_tokens with host caches) costs one 2-D DMA per (layer, K|V)
+    instead of one copy per chunk: fewer, larger copies keep PCIe at full
+    rate (each copy has a fixed ~4 us cost on the DMA engine)."""
+
+    def __init__(self, n_slots: int, rows_max: int, n_layers: int, kv_heads: int, head_dim: int,
+                 dtype: torch.dtype = torch.bfloat16) -> None:
+        if min(n_slots, rows_max, n_layers, kv_heads, head_dim) <= 0:
+            raise ValueError("pool dimensions must be positive")
+        shape = (n_layers, n_slots, rows_max, kv_heads, head_dim)
+        self.k = torch.empty(shape, dtype=dtype, pin_memory=True)
+        self.v = torch.empty(shape, dtype=dtype, pin_memory=True)
+        self.n_slots, self.rows_max = n_slots, rows_max
+        self._next = 0
+
+    def store(self, cache: ChunkCache, slot: int | None = None) -> ChunkCache:
+        """Copy `cache` into `slot` (default: the next free one); returns the
+        pool-resident ChunkCache (same ids, prefix, tokenizer, fingerprint)."""
+        slot = self._next if slot is None else int(slot)
+        if not 0 <= slot < self.n_slots:
+            raise ValueError(f"slot {slot} outside 0..{self.n_slots - 1}")
+        L, R, H, D = cache.k.shape
+        if (L, H, D) != (self.k.shape[0], self.k.shape[3], self.k.shape[4]) or cache.k.dtype != self.k.dtype:
+            raise CacheConsistencyError("chunk cache geometry does not match the pool")
+        if R > self.rows_max:
+            raise CacheConsistencyError(f"{R} rows exceed the pool's {self.rows_max} rows per slot")
+        k, v = self.k[:, slot, :R], self.v[:, slot, :R]
+        k.copy_(cache.k)
+        v.copy_(cache.v)
+        self._next = max(self._next, slot + 1)
+        return ChunkCache(k, v, cache.token_ids, cache.prefix_len, cache.tokenizer_id, cache.model_fingerprint)
 
 
 def stream_local_banks(chunks: Sequence[ChunkCache], rope: RopeParams, device):

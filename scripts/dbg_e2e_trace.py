@@ -25,7 +25,15 @@ pc = [cc.ChunkCache(c.k.cpu().pin_memory(), c.v.cpu().pin_memory(), c.token_ids,
 ac = [cc.ChunkCache(c.k.cpu().pin_memory(), c.v.cpu().pin_memory(), c.token_ids, c.prefix_len,
                     aux.config.tokenizer_id, aux.fingerprint) for c in aux_chunks]
 mode = sys.argv[1] if len(sys.argv) > 1 else "host"
-args = (pc, ac) if mode == "host" else (chunks, aux_chunks)
+
+
+def to_pool(caches):
+    L, _, H, D = caches[0].k.shape
+    pool = cc.HostCachePool(len(caches), max(c.n_rows for c in caches), L, H, D, caches[0].k.dtype)
+    return [pool.store(c) for c in caches]
+
+
+args = {"host": (pc, ac), "device": (chunks, aux_chunks)}.get(mode) or (to_pool(chunks), to_pool(aux_chunks))
 for _ in range(3):
     cc.cacheclip_prefill(primary, aux, *args, query, config)
 torch.cuda.synchronize()

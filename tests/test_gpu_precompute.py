@@ -106,3 +106,43 @@ def test_host_pinned_caches_equal_device_caches():
     banks = stream_local_banks([host(c, aux) for c in ac], aux.config.rope, aux.device)
     s_host = cc.aux_score_tokens(aux, [host(c, aux) for c in ac], query, _banks=banks).scores
     assert np.array_equal(s_dev, s_host)
+
+
+@pytest.mark.parametrize("lens", [(64, 64, 64, 64, 64), (96, 40, 130, 7, 40, 40)])
+def test_host_cache_pool_equals_device_caches(lens):
+    """Chunk caches in a layer-major pinned HostCachePool (runs of same-length
+    chunks in consecutive slots stream as one 2-D DMA per layer; ragged ones
+    per chunk) give bit-identical merged caches, scores, selection and logits
+    to device-resident caches."""
+    import paper_2510_10129_b200 as cc
+    from paper_2510_10129_b200.kv_store import _uniform_runs
+    primary = _model("bf16", 64, 4, 2, 256)
+    aux = _model("fp32", 64, 2, 2, 128)
+    rng = np.random.default_rng(9)
+    prefix = rng.integers(0, 512, 16).tolist()
+    chunks_ids = [rng.integers(0, 512, n).tolist() for n in lens]
+    query = rng.integers(0, 512, 12).tolist()
+    cfg = cc.SelectionConfig(0.3, 8, 1)
+    pc = cc.prefill_chunks(primary, prefix, chunks_ids)
+    ac = cc.prefill_chunks(aux, prefix, chunks_ids)
+    rows = max(c.n_rows for c in pc)
+    ppool = cc.HostCachePool(len(pc), rows, 2, 2, 64, torch.bfloat16)
+    apool = cc.HostCachePool(len(ac), rows, 2, 2, 64, torch.float32)
+    hp = [ppool.store(c) for c in pc]
+    ha = [apool.store(c) for c in ac]
+    assert all(c.k.is_pinned() and not c.k.is_contiguous() for c in hp)
+    if len(set(lens)) == 1:  # body rows of chunks 1.. are one run; the scoring banks one run
+        rb = 2 * 64 * 2
+        spec = [(c, 0 if i == 0 else 16, 0, c.n_rows if i == 0 else c.chunk_len) for i, c in enumerate(hp)]
+        spec = [(c, s0, sum(x[3] for x in spec[:i]), n) for i, (c, s0, _, n) in enumerate(spec)]
+        assert _uniform_runs(spec, rb) == [(0, 1), (1, len(hp))]
+    a = cc.merge_caches(pc, primary.config.rope, capacity=1000)
+    b = cc.merge_caches(hp, primary.config.rope, capacity=1000, device=primary.device)
+    torch.cuda.synchronize()
+    assert torch.equal(a.k_store[:, :a.n_rows], b.k_store[:, :b.n_rows])
+    assert torch.equal(a.v_store[:, :a.n_rows], b.v_store[:, :b.n_rows])
+    dev_out = cc.cacheclip_prefill(primary, aux, pc, ac, query, cfg)
+    host_out = cc.cacheclip_prefill(primary, aux, hp, ha, query, cfg)
+    torch.cuda.synchronize()
+    assert host_out.plan == dev_out.plan
+    assert np.array_equal(host_out.logits, dev_out.logits)

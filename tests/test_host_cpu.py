@@ -138,3 +138,42 @@ def test_streamed_layer_groups_cover_every_layer_once():
             assert all(a[1] == b[0] and a[0] < a[1] for a, b in zip(g, g[1:]))
     assert [l1 - l0 for l0, l1 in _layer_groups(24, **SCORING_GROUPS)] == [1, 2, 3, 6, 6, 4, 2]
     assert [l1 - l0 for l0, l1 in _layer_groups(28, **PRIMARY_GROUPS)] == [1, 3, 6, 8, 8, 2]
+
+
+def test_uniform_runs_detects_pool_slots():
+    """Chunks at a constant stride inside one allocation (HostCachePool slots)
+    with the same rows copied and back-to-back destinations form one run;
+    anything else breaks it (host logic only: tensors stand in for the pinned
+    pool views, which need a GPU to allocate)."""
+    from types import SimpleNamespace
+
+    import torch
+    from paper_2510_10129_b200.kv_store import _uniform_runs
+    pool = torch.zeros(2, 5, 12, 2, 4)  # [L][slots][rows_max][H][D]
+
+    def cc(slot, rows, t=pool):
+        return SimpleNamespace(k=t[:, slot, :rows], v=t[:, slot, :rows])
+
+    rb = 2 * 4 * 4
+    c = [cc(s, 10) for s in range(5)]
+    spec = [(c[0], 0, 0, 10)] + [(c[i], 2, 10 + 8 * (i - 1), 8) for i in range(1, 5)]
+    assert _uniform_runs(spec, rb) == [(0, 1), (1, 5)]
+    spec[3] = (c[3], 2, 10 + 8 * 2 + 1, 8)  # destination gap before and after chunk 3
+    assert _uniform_runs(spec, rb) == [(0, 1), (1, 3), (3, 4), (4, 5)]
+    class _Ptr:  # pointer/stride stand-in: slots 2^31 B apart, beyond the 2-D copy pitch limit
+        def __init__(self, p):
+            self.p = p
+
+        def data_ptr(self):
+            return self.p
+
+        def stride(self):
+            return (640, 32, 4, 1)
+
+    far = [SimpleNamespace(k=_Ptr(i << 31), v=_Ptr((i << 31) + 4096)) for i in range(3)]
+    assert _uniform_runs([(far[i], 2, 8 * i, 8) for i in range(3)], rb) == [(0, 1), (1, 2), (2, 3)]
+    # separately allocated caches never form a run, even at a constant stride
+    sep = [SimpleNamespace(k=torch.zeros(2, 10, 2, 4), v=torch.zeros(2, 10, 2, 4)) for _ in range(3)]
+    assert _uniform_runs([(sep[i], 2, 8 * i, 8) for i in range(3)], rb) == [(0, 1), (1, 2), (2, 3)]
+    rag = [(cc(0, 10), 0, 0, 10), (cc(1, 7), 2, 10, 5), (cc(2, 10), 2, 15, 8)]
+    assert _uniform_runs(rag, rb) == [(0, 1), (1, 2), (2, 3)]
