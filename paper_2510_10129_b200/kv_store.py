@@ -14,6 +14,7 @@ with spare row capacity so the query rows of extend_cache append in place.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 from typing import Sequence
 
@@ -65,6 +66,7 @@ class _PinnedRing:
 
 
 _ring: _PinnedRing | None = None
+_ring_lock = threading.Lock()
 
 
 def host_to_device(data: np.ndarray, device) -> torch.Tensor:
@@ -81,14 +83,15 @@ def host_to_device(data: np.ndarray, device) -> torch.Tensor:
     n = arr.nbytes
     if n > _PinnedRing.SIZE // 4:
         return t.pin_memory().to(device, non_blocking=True)
-    if _ring is None:
-        _ring = _PinnedRing()
-    off = _ring.alloc(n)
-    _ring.np[off:off + n] = arr.reshape(-1).view(np.uint8)
     out = torch.empty((n + 15) & ~15, dtype=torch.uint8, device=device)
-    with torch.cuda.device(out.device):
-        _lib.call("cc_upload", out.data_ptr(), _ring.ptr + off, n, _stream())
-        _ring.release(off, n)
+    with _ring_lock:  # one ring per process, shared by host threads (e.g. thread-per-rank tests)
+        if _ring is None:
+            _ring = _PinnedRing()
+        off = _ring.alloc(n)
+        _ring.np[off:off + n] = arr.reshape(-1).view(np.uint8)
+        with torch.cuda.device(out.device):
+            _lib.call("cc_upload", out.data_ptr(), _ring.ptr + off, n, _stream())
+            _ring.release(off, n)
     return out[:n].view(t.dtype).view(t.shape)
 
 
