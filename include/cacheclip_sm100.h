@@ -206,20 +206,22 @@ int cc_sparse_row_attention_ranged(const void* q, int64_t ldq, const int64_t* po
 /* Split-KV partial attention for sequence-sharded caches:
  * same kernel, but row i attends local keys [0, limits[i]] (limits = local
  * index of its last visible key, -1 = none; cc_local_limits) and writes the
- * locally normalised context o_part[i][Hq][D] (fp32) plus its log2-domain
- * log-sum-exp lse[i][Hq] (-inf when no key is visible). */
+ * locally normalised context o_part[i][Hq][D] (part_dtype CC_F32 or CC_BF16:
+ * bf16 halves the all_to_all and merge bytes) plus its log2-domain
+ * log-sum-exp lse[i][Hq] (fp32, -inf when no key is visible). */
 int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const int64_t* limits, int64_t m,
                                     const void* k_cache, const void* v_cache, int64_t n_keys,
                                     int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim,
-                                    float factor, const float* row_factor, float* o_part, float* lse,
-                                    void* stream);
+                                    float factor, const float* row_factor, void* o_part, int32_t part_dtype,
+                                    float* lse, void* stream);
 /* limits[i] = (number of sorted local key positions <= row_pos[i]) - 1. */
 int cc_local_limits(const int64_t* row_pos, int64_t m, const int64_t* local_pos, int64_t n_local,
                     int64_t* limits, void* stream);
 /* Log-sum-exp merge of n_parts partial attentions (parts stride
  * part_stride rows): out[i][h*D..] = sum_w 2^(lse_w - M) O_w / sum_w 2^(lse_w - M). */
-int cc_lse_merge(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t part_stride, int64_t m,
-                 int32_t n_q_heads, int32_t head_dim, void* out, int64_t ldo, int32_t out_dtype, void* stream);
+int cc_lse_merge(const void* o_parts, int32_t part_dtype, const float* lse_parts, int32_t n_parts,
+                 int64_t part_stride, int64_t m, int32_t n_q_heads, int32_t head_dim, void* out, int64_t ldo,
+                 int32_t out_dtype, void* stream);
 /* Same contract on legacy mma.sync tensor cores: the baseline the tcgen05
  * kernel above is measured against (kept for A/B tests and the bench). */
 int cc_sparse_row_attention_mma(const void* q, int64_t ldq, const int64_t* positions, int64_t m,

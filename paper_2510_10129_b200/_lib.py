@@ -100,10 +100,11 @@ _SIGS = {
     "cc_sparse_row_attention": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),
     "cc_sparse_row_attention_ranged": ([vp, i64, vp, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp],
                                        i32),
-    "cc_sparse_row_attention_partial": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, vp, vp], i32),
+    "cc_sparse_row_attention_partial": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i32, vp, vp],
+                                        i32),
     "cc_row_l2_diff": ([vp, i32, i64, vp, i32, i64, i64, i32, vp, vp], i32),
     "cc_local_limits": ([vp, i64, vp, i64, vp, vp], i32),
-    "cc_lse_merge": ([vp, vp, i32, i64, i64, i32, i32, vp, i64, i32, vp], i32),
+    "cc_lse_merge": ([vp, i32, vp, i32, i64, i64, i32, i32, vp, i64, i32, vp], i32),
     "cc_sparse_row_attention_mma": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),
     "cc_banked_attention_f32": ([vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, f32, vp, i32, vp, i64, i64, vp], i32),
     "cc_banked_attention_simt": ([vp, i32, i32, i64, vp, vp, vp, i32, i32, i32, f32, vp, i32, vp, i64, i64, vp], i32),

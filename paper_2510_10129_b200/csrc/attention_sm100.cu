@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
                          const int64_t* __restrict__ kstart, int64_t m,
                          int64_t n_keys, int n_q_heads, int n_kv_heads, float factor,
                          const float* __restrict__ row_factor, __nv_bfloat16* __restrict__ out, int64_t ldo,
-                         int n_ctas, float* __restrict__ o_part, float* __restrict__ lse_part) {
+                         int n_ctas, void* __restrict__ o_part, float* __restrict__ lse_part, int part_bf16) {
   using Cfg = FaCfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -466,13 +466,22 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       tmem_ld32(o_addr + c * 32, ov);
       if (o_part) {
         if (part_row >= 0) {
-          float4* dst = reinterpret_cast<float4*>(o_part + part_row * D + c * 32);
           const bool live = l_run > 0.f && n_tiles > 0;
+          const float sc = live ? inv : 0.f;
+          if (part_bf16) {  // bf16 partials: half the exchange and merge bytes
+            uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(o_part) + part_row * D + c * 32);
 #pragma unroll
-          for (int qd = 0; qd < 8; ++qd)
-            dst[qd] = live ? make_float4(ov[4 * qd] * inv, ov[4 * qd + 1] * inv, ov[4 * qd + 2] * inv,
-                                         ov[4 * qd + 3] * inv)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int qd = 0; qd < 4; ++qd)
+              dst[qd] = make_uint4(pack2_bf16(ov[8 * qd] * sc, ov[8 * qd + 1] * sc),
+                                   pack2_bf16(ov[8 * qd + 2] * sc, ov[8 * qd + 3] * sc),
+                                   pack2_bf16(ov[8 * qd + 4] * sc, ov[8 * qd + 5] * sc),
+                                   pack2_bf16(ov[8 * qd + 6] * sc, ov[8 * qd + 7] * sc));
+          } else {
+            float4* dst = reinterpret_cast<float4*>(reinterpret_cast<float*>(o_part) + part_row * D + c * 32);
+#pragma unroll
+            for (int qd = 0; qd < 8; ++qd)
+              dst[qd] = make_float4(ov[4 * qd] * sc, ov[4 * qd + 1] * sc, ov[4 * qd + 2] * sc, ov[4 * qd + 3] * sc);
+          }
         }
       } else if (out_off >= 0) {
         uint4* dst = reinterpret_cast<uint4*>(out + out_off + c * 32);
@@ -525,7 +534,7 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const
                      const void* k_cache,
                      const void* v_cache, int64_t n_keys, int32_t hq, int32_t hkv, float factor,
                      const float* row_factor, void* out, int64_t ldo, cudaStream_t st, double flops,
-                     float* o_part = nullptr, float* lse_part = nullptr) {
+                     void* o_part = nullptr, float* lse_part = nullptr, int part_bf16 = 0) {
   CUtensorMap tk, tv;
   int rc = make_kv_map(&tk, k_cache, n_keys, hkv, D);
   if (rc) return rc;
@@ -542,13 +551,14 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const
   ProfScope ps(st, OP_ATTENTION, flops);
   fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
       tk, tv, (const __nv_bfloat16*)q, ldq, positions, kstart, m, n_keys, hq, hkv, factor, row_factor,
-      (__nv_bfloat16*)out, ldo, n_ctas, o_part, lse_part);
+      (__nv_bfloat16*)out, ldo, n_ctas, o_part, lse_part, part_bf16);
   CC_LAUNCH_CHECK("fa_sparse_row");
   return CC_OK;
 }
 
 // Split-KV merge: one warp per (row, head), lanes over head_dim.
-__global__ void lse_merge_kernel(const float* __restrict__ o_parts, const float* __restrict__ lse_parts, int n_parts,
+template <typename P>
+__global__ void lse_merge_kernel(const P* __restrict__ o_parts, const float* __restrict__ lse_parts, int n_parts,
                                  int64_t part_stride, int64_t m, int hq, int d, void* __restrict__ out, int64_t ldo,
                                  int out_dtype) {
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -565,10 +575,10 @@ __global__ void lse_merge_kernel(const float* __restrict__ o_parts, const float*
     if (l == -INFINITY) continue;
     const float a = exp2f(l - mx);
     wsum += a;
-    const float* o = o_parts + ((w * part_stride + i) * hq + h) * (int64_t)d;
+    const P* o = o_parts + ((w * part_stride + i) * hq + h) * (int64_t)d;
 #pragma unroll
     for (int k = 0; k < 8; ++k)
-      if (lane + 32 * k < d) acc[k] = fmaf(a, o[lane + 32 * k], acc[k]);
+      if (lane + 32 * k < d) acc[k] = fmaf(a, static_cast<float>(o[lane + 32 * k]), acc[k]);
   }
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
 #pragma unroll
@@ -649,14 +659,17 @@ extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t
 extern "C" int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const int64_t* limits, int64_t m,
                                                const void* k_cache, const void* v_cache, int64_t n_keys,
                                                int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim, float factor,
-                                               const float* row_factor, float* o_part, float* lse, void* stream) {
+                                               const float* row_factor, void* o_part, int32_t part_dtype, float* lse,
+                                               void* stream) {
   CC_CHECK_ARG(n_kv_heads > 0 && n_q_heads % n_kv_heads == 0, CC_ERR_DIMENSION, "bad head counts");
   CC_CHECK_ARG(head_dim == 64 || head_dim == 128, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
   CC_CHECK_ARG(o_part && lse, CC_ERR_VALUE, "partial attention needs o_part and lse outputs");
+  CC_CHECK_ARG(part_dtype == CC_F32 || part_dtype == CC_BF16, CC_ERR_UNSUPPORTED, "partial dtype %d", part_dtype);
+  const int part_bf16 = part_dtype == CC_BF16;
   if (m <= 0) return CC_OK;
   cudaStream_t st = as_stream(stream);
   if (n_keys <= 0) {  // an empty shard contributes nothing: O = 0, LSE = -inf
-    cudaMemsetAsync(o_part, 0, (size_t)m * n_q_heads * head_dim * sizeof(float), st);
+    cudaMemsetAsync(o_part, 0, (size_t)m * n_q_heads * head_dim * (part_bf16 ? 2 : 4), st);
     const int64_t n = m * n_q_heads;
     fill_neg_inf_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(lse, n);
     CC_LAUNCH_CHECK("partial attention (empty shard)");
@@ -664,9 +677,9 @@ extern "C" int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const
   }
   if (head_dim == 128)
     return fa_launch<128>(q, ldq, limits, nullptr, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
-                          nullptr, 0, st, g_attn_flops, o_part, lse);
+                          nullptr, 0, st, g_attn_flops, o_part, lse, part_bf16);
   return fa_launch<64>(q, ldq, limits, nullptr, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor, row_factor,
-                       nullptr, 0, st, g_attn_flops, o_part, lse);
+                       nullptr, 0, st, g_attn_flops, o_part, lse, part_bf16);
 }
 
 extern "C" int cc_local_limits(const int64_t* row_pos, int64_t m, const int64_t* local_pos, int64_t n_local,
@@ -678,14 +691,22 @@ extern "C" int cc_local_limits(const int64_t* row_pos, int64_t m, const int64_t*
   return CC_OK;
 }
 
-extern "C" int cc_lse_merge(const float* o_parts, const float* lse_parts, int32_t n_parts, int64_t part_stride,
-                            int64_t m, int32_t n_q_heads, int32_t head_dim, void* out, int64_t ldo, int32_t out_dtype,
-                            void* stream) {
+extern "C" int cc_lse_merge(const void* o_parts, int32_t part_dtype, const float* lse_parts, int32_t n_parts,
+                            int64_t part_stride, int64_t m, int32_t n_q_heads, int32_t head_dim, void* out,
+                            int64_t ldo, int32_t out_dtype, void* stream) {
   CC_CHECK_ARG(head_dim > 0 && head_dim <= 256, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
+  CC_CHECK_ARG(part_dtype == CC_F32 || part_dtype == CC_BF16, CC_ERR_UNSUPPORTED, "partial dtype %d", part_dtype);
   if (m <= 0 || n_parts <= 0) return CC_OK;
   const int64_t warps = m * n_q_heads;
-  lse_merge_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(
-      o_parts, lse_parts, n_parts, part_stride, m, n_q_heads, head_dim, out, ldo, out_dtype);
+  const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
+  if (part_dtype == CC_BF16)
+    lse_merge_kernel<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>(
+        static_cast<const __nv_bfloat16*>(o_parts), lse_parts, n_parts, part_stride, m, n_q_heads, head_dim, out,
+        ldo, out_dtype);
+  else
+    lse_merge_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const float*>(o_parts), lse_parts,
+                                                                 n_parts, part_stride, m, n_q_heads, head_dim, out,
+                                                                 ldo, out_dtype);
   CC_LAUNCH_CHECK("lse_merge");
   return CC_OK;
 }

@@ -326,7 +326,8 @@ class DeviceShardCompute:
         self.q = torch.zeros(R, qw, dtype=torch.bfloat16, device=self.dev)
         self.ctx = torch.zeros(R, qw, dtype=torch.bfloat16, device=self.dev)
         self.act = torch.empty(R, c.d_ff, dtype=torch.bfloat16, device=self.dev)
-        self.o_part = torch.empty(W * R, c.n_heads, c.d_head, dtype=torch.float32, device=self.dev)
+        # bf16 partials: half the all_to_all and merge bytes (merged in fp32)
+        self.o_part = torch.empty(W * R, c.n_heads, c.d_head, dtype=torch.bfloat16, device=self.dev)
         self.lse = torch.empty(W * R, c.n_heads, dtype=torch.float32, device=self.dev)
 
     def _s(self) -> int:
@@ -358,7 +359,7 @@ class DeviceShardCompute:
         _lib.call("cc_sparse_row_attention_partial", q_all.data_ptr(), qw, self.limits.data_ptr(), q_all.shape[0],
                   self.k[layer].data_ptr(), self.v[layer].data_ptr(), self.local_pos.numel(), c.n_heads, c.kv_heads,
                   c.d_head, factor, self.row_factor.data_ptr() if self.row_factor is not None else None,
-                  self.o_part.data_ptr(), self.lse.data_ptr(), self._s())
+                  self.o_part.data_ptr(), _lib.CC_BF16, self.lse.data_ptr(), self._s())
         return self.o_part, self.lse
 
     def post_attention(self, layer: int, o_recv: torch.Tensor, lse_recv: torch.Tensor) -> None:
@@ -369,7 +370,7 @@ class DeviceShardCompute:
         if not n:
             return
         W, R = self.plan.world, self.rows.r_max
-        _lib.call("cc_lse_merge", o_recv.data_ptr(), lse_recv.data_ptr(), W, R, n, c.n_heads, c.d_head,
+        _lib.call("cc_lse_merge", o_recv.data_ptr(), _lib.CC_BF16, lse_recv.data_ptr(), W, R, n, c.n_heads, c.d_head,
                   self.ctx.data_ptr(), qw, _lib.CC_BF16, self._s())
         gemm(_lib.CC_GEMM_BF16, _lib.CC_EPI_RESIDUAL, n, d, qw, self.ctx, lw.w_o, bias=lw.b_o, C=self.h, ldc=d,
              c_mode=_lib.CC_F32)

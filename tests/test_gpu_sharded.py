@@ -35,9 +35,11 @@ def _attn_ref(q, k, v, limits, factor):
     return torch.einsum("hmn,nhd->mhd", torch.softmax(s, -1), vv)
 
 
+@pytest.mark.parametrize("part", ["f32", "bf16"])
 @pytest.mark.parametrize("D,Hq,Hkv", [(128, 28, 4), (64, 4, 2)])
-def test_partial_attention_and_lse_merge(D, Hq, Hkv):
+def test_partial_attention_and_lse_merge(D, Hq, Hkv, part):
     from paper_2510_10129_b200 import _lib as L
+    pdt = L.CC_BF16 if part == "bf16" else L.CC_F32
     g = torch.Generator(device=DEV).manual_seed(D)
     n, m, W = 1500, 300, 3
     q = torch.randn(m, Hq, D, device=DEV, generator=g).to(torch.bfloat16)
@@ -48,7 +50,7 @@ def test_partial_attention_and_lse_merge(D, Hq, Hkv):
     owner = (torch.arange(n, device=DEV) // 100) % W
     factor = 1.0 / math.sqrt(D)
     s = torch.cuda.current_stream().cuda_stream
-    o_parts = torch.empty(W, m, Hq, D, device=DEV)
+    o_parts = torch.empty(W, m, Hq, D, device=DEV, dtype=torch.bfloat16 if part == "bf16" else torch.float32)
     lse_parts = torch.empty(W, m, Hq, device=DEV)
     for w in range(W):
         local_pos = torch.nonzero(owner == w).flatten().contiguous()
@@ -58,9 +60,10 @@ def test_partial_attention_and_lse_merge(D, Hq, Hkv):
         ref_lim = torch.searchsorted(local_pos, pos, right=True) - 1
         assert torch.equal(lim, ref_lim)
         L.call("cc_sparse_row_attention_partial", q.data_ptr(), Hq * D, lim.data_ptr(), m, lk.data_ptr(),
-               lv.data_ptr(), lk.shape[0], Hq, Hkv, D, factor, None, o_parts[w].data_ptr(), lse_parts[w].data_ptr(), s)
+               lv.data_ptr(), lk.shape[0], Hq, Hkv, D, factor, None, o_parts[w].data_ptr(), pdt,
+               lse_parts[w].data_ptr(), s)
     out = torch.empty(m, Hq * D, device=DEV, dtype=torch.bfloat16)
-    L.call("cc_lse_merge", o_parts.data_ptr(), lse_parts.data_ptr(), W, m, m, Hq, D, out.data_ptr(), Hq * D,
+    L.call("cc_lse_merge", o_parts.data_ptr(), pdt, lse_parts.data_ptr(), W, m, m, Hq, D, out.data_ptr(), Hq * D,
            L.CC_BF16, s)
     torch.cuda.synchronize()
     ref = _attn_ref(q, k, v, pos + 1, factor)
