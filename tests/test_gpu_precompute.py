@@ -143,6 +143,8 @@ def test_host_cache_pool_equals_device_caches(lens):
     assert torch.equal(a.v_store[:, :a.n_rows], b.v_store[:, :b.n_rows])
     dev_out = cc.cacheclip_prefill(primary, aux, pc, ac, query, cfg)
     host_out = cc.cacheclip_prefill(primary, aux, hp, ha, query, cfg)
+    serial_out = cc.cacheclip_prefill(primary, aux, hp, ha, query, cfg, workers=1)  # plain uploads, one stream
     torch.cuda.synchronize()
-    assert host_out.plan == dev_out.plan
+    assert host_out.plan == dev_out.plan == serial_out.plan
     assert np.array_equal(host_out.logits, dev_out.logits)
+    assert np.array_equal(serial_out.logits, dev_out.logits)
