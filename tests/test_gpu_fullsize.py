@@ -116,3 +116,31 @@ def test_deterministic(c2):
     b = cc.cacheclip_prefill(*args)
     assert a.plan == b.plan
     np.testing.assert_array_equal(a.logits, b.logits)
+
+
+def test_merge_rope_at_200k_positions():
+    """C4-scale positions (RoPE base 1e6 beyond 32K is pinned by
+    no reference test): 400 chunks x 500 rows + a 32-row prefix merged into a
+    200,032-row cache; sampled keys equal the oracle's float64-angle rotation
+    bitwise after bf16 rounding, values pass through untouched."""
+    import paper_2510_10129_b200 as cc
+    from paper_2510_10129_b200.config import RopeParams
+    g = torch.Generator(device="cuda").manual_seed(3)
+    P, C, n, H, D = 32, 500, 400, 1, 128
+    prefix_k = torch.randn(1, P, H, D, device="cuda", generator=g).to(torch.bfloat16)
+    chunks = []
+    for i in range(n):
+        body = torch.randn(1, C, H, D, device="cuda", generator=g).to(torch.bfloat16)
+        k = torch.cat([prefix_k, body], 1)
+        chunks.append(cc.ChunkCache(k, k.clone(), list(range(P)) + [i] * C, P, "t", "f"))
+    rope = RopeParams(D, 1e6)
+    merged = cc.merge_caches(chunks, rope)
+    assert merged.n_rows == P + n * C == 200_032
+    rows = np.array([0, 31, 32, 99_999, 150_001, 200_031])
+    src = [(0, r) if r < P else ((r - P) // C, P + (r - P) % C) for r in rows]
+    raw = torch.stack([chunks[c].k[0, s] for c, s in src]).float().cpu().numpy()
+    want = orc.rope_rotate(raw, rows, D, 1e6)
+    got = merged.k_store[0, rows].float().cpu().numpy()
+    np.testing.assert_array_equal(got, orc.round_to_bf16(want))
+    vals = torch.stack([chunks[c].v[0, s] for c, s in src])
+    assert torch.equal(merged.v_store[0, rows], vals)
