@@ -221,15 +221,28 @@ __global__ void __launch_bounds__(kHeadThreads) lm_head_kernel(const float* __re
   for (int64_t v = row0; v < vocab; v += (int64_t)gridDim.x * (kHeadThreads / 32)) {
     float acc = 0.f;
     if (dtype == CC_BF16) {
+      // batches of 8 row segments per lane: all loads of a batch are in flight
+      // before the first FMA (one load per lane at a time left HBM at ~0.6)
       const uint4* wr = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(W) + v * d);
-      for (int c = lane; c < d / 8; c += 32) {
-        uint4 u = __ldg(wr + c);
-        const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const int n8 = d / 8;
+      for (int c0 = lane; c0 < n8; c0 += 32 * 8) {
+        uint4 u[8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          float2 f = __bfloat1622float2(p[i]);
-          acc = fmaf(xs[c * 8 + 2 * i], f.x, acc);
-          acc = fmaf(xs[c * 8 + 2 * i + 1], f.y, acc);
+        for (int b = 0; b < 8; ++b) {
+          const int c = c0 + 32 * b;
+          u[b] = c < n8 ? __ldg(wr + c) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const int c = c0 + 32 * b;
+          if (c >= n8) break;
+          const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&u[b]);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float2 f = __bfloat1622float2(p[i]);
+            acc = fmaf(xs[c * 8 + 2 * i], f.x, acc);
+            acc = fmaf(xs[c * 8 + 2 * i + 1], f.y, acc);
+          }
         }
       }
     } else {
