@@ -177,3 +177,54 @@ def test_uniform_runs_detects_pool_slots():
     assert _uniform_runs([(sep[i], 2, 8 * i, 8) for i in range(3)], rb) == [(0, 1), (1, 2), (2, 3)]
     rag = [(cc(0, 10), 0, 0, 10), (cc(1, 7), 2, 10, 5), (cc(2, 10), 2, 15, 8)]
     assert _uniform_runs(rag, rb) == [(0, 1), (1, 2), (2, 3)]
+
+
+def test_request_validation_raises_before_any_device_work():
+    """The reference's error conventions on the request path (every error a
+    ValueError subclass, raised before any mutation: kv_store.py:193-235,
+    pipeline.py:156-200, tokenizers.py): checked here on CPU tensors, so no
+    kernel can have run when they fire."""
+    import pytest
+    import torch
+
+    import paper_2510_10129_b200 as cc
+    from paper_2510_10129_b200.config import RopeParams
+
+    def chunk(prefix, body, fp="f", tok="t", dtype=torch.float32, heads=2):
+        n = len(prefix) + len(body)
+        k = torch.zeros(2, n, heads, 8, dtype=dtype)
+        return cc.ChunkCache(k, k.clone(), list(prefix) + list(body), len(prefix), tok, fp)
+
+    rope = RopeParams(8)
+    a, b = chunk([1, 2], [3, 4, 5]), chunk([1, 2], [6, 7])
+    with pytest.raises(cc.CacheConsistencyError):
+        cc.merge_caches([], rope)
+    with pytest.raises(cc.CacheConsistencyError):  # different prefix tokens
+        cc.merge_caches([a, chunk([1, 9], [6])], rope)
+    with pytest.raises(cc.CacheConsistencyError):  # different prefix length
+        cc.merge_caches([a, chunk([1], [6])], rope)
+    with pytest.raises(cc.CacheConsistencyError):  # different model
+        cc.merge_caches([a, chunk([1, 2], [6], fp="g")], rope)
+    with pytest.raises(cc.CacheConsistencyError):  # different tokenizer
+        cc.merge_caches([a, chunk([1, 2], [6], tok="u")], rope)
+    with pytest.raises(cc.CacheConsistencyError):  # different geometry
+        cc.merge_caches([a, chunk([1, 2], [6], heads=1)], rope)
+    with pytest.raises(cc.CacheConsistencyError):  # rows vs ids
+        cc.ChunkCache(torch.zeros(2, 3, 2, 8), torch.zeros(2, 3, 2, 8), [1, 2], 1, "t", "f")
+    with pytest.raises(cc.CacheConsistencyError):  # K / V shapes
+        cc.ChunkCache(torch.zeros(2, 3, 2, 8), torch.zeros(2, 3, 1, 8), [1, 2, 3], 1, "t", "f")
+    assert issubclass(cc.CacheConsistencyError, ValueError) and issubclass(cc.DimensionError, ValueError)
+    model = object()  # never reached: the pipeline validates its inputs first
+    cfg = cc.SelectionConfig(0.2)
+    with pytest.raises(ValueError):
+        cc.cacheclip_prefill(model, model, [a, b], [a], [1], cfg)      # chunk counts differ
+    with pytest.raises(ValueError):
+        cc.cacheclip_prefill(model, model, [], [], [1], cfg)          # no chunks
+    with pytest.raises(ValueError):
+        cc.cacheclip_prefill(model, model, [a], [b], [1], cfg)        # cached texts differ
+    with pytest.raises(ValueError):
+        cc.cacheclip_prefill(model, model, [a], [a], [], cfg)         # empty query
+    with pytest.raises(ValueError):
+        cc.cacheclip_prefill(model, model, [a], [a], "text", cfg)     # text query without tokenizers
+    with pytest.raises(ValueError):
+        cc.SelectionConfig(1.5)
