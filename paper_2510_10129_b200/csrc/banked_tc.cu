@@ -11,13 +11,15 @@
 //
 // hi = x rounded to tf32, lo = tf32(x - hi): the dropped lo*lo term and the
 // tf32 rounding of lo leave ~2^-22 relative error per product (fp32 level).
-// A row's 576 logits do not fit TMEM, so the key tiles are swept more than
-// once (recomputing Q K^T is cheap next to the softmax):
+// A row's 576 logits do not fit TMEM. The scoring layer sweeps the key tiles
+// three times to follow the reference's order exactly; context layers make
+// one online pass:
 //   - last (scoring) layer: the reference's order exactly (tensor_core.py:
 //     88-96, 165-170) — max of S * factor, then the sum of exp(x - max), then
 //     p = exp(x - max) / sum written as the weights (selector.py:157-165);
-//   - other layers: an online max / sum in the log2 domain (MUFU ex2), then
-//     P = 2^(y - max) / sum fed to O += P V.
+//   - other layers: one sweep, online softmax in the log2 domain (MUFU ex2)
+//     with a lazy rescale of O, P = 2^(y - max) fed to O += P V, O / sum at
+//     the end.
 //
 // CTA = one sequence x one KV head x (128 / G) query rows; packed row r =
 // query i0 + r / G, head kvh*G + r % G, so the K/V tiles are read once for
@@ -323,38 +325,54 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
       }
     });
   } else {
-    // Context rows: online max / sum in the log2 domain (MUFU ex2), then
-    // P = 2^(y - max) / sum fed to O += P V on the tensor core.
+    // Context rows: ONE sweep, online softmax in the log2 domain (MUFU ex2).
+    // Per key tile the two column halves of a row agree on the tile max
+    // through shared memory; the running max moves only when a tile raises
+    // it by more than 2^8 (lazy rescale: O in TMEM and the partial sums are
+    // scaled then), P = 2^(y - max) unnormalised feeds O += P V, and the
+    // epilogue divides by the row sum.
     const float fl = factor * 1.4426950408889634f;
-    float m = -INFINITY, l = 0.f;
-    sweep(false, [&](int, int c0, float* s) {
-      float tm = m;
+    float m_run = -INFINITY, l_half = 0.f;
+    sweep(true, [&](int j, int c0, float* s) {
+      float tm = -INFINITY;
 #pragma unroll
       for (int t = 0; t < HC; ++t) {
         s[t] = c0 + t < limit ? s[t] * fl : -INFINITY;
         tm = fmaxf(tm, s[t]);
       }
-      if (tm == -INFINITY) return;
-      l *= ex2_approx(m - tm);
-      m = tm;
+      red[half * kBtRows + r] = tm;
+      __syncthreads();
+      tm = fmaxf(tm, red[(half ^ 1) * kBtRows + r]);
+      float alpha = 1.f;
+      bool resc = false;
+      if (tm > m_run + 8.0f) {
+        alpha = m_run == -INFINITY ? 0.f : ex2_approx(m_run - tm);
+        m_run = tm;
+        resc = true;
+      }
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        // O is stable: the sweep waited for PV(j-1) before staging this tile
+        const float a = resc ? alpha : 1.f;
 #pragma unroll
-      for (int t = 0; t < HC; ++t) l += ex2_approx(s[t] - m);
-    });
-    float m1, l1;
-    exchange(m, l, m1, l1);
-    const float M = fmaxf(m, m1);
-    const float L = (m == -INFINITY ? 0.f : l * ex2_approx(m - M)) + (m1 == -INFINITY ? 0.f : l1 * ex2_approx(m1 - M));
-    const float inv = L > 0.f ? 1.0f / L : 0.f;
-    sweep(true, [&](int j, int c0, float* s) {
-      float ph[HC];
+        for (int c = 0; c < HD / 64; ++c) {
+          float o[32];
+          tmem_ld32(tl + Cfg::T_O + half * (HD / 2) + c * 32, o);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] *= a;
+          tmem_st32_f(tl + Cfg::T_O + half * (HD / 2) + c * 32, o);
+        }
+      }
+      float ph[HC], ls = 0.f;
 #pragma unroll
       for (int t = 0; t < HC; ++t) {
-        const float pv = c0 + t < limit ? ex2_approx(s[t] * fl - M) * inv : 0.f;
+        const float pv = c0 + t < limit ? ex2_approx(s[t] - m_run) : 0.f;
+        ls += pv;
         float lo;
         split_tf32_finite(pv, ph[t], lo);
         float l2;
         split_tf32_finite(lo, s[t], l2);
       }
+      l_half = l_half * alpha + ls;
       tmem_st16_f(tl + Cfg::T_PH + half * HC, ph);
       tmem_st16_f(tl + Cfg::T_PL + half * HC, s);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -373,6 +391,10 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
         tc_commit(pv_bar);
       }
     });
+    float l_other, unused;
+    exchange(l_half, 0.f, l_other, unused);
+    const float L = half == 0 ? l_half + l_other : l_other + l_half;
+    const float inv = L > 0.f ? 1.0f / L : 0.f;
     mbar_wait(pv_bar, pv_phase);
     tc_fence_after();
 #pragma unroll
@@ -381,6 +403,8 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
       const int d0 = half * (HD / 2) + c * 32;
       tmem_ld32(tl + Cfg::T_O + d0, o);
       if (!live) continue;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] *= inv;
       const int64_t row = sq.row0 + qi;
       const int64_t col0 = (int64_t)head * HD + d0;
       if (out_mode == CC_F32) {
