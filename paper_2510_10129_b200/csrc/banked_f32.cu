@@ -212,8 +212,7 @@ __global__ void __launch_bounds__(kBkThreads) banked_f32_kernel(
           split_tf32(v, hi, lo);
           split_tf32(lo, lh, ll);
           float* p = reinterpret_cast<float*>(out) + row * qw * 3;
-          p[col] = hi;
-          p[qw + col] = hi;
+          p[col] = hi;  // (middle hi copy unread by the 3xTF32 GEMM)
           p[2 * qw + col] = lh;
         }
       }

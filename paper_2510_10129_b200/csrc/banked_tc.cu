@@ -418,8 +418,7 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
           float4 v = make_float4(o[4 * t], o[4 * t + 1], o[4 * t + 2], o[4 * t + 3]), hi, lo, lh, ll;
           split4(v, hi, lo);
           split4(lo, lh, ll);
-          reinterpret_cast<float4*>(p)[t] = hi;
-          reinterpret_cast<float4*>(p + qw)[t] = hi;
+          reinterpret_cast<float4*>(p)[t] = hi;  // (middle hi copy unread by the 3xTF32 GEMM)
           reinterpret_cast<float4*>(p + 2 * qw)[t] = lh;
         }
       }

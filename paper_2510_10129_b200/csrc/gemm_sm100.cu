@@ -88,7 +88,9 @@ __device__ __forceinline__ float act_apply(int act, float x) {
 }
 
 // Store 4 consecutive values of one row (cols [col, col+4)) in `mode`; the
-// split layout keeps a 3*ld row pitch with [hi | hi | lo] segments `width` apart.
+// split layout keeps a 3*ld row pitch with [hi | hi | lo] segments `width` apart
+// (activations: only the hi and lo segments are written; the 3xTF32 GEMM reads
+// A_hi at column k and A_lo at 2K + k).
 __device__ __forceinline__ void store4(void* base, int mode, int64_t row, int64_t ld, int64_t col, int64_t width,
                                        float4 v) {
   if (mode == CC_BF16) {
@@ -110,8 +112,7 @@ __device__ __forceinline__ void store4(void* base, int mode, int64_t row, int64_
       split_tf32(lo, lh[i], ll);
     }
     const float4 h4 = make_float4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<float4*>(p) = h4;
-    *reinterpret_cast<float4*>(p + width) = h4;
+    *reinterpret_cast<float4*>(p) = h4;  // the middle hi copy is never read (the GEMM loads hi and lo only)
     *reinterpret_cast<float4*>(p + 2 * width) = make_float4(lh[0], lh[1], lh[2], lh[3]);
   }
 }

@@ -327,8 +327,7 @@ __device__ __forceinline__ void store_x4(void* x_out, int mode, int64_t row, int
       lo[e] = lh;
     }
     float* o = reinterpret_cast<float*>(x_out) + row * (int64_t)d * 3;
-    *reinterpret_cast<float4*>(o + j) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-    *reinterpret_cast<float4*>(o + d + j) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<float4*>(o + j) = make_float4(hi[0], hi[1], hi[2], hi[3]);  // (middle hi copy unread)
     *reinterpret_cast<float4*>(o + 2 * d + j) = make_float4(lo[0], lo[1], lo[2], lo[3]);
   }
 }

@@ -343,9 +343,9 @@ def test_banked_attention_f32_matches_reference_math(fn, Hq, Hkv, D, Q, nbs):
     wg = w.cpu().numpy()
     sp = split.cpu().numpy()
     w_ = Hq * D
-    # split layout [hi | hi | lo]: hi + lo reproduces the context to ~2^-22
+    # split layout [hi | . | lo] (the 3xTF32 GEMM reads hi and lo only; the
+    # middle segment is not written): hi + lo reproduces the context to ~2^-22
     np.testing.assert_allclose(sp[:, :w_] + sp[:, 2 * w_:], got, rtol=1e-6, atol=1e-7)
-    assert np.array_equal(sp[:, :w_], sp[:, w_:2 * w_])
     for s in range(S):
         nb = banks[s].shape[1]
         bank_k = np.concatenate([banks[s][0], kn[s * Q:(s + 1) * Q].reshape(Q, Hkv, D)])
