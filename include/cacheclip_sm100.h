@@ -363,11 +363,16 @@ int64_t cc_forward_rows_workspace_bytes(const cc_model_desc* md, int64_t rows);
 int64_t cc_forward_banked_workspace_bytes(const cc_model_desc* md, int64_t rows);
 /* bf16 engine: rows (ids, positions) through every layer; logits of the last
  * row + argmax when logits != NULL. attn_pairs = sum of visible keys (for the
- * profiler's algorithmic FLOPs only). The residual stream stays at the start
- * of the workspace ([rows][d] fp32). */
+ * profiler's algorithmic FLOPs only). tail_rows (0, 1 or rows): how many
+ * trailing rows' final states the caller reads. Every row's K/V are written
+ * at every layer; in the LAST layer the attention, o-proj and MLP run only
+ * for the tail rows (the reference computes them for all rows, but nothing
+ * reads them: selective_forward returns the cache, extend_cache the last
+ * row's logits). The residual stream stays at the start of the workspace
+ * ([rows][d] fp32; after the call only the tail rows hold final states). */
 int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t rows,
                     const cc_kv_plan* plan, int64_t n_keys, double attn_pairs, const float* row_factor,
-                    void* workspace, float* logits, int64_t* argmax, void* stream);
+                    int64_t tail_rows, void* workspace, float* logits, int64_t* argmax, void* stream);
 /* fp32 engine over sequences with banks (tables: device cc_bank_seq[n_layers][n_seqs]).
  * layer_ready: optional host array of cudaEvent_t — layer l waits for
  * layer_ready[l] (banks streamed in from pinned host memory on another stream). */

@@ -118,7 +118,7 @@ _SIGS = {
     "cc_forward_rows_workspace_bytes": ([ctypes.POINTER(ModelDesc), i64], i64),
     "cc_forward_banked_workspace_bytes": ([ctypes.POINTER(ModelDesc), i64], i64),
     "cc_forward_rows": ([ctypes.POINTER(ModelDesc), vp, vp, i64, ctypes.POINTER(KvPlan), i64, ctypes.c_double,
-                         vp, vp, vp, vp, vp], i32),
+                         vp, i64, vp, vp, vp, vp], i32),
     "cc_forward_banked": ([ctypes.POINTER(ModelDesc), vp, vp, i64, vp, i32, i32, i64, vp, i64, vp, i64,
                            ctypes.POINTER(ScoreSpec), ctypes.POINTER(vp), vp, vp], i32),
     "cc_profile_enable": ([i32], None),

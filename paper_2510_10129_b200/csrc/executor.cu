@@ -115,9 +115,12 @@ int64_t cc_forward_banked_workspace_bytes(const cc_model_desc* md, int64_t rows)
 
 int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t R,
                     const cc_kv_plan* plan, int64_t n_keys, double attn_pairs, const float* row_factor,
-                    void* workspace, float* logits, int64_t* argmax, void* stream) {
+                    int64_t tail_rows, void* workspace, float* logits, int64_t* argmax, void* stream) {
   CC_CHECK_ARG(md && plan && workspace, CC_ERR_VALUE, "null model / plan / workspace");
   CC_CHECK_ARG(md->dtype == CC_BF16, CC_ERR_UNSUPPORTED, "cc_forward_rows runs bf16 models");
+  CC_CHECK_ARG(tail_rows == R || tail_rows == 1 || tail_rows == 0, CC_ERR_VALUE,
+               "tail_rows must be 0, 1 or rows (got %lld)", (long long)tail_rows);
+  CC_CHECK_ARG(!logits || tail_rows >= 1, CC_ERR_VALUE, "logits need the last row's final state (tail_rows >= 1)");
   if (R <= 0) return CC_OK;
   const int64_t d = md->d_model, qw = (int64_t)md->n_heads * md->head_dim;
   const int64_t kw = (int64_t)md->n_kv_heads * md->head_dim;
@@ -172,15 +175,26 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
     a.k_raw = lp(plan->k_raw, plan->k_raw_stride, l);
     a.raw_rows = plan->raw_rows;
     CC_TRY(cc_gemm(&a, stream));
-    g_attn_flops = 4.0 * md->n_heads * md->head_dim * attn_pairs;
-    CC_TRY(cc_sparse_row_attention_ranged(q, qw, positions, plan->key_start, R,
-                                          lp(plan->attn_k, plan->attn_k_stride, l),
-                                          lp(plan->attn_v, plan->attn_v_stride, l), n_keys, md->n_heads,
-                                          md->n_kv_heads, md->head_dim, factor, row_factor, ctx, qw, stream));
-    g_attn_flops = 0.0;
-    CC_TRY(gemm_call(CC_GEMM_BF16, CC_EPI_RESIDUAL, R, d, qw, ctx, qw, lw.w_o, qw, lw.b_o, h, d, CC_F32, 0, 0,
-                     stream));
-    CC_TRY(run_mlp(md, lw, h, x, act, R, CC_GEMM_BF16, CC_BF16, stream));
+    // Last layer: every row's K/V are in the cache now (the QKV epilogue
+    // scattered them); its attention output, o-proj and MLP feed nothing but
+    // the final state of the rows the caller reads (tail_rows: the head's last
+    // row, all rows, or none), so only those rows continue.
+    const int64_t r0 = (l == md->n_layers - 1) ? R - tail_rows : 0;
+    const int64_t Rl = R - r0;
+    if (Rl > 0) {
+      g_attn_flops = 4.0 * md->n_heads * md->head_dim *
+                     (r0 == 0 ? attn_pairs : (attn_pairs < 0 ? -1.0 : (double)n_keys * Rl));
+      CC_TRY(cc_sparse_row_attention_ranged(q + r0 * qw, qw, positions + r0,
+                                            plan->key_start ? plan->key_start + r0 : nullptr, Rl,
+                                            lp(plan->attn_k, plan->attn_k_stride, l),
+                                            lp(plan->attn_v, plan->attn_v_stride, l), n_keys, md->n_heads,
+                                            md->n_kv_heads, md->head_dim, factor,
+                                            row_factor ? row_factor + r0 : nullptr, ctx + r0 * qw, qw, stream));
+      g_attn_flops = 0.0;
+      CC_TRY(gemm_call(CC_GEMM_BF16, CC_EPI_RESIDUAL, Rl, d, qw, ctx + r0 * qw, qw, lw.w_o, qw, lw.b_o, h + r0 * d,
+                       d, CC_F32, 0, 0, stream));
+      CC_TRY(run_mlp(md, lw, h + r0 * d, x, act, Rl, CC_GEMM_BF16, CC_BF16, stream));
+    }
   }
   (void)kw;
   if (logits)

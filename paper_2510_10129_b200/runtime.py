@@ -139,7 +139,11 @@ def forward_rows(model: Model, ids: torch.Tensor, positions: torch.Tensor, plan:
                  row_factor: torch.Tensor | None = None, want_logits: bool = True, pairs: int = 0,
                  layers: int | None = None) -> RowsResult:
     """``layers``: run only the first `layers` layers (no head); the residual
-    stream after them is returned (CacheBlend's layer-0 pass)."""
+    stream of every row after them is returned (CacheBlend's layer-0 pass).
+    A full pass keeps only what its outputs read: K/V of every row at every
+    layer, and the last layer's attention / o-proj / MLP for the head's last
+    row (want_logits) or for no row (cache-only prefill) — RowsResult.h then
+    holds final states for those rows only."""
     c = model.config
     if c.dtype != "bf16":
         raise ValueError("forward_rows runs bf16 models; fp32 models use forward_banked")
@@ -159,8 +163,10 @@ def forward_rows(model: Model, ids: torch.Tensor, positions: torch.Tensor, plan:
         logits = torch.empty(c.vocab_size, dtype=torch.float32, device=dev)
         argmax = torch.empty(1, dtype=torch.int64, device=dev)
     cplan = plan.to_c()
+    tail = R if layers is not None else (1 if want_logits else 0)
     _lib.check(lib.cc_forward_rows(ctypes.byref(md), ids.data_ptr(), positions.data_ptr(), R, ctypes.byref(cplan),
-                                   n_keys, float(pairs), _p(row_factor), ws.data_ptr(), _p(logits), _p(argmax), _s()))
+                                   n_keys, float(pairs), _p(row_factor), tail, ws.data_ptr(), _p(logits),
+                                   _p(argmax), _s()))
     h = ws[: R * c.d_model * 4].view(torch.float32).view(R, c.d_model)
     return RowsResult(h, logits, argmax)
 
