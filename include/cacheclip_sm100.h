@@ -375,11 +375,14 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
                     int64_t tail_rows, void* workspace, float* logits, int64_t* argmax, void* stream);
 /* fp32 engine over sequences with banks (tables: device cc_bank_seq[n_layers][n_seqs]).
  * layer_ready: optional host array of cudaEvent_t — layer l waits for
- * layer_ready[l] (banks streamed in from pinned host memory on another stream). */
+ * layer_ready[l] (banks streamed in from pinned host memory on another stream).
+ * want_state = 0: the caller reads only the written K/V (cache-only prefill),
+ * so the last layer stops after its QKV GEMM. */
 int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t rows,
                       const cc_bank_seq* tables, int32_t n_seqs, int32_t max_new, int64_t max_bank,
                       void* v_dst, int64_t v_dst_stride, void* k_raw_dst, int64_t k_raw_stride,
-                      const cc_score_spec* score, void* const* layer_ready, void* workspace, void* stream);
+                      const cc_score_spec* score, void* const* layer_ready, int32_t want_state,
+                      void* workspace, void* stream);
 
 /* Launch profiler: CUDA events around every launch while enabled; collect
  * returns (op id, algorithmic work, ms) per launch and clears. op ids:

@@ -120,7 +120,7 @@ _SIGS = {
     "cc_forward_rows": ([ctypes.POINTER(ModelDesc), vp, vp, i64, ctypes.POINTER(KvPlan), i64, ctypes.c_double,
                          vp, i64, vp, vp, vp, vp], i32),
     "cc_forward_banked": ([ctypes.POINTER(ModelDesc), vp, vp, i64, vp, i32, i32, i64, vp, i64, vp, i64,
-                           ctypes.POINTER(ScoreSpec), ctypes.POINTER(vp), vp, vp], i32),
+                           ctypes.POINTER(ScoreSpec), ctypes.POINTER(vp), i32, vp, vp], i32),
     "cc_profile_enable": ([i32], None),
     "cc_profile_collect": ([vp, vp, vp, i64], i64),
     "cc_profile_fill_work": ([i32, ctypes.c_double], None),

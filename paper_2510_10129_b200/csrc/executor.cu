@@ -206,7 +206,7 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
 int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t* positions, int64_t R,
                       const cc_bank_seq* tables, int32_t n_seqs, int32_t max_new, int64_t max_bank, void* v_dst,
                       int64_t v_dst_stride, void* k_raw_dst, int64_t k_raw_stride, const cc_score_spec* score,
-                      void* const* layer_ready, void* workspace, void* stream) {
+                      void* const* layer_ready, int32_t want_state, void* workspace, void* stream) {
   CC_CHECK_ARG(md && tables && workspace, CC_ERR_VALUE, "null model / tables / workspace");
   CC_CHECK_ARG(md->dtype == CC_F32, CC_ERR_UNSUPPORTED, "cc_forward_banked runs fp32 (3xTF32) models");
   if (R <= 0) return CC_OK;
@@ -270,6 +270,7 @@ int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t
       return cc_reduce_scores(score->weights, n_seqs, md->n_heads, max_new, score->max_chunk, score->chunk_lens,
                               score->col_off, score->max_chunk, score->scores, stream);
     }
+    if (l == L - 1 && !want_state) break;  // cache-only prefill: the last layer's K/V are written, nothing reads h
     CC_TRY(cc_banked_attention_f32(tl, n_seqs, max_new, max_bank, q, k_new, vd, md->n_heads, md->n_kv_heads,
                                    md->head_dim, factor, ctx, CC_F32_SPLIT3, nullptr, 0, 0, stream));
     CC_TRY(gemm_call(CC_GEMM_TF32X3, CC_EPI_RESIDUAL, R, d, qw, ctx, 3 * qw, lw.w_o, 3 * qw, lw.b_o, h, d, CC_F32,

@@ -91,7 +91,7 @@ def _dense(model: Model, ids: torch.Tensor, want_logits: bool):
         res = forward_rows(model, ids, pos, plan, n, want_logits=want_logits, pairs=visible_pairs(n))
         return K, V, res.logits, res.argmax
     tables = bank_tables(c.n_layers, [(None, None, 0, 0, n)], dev)
-    h = forward_banked(model, ids, pos, tables, 1, n, 0, v_dst=V, k_raw_dst=K)
+    h = forward_banked(model, ids, pos, tables, 1, n, 0, v_dst=V, k_raw_dst=K, want_state=want_logits)
     logits = argmax = None
     if want_logits:
         logits, argmax = final_logits(model, h[n - 1])
@@ -167,7 +167,7 @@ def _dense_batched(model: Model, seqs: list[list[int]]):
     K = torch.empty(c.n_layers, R, c.kv_heads, c.d_head, dtype=torch.float32, device=dev)
     V = torch.empty_like(K)
     tables = bank_tables(c.n_layers, [(None, None, 0, int(r0), int(n)) for r0, n in zip(row0, lens)], dev)
-    forward_banked(model, ids, pos, tables, len(seqs), int(lens.max()), 0, v_dst=V, k_raw_dst=K)
+    forward_banked(model, ids, pos, tables, len(seqs), int(lens.max()), 0, v_dst=V, k_raw_dst=K, want_state=False)
     return [(K[:, b:b + n], V[:, b:b + n]) for b, n in zip(row0.tolist(), lens.tolist())]
 
 

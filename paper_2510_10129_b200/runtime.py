@@ -203,10 +203,12 @@ class ScoreSpec:
 def forward_banked(model: Model, ids: torch.Tensor, positions: torch.Tensor, tables: torch.Tensor,
                    n_seqs: int, max_new: int, max_bank: int, *, v_dst: torch.Tensor | None = None,
                    k_raw_dst: torch.Tensor | None = None, score: ScoreSpec | None = None,
-                   layer_ready: list | None = None) -> torch.Tensor:
+                   layer_ready: list | None = None, want_state: bool = True) -> torch.Tensor:
     """fp32 engine. tables: device cc_bank_seq[n_layers][n_seqs]. v_dst /
     k_raw_dst: optional [L, rows, Hkv, D] destinations of the new rows' values
-    and position-free keys (dense precompute). Returns the residual stream."""
+    and position-free keys (dense precompute). Returns the residual stream
+    (meaningless with want_state=False: the last layer then stops after its
+    QKV GEMM, K/V being all the caller reads)."""
     c = model.config
     if c.dtype != "fp32":
         raise ValueError("forward_banked runs fp32 models")
@@ -229,7 +231,7 @@ def forward_banked(model: Model, ids: torch.Tensor, positions: torch.Tensor, tab
                                      n_seqs, max_new, max_bank, _p(v_dst), _layer_stride(v_dst), _p(k_raw_dst),
                                      _layer_stride(k_raw_dst), ctypes.byref(spec_c) if spec_c is not None else None,
                                      ctypes.cast(ready, ctypes.POINTER(ctypes.c_void_p)) if ready else None,
-                                     ws.data_ptr(), _s()))
+                                     1 if want_state else 0, ws.data_ptr(), _s()))
     return ws[: R * c.d_model * 4].view(torch.float32).view(R, c.d_model)
 
 
