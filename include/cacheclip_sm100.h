@@ -217,6 +217,20 @@ int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const int64_t* l
 /* limits[i] = (number of sorted local key positions <= row_pos[i]) - 1. */
 int cc_local_limits(const int64_t* row_pos, int64_t m, const int64_t* local_pos, int64_t n_local,
                     int64_t* limits, void* stream);
+/* Split-KV attention on ONE GPU for launches of few rows over long key
+ * ranges (a decode step, the last layer's head row): each CTA's key tiles
+ * are cut into n_splits parts run as separate CTAs (partials in o_parts
+ * [n_splits][m][Hq][D] fp32 and lse_parts [n_splits][m][Hq], caller-owned),
+ * then merged by log-sum-exp into `out` (bf16). n_splits <= 1 is
+ * cc_sparse_row_attention_ranged. */
+int cc_sparse_row_attention_split(const void* q, int64_t ldq, const int64_t* positions, const int64_t* key_start,
+                                  int64_t m, const void* k_cache, const void* v_cache, int64_t n_keys,
+                                  int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim, float factor,
+                                  const float* row_factor, int32_t n_splits, float* o_parts, float* lse_parts,
+                                  void* out, int64_t ldo, void* stream);
+/* The split count cc_forward_rows uses: > 1 only for m * (Hq / Hkv) <= 256
+ * packed rows over >= 4096 keys (up to 32 parts); 1 otherwise. */
+int32_t cc_attention_splits(int64_t m, int32_t n_q_heads, int32_t n_kv_heads, int64_t n_keys);
 /* Log-sum-exp merge of n_parts partial attentions (parts stride
  * part_stride rows): out[i][h*D..] = sum_w 2^(lse_w - M) O_w / sum_w 2^(lse_w - M). */
 int cc_lse_merge(const void* o_parts, int32_t part_dtype, const float* lse_parts, int32_t n_parts,

@@ -100,6 +100,9 @@ _SIGS = {
     "cc_sparse_row_attention": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),
     "cc_sparse_row_attention_ranged": ([vp, i64, vp, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp],
                                        i32),
+    "cc_sparse_row_attention_split": ([vp, i64, vp, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, i32, vp, vp, vp,
+                                       i64, vp], i32),
+    "cc_attention_splits": ([i64, i32, i32, i64], i32),
     "cc_sparse_row_attention_partial": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i32, vp, vp],
                                         i32),
     "cc_row_l2_diff": ([vp, i32, i64, vp, i32, i64, i64, i32, vp, vp], i32),

@@ -26,6 +26,9 @@
 //               polynomial on the FMA pipe to offload MUFU.
 #include "cc_common.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -50,6 +53,7 @@ constexpr int kFaThreads = 384;  // 3 warpgroups: producer/MMA, softmax A, softm
 constexpr int kFaCtlRegs = 56;    // setmaxnreg budgets: 128*56 + 256*224 <= 64K
 constexpr int kFaSoftmaxRegs = 224;
 constexpr float kFaRescaleThreshold = 8.0f;  // log2 domain
+constexpr int kMaxAttnSplits = 32;
 
 template <int D>
 struct FaCfg {
@@ -289,8 +293,16 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   const uint32_t tmem = *tmem_slot;
   // key tiles [j0, j0 + n_tiles) cover every row's range (rows are sorted, so a
   // CTA's ranges are nearly contiguous; tiles outside a row's range are masked)
-  const int j0 = *s_kmax > 0 ? *s_kmin / kFaKeys : 0;
-  const int n_tiles = (*s_kmax + kFaKeys - 1) / kFaKeys - j0;
+  int j0 = *s_kmax > 0 ? *s_kmin / kFaKeys : 0;
+  int n_tiles = (*s_kmax + kFaKeys - 1) / kFaKeys - j0;
+  if (gridDim.z > 1) {  // split-KV (few rows, long keys): this CTA takes part blockIdx.z of the tile range
+    const int per = (n_tiles + (int)gridDim.z - 1) / (int)gridDim.z;
+    const int a = min(n_tiles, (int)blockIdx.z * per), b = min(n_tiles, a + per);
+    j0 += a;
+    n_tiles = b - a;
+    o_part = static_cast<uint8_t*>(o_part) + (size_t)blockIdx.z * m * n_q_heads * D * (part_bf16 ? 2 : 4);
+    lse_part += (int64_t)blockIdx.z * m * n_q_heads;
+  }
 
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kFaCtlRegs));
@@ -534,7 +546,7 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const
                      const void* k_cache,
                      const void* v_cache, int64_t n_keys, int32_t hq, int32_t hkv, float factor,
                      const float* row_factor, void* out, int64_t ldo, cudaStream_t st, double flops,
-                     void* o_part = nullptr, float* lse_part = nullptr, int part_bf16 = 0) {
+                     void* o_part = nullptr, float* lse_part = nullptr, int part_bf16 = 0, int n_splits = 1) {
   CUtensorMap tk, tv;
   int rc = make_kv_map(&tk, k_cache, n_keys, hkv, D);
   if (rc) return rc;
@@ -547,7 +559,7 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const
   }
   const int G = hq / hkv;
   const int n_ctas = (int)((m * G + 2 * kFaTileRows - 1) / (2 * kFaTileRows));
-  dim3 grid(n_ctas, hkv);
+  dim3 grid(n_ctas, hkv, n_splits);
   ProfScope ps(st, OP_ATTENTION, flops);
   fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
       tk, tv, (const __nv_bfloat16*)q, ldq, positions, kstart, m, n_keys, hq, hkv, factor, row_factor,
@@ -646,6 +658,54 @@ extern "C" int cc_sparse_row_attention_ranged(const void* q, int64_t ldq, const 
                           row_factor, out, ldo, st, g_attn_flops);
   return fa_launch<64>(q, ldq, positions, key_start, m, k_cache, v_cache, n_keys, n_q_heads, n_kv_heads, factor,
                        row_factor, out, ldo, st, g_attn_flops);
+}
+
+// Split-KV count for a launch of m rows over n_keys keys: > 1 only when the
+// rows fit one query-tile pair per KV head (decode steps, the last layer's
+// head row) and the keys are long, so a handful of CTAs would otherwise walk
+// the whole key range alone; then each CTA takes 1/S of the key tiles and
+// the parts are merged by log-sum-exp. Larger launches are never split
+// (measured: the per-CTA fixed costs outweigh a fuller grid there).
+extern "C" int32_t cc_attention_splits(int64_t m, int32_t n_q_heads, int32_t n_kv_heads, int64_t n_keys) {
+  static int enabled = -1;  // CC_ATTN_SPLIT=0 in the environment: never split (A/B runs)
+  if (enabled < 0) {
+    const char* e = getenv("CC_ATTN_SPLIT");
+    enabled = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!enabled || m <= 0 || n_kv_heads <= 0 || n_q_heads % n_kv_heads) return 1;
+  if (m * (n_q_heads / n_kv_heads) > 2 * kFaTileRows || n_keys < 4096) return 1;
+  return (int32_t)std::min<int64_t>(kMaxAttnSplits, n_keys / 1024);
+}
+
+extern "C" int cc_sparse_row_attention_split(const void* q, int64_t ldq, const int64_t* positions,
+                                             const int64_t* key_start, int64_t m, const void* k_cache,
+                                             const void* v_cache, int64_t n_keys, int32_t n_q_heads,
+                                             int32_t n_kv_heads, int32_t head_dim, float factor,
+                                             const float* row_factor, int32_t n_splits, float* o_parts,
+                                             float* lse_parts, void* out, int64_t ldo, void* stream) {
+  if (n_splits <= 1)
+    return cc_sparse_row_attention_ranged(q, ldq, positions, key_start, m, k_cache, v_cache, n_keys, n_q_heads,
+                                          n_kv_heads, head_dim, factor, row_factor, out, ldo, stream);
+  CC_CHECK_ARG(n_kv_heads > 0 && n_q_heads % n_kv_heads == 0, CC_ERR_DIMENSION,
+               "query heads %d not a multiple of kv heads %d", n_q_heads, n_kv_heads);
+  CC_CHECK_ARG(head_dim == 64 || head_dim == 128, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
+  CC_CHECK_ARG(n_keys > 0 && n_keys < (int64_t)1 << 31, CC_ERR_VALUE, "bad key bank size");
+  CC_CHECK_ARG(n_splits <= kMaxAttnSplits && o_parts && lse_parts, CC_ERR_VALUE,
+               "split attention needs partial buffers and at most %d parts", kMaxAttnSplits);
+  CC_CHECK_ARG(((uintptr_t)k_cache % 16) == 0 && ((uintptr_t)v_cache % 16) == 0 && ((uintptr_t)q % 16) == 0 &&
+                   (ldq % 8) == 0 && (ldo % 8) == 0,
+               CC_ERR_UNSUPPORTED, "attention operands must be 16-byte aligned");
+  if (m <= 0) return CC_OK;
+  cudaStream_t st = as_stream(stream);
+  const int rc = head_dim == 128
+                     ? fa_launch<128>(q, ldq, positions, key_start, m, k_cache, v_cache, n_keys, n_q_heads,
+                                      n_kv_heads, factor, row_factor, nullptr, 0, st, g_attn_flops, o_parts,
+                                      lse_parts, 0, n_splits)
+                     : fa_launch<64>(q, ldq, positions, key_start, m, k_cache, v_cache, n_keys, n_q_heads,
+                                     n_kv_heads, factor, row_factor, nullptr, 0, st, g_attn_flops, o_parts,
+                                     lse_parts, 0, n_splits);
+  if (rc) return rc;
+  return cc_lse_merge(o_parts, CC_F32, lse_parts, n_splits, m, m, n_q_heads, head_dim, out, ldo, CC_BF16, stream);
 }
 
 extern "C" int cc_sparse_row_attention(const void* q, int64_t ldq, const int64_t* positions, int64_t m,

@@ -6,6 +6,7 @@
 // validation, error codes and the launch profiler are shared.
 #include "cc_common.cuh"
 
+#include <cstdint>
 #include <vector>
 
 extern double g_attn_flops;
@@ -35,6 +36,13 @@ static size_t rows_ws_bytes(const cc_model_desc* md, int64_t R) {
   s += align256(R * ff * 2);         // act
   s += 2 * align256(R * (md->head_dim / 2) * 4);  // cos, sin
   s += align256(64);                 // head workspace
+  // split-KV partials for launches of few rows (decode, the last layer's head
+  // row): sized for the largest split count any key count can ask for
+  const int S = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
+  if (S > 1) {
+    s += align256((size_t)S * R * qw * 4);
+    s += align256((size_t)S * R * md->n_heads * 4);
+  }
   return s;
 }
 
@@ -133,6 +141,9 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
   float* cs = cv.take<float>(R * (md->head_dim / 2));
   float* sn = cv.take<float>(R * (md->head_dim / 2));
   void* hws = cv.take<uint8_t>(64);
+  const int s_max = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
+  float* o_parts = s_max > 1 ? cv.take<float>((size_t)s_max * R * qw) : nullptr;
+  float* lse_parts = s_max > 1 ? cv.take<float>((size_t)s_max * R * md->n_heads) : nullptr;
   CC_TRY(cc_rope_table(positions, R, md->inv_freq, md->head_dim, cs, sn, stream));
   const float factor = (float)(1.0 / sqrt((double)md->head_dim));  // np.float32(1/sqrt(d))
   auto lp = [](const void* base, int64_t stride, int l) -> void* {
@@ -184,12 +195,14 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
     if (Rl > 0) {
       g_attn_flops = 4.0 * md->n_heads * md->head_dim *
                      (r0 == 0 ? attn_pairs : (attn_pairs < 0 ? -1.0 : (double)n_keys * Rl));
-      CC_TRY(cc_sparse_row_attention_ranged(q + r0 * qw, qw, positions + r0,
-                                            plan->key_start ? plan->key_start + r0 : nullptr, Rl,
-                                            lp(plan->attn_k, plan->attn_k_stride, l),
-                                            lp(plan->attn_v, plan->attn_v_stride, l), n_keys, md->n_heads,
-                                            md->n_kv_heads, md->head_dim, factor,
-                                            row_factor ? row_factor + r0 : nullptr, ctx + r0 * qw, qw, stream));
+      const int n_splits = o_parts ? cc_attention_splits(Rl, md->n_heads, md->n_kv_heads, n_keys) : 1;
+      CC_TRY(cc_sparse_row_attention_split(q + r0 * qw, qw, positions + r0,
+                                           plan->key_start ? plan->key_start + r0 : nullptr, Rl,
+                                           lp(plan->attn_k, plan->attn_k_stride, l),
+                                           lp(plan->attn_v, plan->attn_v_stride, l), n_keys, md->n_heads,
+                                           md->n_kv_heads, md->head_dim, factor,
+                                           row_factor ? row_factor + r0 : nullptr, n_splits, o_parts, lse_parts,
+                                           ctx + r0 * qw, qw, stream));
       g_attn_flops = 0.0;
       CC_TRY(gemm_call(CC_GEMM_BF16, CC_EPI_RESIDUAL, Rl, d, qw, ctx + r0 * qw, qw, lw.w_o, qw, lw.b_o, h + r0 * d,
                        d, CC_F32, 0, 0, stream));

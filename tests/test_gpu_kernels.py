@@ -285,6 +285,38 @@ def test_sparse_row_attention(entry, D, Hq, Hkv, m, n, spread):
     assert err < 2e-2, err
 
 
+@pytest.mark.parametrize("m,S", [(1, 32), (1, 7), (5, 16), (36, 4)])
+def test_split_kv_attention_few_rows(m, S):
+    """cc_sparse_row_attention_split (decode steps, the last layer's head row):
+    each CTA's key tiles cut into S parts, fp32 partials merged by
+    log-sum-exp — against the fp64 reference; and the split-count rule."""
+    from paper_2510_10129_b200 import _lib as L
+    D, Hq, Hkv, n = 128, 28, 4, 9000
+    g = torch.Generator(device=DEV).manual_seed(m + S)
+    q = torch.randn(m, Hq, D, device=DEV, generator=g).to(torch.bfloat16)
+    k = (torch.randn(n, Hkv, D, device=DEV, generator=g) * 2).to(torch.bfloat16)
+    v = torch.randn(n, Hkv, D, device=DEV, generator=g).to(torch.bfloat16)
+    pos = torch.arange(n - m, n, device=DEV)  # the newest rows: every key visible
+    pos[0] = min(int(pos[0]), 100)            # one row whose keys end in the first parts
+    out = torch.zeros(m, Hq * D, device=DEV, dtype=torch.bfloat16)
+    o_parts = torch.empty(S, m, Hq, D, device=DEV)
+    lse = torch.empty(S, m, Hq, device=DEV)
+    factor = 1.0 / math.sqrt(D)
+    L.call("cc_sparse_row_attention_split", q.data_ptr(), Hq * D, pos.data_ptr(), None, m, k.data_ptr(),
+           v.data_ptr(), n, Hq, Hkv, D, factor, None, S, o_parts.data_ptr(), lse.data_ptr(), out.data_ptr(),
+           Hq * D, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    ref = _attn_ref(q, k, v, pos + 1, factor)
+    err = (out.double().view(m, Hq, D) - ref).abs().max().item()
+    assert err < 2e-2, err
+    lib = L.load()
+    import os
+    if os.environ.get("CC_ATTN_SPLIT", "1") != "0":
+        assert lib.cc_attention_splits(1, Hq, Hkv, 32800) == 32
+    assert lib.cc_attention_splits(1, Hq, Hkv, 2000) == 1       # short key ranges: never split
+    assert lib.cc_attention_splits(6586, Hq, Hkv, 32800) == 1   # full grids: never split
+
+
 def test_sparse_row_attention_row_factor():
     from paper_2510_10129_b200 import _lib as L
     g = torch.Generator(device=DEV).manual_seed(9)

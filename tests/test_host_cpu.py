@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "cacheclip_sm100.h")
 
 def _declared():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char\*)\s+(cc_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int32_t|int64_t|void|const char\*)\s+(cc_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
