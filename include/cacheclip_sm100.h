@@ -90,13 +90,6 @@ int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_
                    int32_t n_layers, int32_t kv_heads, int32_t head_dim, int32_t dtype,
                    const double* inv_freq_host, int64_t pos_offset,
                    void* dst_k, void* dst_v, int64_t dst_rows_cap, void* stream);
-/* Same, grid capped at max_ctas CTAs (grid-stride): used when the sources are
- * pinned HOST memory read zero-copy over PCIe, so the transfer keeps the link
- * saturated while leaving the SMs to concurrently running kernels. */
-int cc_assemble_kv_capped(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows,
-                          int32_t n_layers, int32_t kv_heads, int32_t head_dim, int32_t dtype,
-                          const double* inv_freq_host, int64_t pos_offset,
-                          void* dst_k, void* dst_v, int64_t dst_rows_cap, int32_t max_ctas, void* stream);
 
 /* Small host -> device upload (tables, ids) read by the SMs straight from
  * pinned host memory (src_pinned: a pinned host pointer, 16-byte aligned),

@@ -558,22 +558,10 @@ int cc_device_check(int dev) {
   return CC_OK;
 }
 
-int cc_assemble_kv_capped(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows, int32_t n_layers,
-                          int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
-                          int64_t pos_offset, void* dst_k, void* dst_v, int64_t dst_rows_cap, int32_t max_ctas,
-                          void* stream);
-
 int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows, int32_t n_layers,
                    int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
                    int64_t pos_offset, void* dst_k, void* dst_v, int64_t dst_rows_cap, void* stream) {
-  return cc_assemble_kv_capped(segs_dev, n_segs, n_dst_rows, n_layers, kv_heads, head_dim, dtype, inv_freq_host,
-                               pos_offset, dst_k, dst_v, dst_rows_cap, 0, stream);
-}
-
-int cc_assemble_kv_capped(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows, int32_t n_layers,
-                          int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
-                          int64_t pos_offset, void* dst_k, void* dst_v, int64_t dst_rows_cap, int32_t max_ctas,
-                          void* stream) {
+  const int32_t max_ctas = 0;  // full grid (the kernel is grid-stride)
   CC_CHECK_ARG(segs_dev && n_segs > 0, CC_ERR_CONSISTENCY, "nothing to merge");
   CC_CHECK_ARG(n_layers > 0 && kv_heads > 0, CC_ERR_DIMENSION, "bad geometry");
   CC_CHECK_ARG(n_dst_rows <= dst_rows_cap, CC_ERR_DIMENSION, "destination capacity %lld < rows %lld",
