@@ -15,7 +15,7 @@ the metadata, so a version-1 reader rejects them with VersionMismatchError
 instead of misreading them.
 
 load_cache returns caches in pinned host memory by default — the form the
-streamed merge consumes zero-copy (merge_caches(..., device=...)), so loading
+streamed merge consumes (copy-engine DMA, merge_caches(..., device=...)), so loading
 from disk overlaps with scoring on the request path — or directly on a device.
 """
 

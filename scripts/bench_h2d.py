@@ -1,4 +1,4 @@
-"""PCIe paths for host-resident chunk caches at C3: zero-copy streamed
+"""PCIe paths for host-resident chunk caches at C3: copy-engine streamed
 assembly (scoring banks, primary merge) vs a plain pinned cudaMemcpy."""
 import os
 import sys
@@ -47,8 +47,8 @@ def timed(fn, label, nbytes):
 
 abytes = sum(c.k.numel() * 4 * 2 for c in ha)
 pbytes = sum(c.k.numel() * 2 * 2 for c in hp)
-timed(lambda: stream_local_banks(ha, aux.config.rope, dev), "scoring banks, zero-copy stream", abytes)
-timed(lambda: cc.merge_caches(hp, primary.config.rope, device=dev), "primary merge, zero-copy stream", pbytes)
+timed(lambda: stream_local_banks(ha, aux.config.rope, dev), "scoring banks, copy-engine stream", abytes)
+timed(lambda: cc.merge_caches(hp, primary.config.rope, device=dev), "primary merge, copy-engine stream", pbytes)
 big = torch.empty(abytes // 4, dtype=torch.float32).pin_memory()
 dst = torch.empty_like(big, device=dev)
 timed(lambda: dst.copy_(big, non_blocking=True), "one pinned cudaMemcpy (copy engine)", abytes)

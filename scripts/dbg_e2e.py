@@ -1,6 +1,6 @@
 """Where does the e2e (host-pinned chunk caches) step lose time against the
 device-resident step?  Wall-clock per step for: device caches, pinned caches
-with the zero-copy streamed merge at several CTA caps, and a bare H2D copy."""
+with the copy-engine streamed merge, and a bare H2D copy."""
 import os
 import sys
 import time
