@@ -469,11 +469,13 @@ def run_ours(args, rank: int, world: int):
             return [pool.store(c) for c in caches]
 
         pc, ac = to_pool(chunks), to_pool(aux_chunks)
-        row_b = lambda c: c.k.shape[2] * c.k.shape[3] * c.k.element_size() * c.n_layers * 2  # noqa: E731  K+V
+        row_b = lambda c, kv: c.k.shape[2] * c.k.shape[3] * c.k.element_size() * kv  # noqa: E731
         # bytes actually moved: the primary's shared prefix once (the merge
-        # dedups it), every scoring cache whole, the query ids
-        h2d = (row_b(pc[0]) * (pc[0].prefix_len + sum(c.chunk_len for c in pc))
-               + sum(row_b(c) * c.n_rows for c in ac) + 8 * len(query))
+        # dedups it), the scoring caches whole except the last layer's values
+        # (the scoring layer reads none), the query ids
+        L_p, L_a = pc[0].n_layers, ac[0].n_layers
+        h2d = (row_b(pc[0], 2 * L_p) * (pc[0].prefix_len + sum(c.chunk_len for c in pc))
+               + sum(row_b(c, 2 * L_a - 1) * c.n_rows for c in ac) + 8 * len(query))
 
         def e2e_step():
             o = cc.cacheclip_prefill(primary, aux, pc, ac, list(query), config)

@@ -101,7 +101,8 @@ int cc_upload(void* dst_dev, const void* src_pinned, int64_t bytes, void* stream
  * layers [layer0, layer0 + n_layers) of every segment (segs_host: a HOST
  * array whose k/v are pinned host pointers) into dst_k / dst_v
  * ([layers][dst_rows_cap][H][D]) at the segments' destination rows, keys still
- * position-free. One cudaMemcpy2DAsync per (segment, K|V): no SM is occupied
+ * position-free (dst_v = NULL: keys only). One cudaMemcpy2DAsync per
+ * (segment, K|V): no SM is occupied
  * by the transfer, so it overlaps scoring and recompute kernels at full PCIe
  * rate. Replaces the per-chunk array reads of merge_caches / attention_banks
  * (kv_store.py:237-248, :106-116) when the caches live in host memory. */
@@ -112,8 +113,8 @@ int cc_h2d_segments(const cc_kv_segment* segs_host, int32_t n_segs, int32_t laye
  * a layer-major HostCachePool) that land back to back: one cudaMemcpy2DAsync
  * per (layer, K|V) moves `width` bytes of every chunk (rows = chunks, source
  * pitch src_chunk_pitch, destination pitch dst_chunk_pitch), layers
- * [layer0, layer0 + n_layers) at the given layer pitches. All sizes in bytes;
- * src pointers are pinned host, dst device. */
+ * [layer0, layer0 + n_layers) at the given layer pitches (dst_v = NULL: keys
+ * only). All sizes in bytes; src pointers are pinned host, dst device. */
 int cc_h2d_uniform(const void* src_k, const void* src_v, int64_t src_chunk_pitch, int64_t src_layer_pitch,
                    void* dst_k, void* dst_v, int64_t width, int64_t dst_layer_pitch, int64_t dst_chunk_pitch,
                    int32_t n_chunks, int32_t layer0, int32_t n_layers, void* stream);

@@ -614,7 +614,7 @@ int cc_h2d_segments(const cc_kv_segment* segs_host, int32_t n_segs, int32_t laye
   CC_CHECK_ARG(segs_host && n_segs > 0, CC_ERR_CONSISTENCY, "nothing to copy");
   CC_CHECK_ARG(layer0 >= 0 && n_layers > 0 && kv_heads > 0 && head_dim > 0, CC_ERR_DIMENSION, "bad geometry");
   CC_CHECK_ARG(dtype == CC_BF16 || dtype == CC_F32, CC_ERR_UNSUPPORTED, "cache dtype %d unsupported", dtype);
-  CC_CHECK_ARG(dst_k && dst_v, CC_ERR_VALUE, "null destination");
+  CC_CHECK_ARG(dst_k, CC_ERR_VALUE, "null destination");  // dst_v == NULL: keys only
   const size_t row_bytes = (size_t)kv_heads * head_dim * (dtype == CC_BF16 ? 2 : 4);
   cudaStream_t st = as_stream(stream);
   for (int i = 0; i < n_segs; ++i) {
@@ -628,7 +628,7 @@ int cc_h2d_segments(const cc_kv_segment* segs_host, int32_t n_segs, int32_t laye
     const size_t width = (size_t)s.n_rows * row_bytes;
     const void* srcs[2] = {s.k, s.v};
     void* dsts[2] = {dst_k, dst_v};
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < (dst_v ? 2 : 1); ++t) {
       cudaError_t e = cudaMemcpy2DAsync(static_cast<uint8_t*>(dsts[t]) + dst_off, dst_rows_cap * row_bytes,
                                         static_cast<const uint8_t*>(srcs[t]) + src_off, s.src_rows * row_bytes,
                                         width, n_layers, cudaMemcpyHostToDevice, st);
@@ -641,7 +641,7 @@ int cc_h2d_segments(const cc_kv_segment* segs_host, int32_t n_segs, int32_t laye
 int cc_h2d_uniform(const void* src_k, const void* src_v, int64_t src_chunk_pitch, int64_t src_layer_pitch,
                    void* dst_k, void* dst_v, int64_t width, int64_t dst_layer_pitch, int64_t dst_chunk_pitch,
                    int32_t n_chunks, int32_t layer0, int32_t n_layers, void* stream) {
-  CC_CHECK_ARG(src_k && src_v && dst_k && dst_v, CC_ERR_VALUE, "null pointer");
+  CC_CHECK_ARG(src_k && dst_k && (!dst_v || src_v), CC_ERR_VALUE, "null pointer");  // dst_v == NULL: keys only
   CC_CHECK_ARG(n_chunks > 0 && layer0 >= 0 && n_layers > 0 && width > 0, CC_ERR_DIMENSION, "bad geometry");
   CC_CHECK_ARG(src_chunk_pitch >= width && dst_chunk_pitch >= width, CC_ERR_DIMENSION,
                "chunk pitch smaller than the copied rows");
@@ -649,7 +649,7 @@ int cc_h2d_uniform(const void* src_k, const void* src_v, int64_t src_chunk_pitch
   for (int l = layer0; l < layer0 + n_layers; ++l) {
     const void* srcs[2] = {src_k, src_v};
     void* dsts[2] = {dst_k, dst_v};
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < (dst_v ? 2 : 1); ++t) {
       cudaError_t e = cudaMemcpy2DAsync(static_cast<uint8_t*>(dsts[t]) + (size_t)l * dst_layer_pitch,
                                         dst_chunk_pitch,
                                         static_cast<const uint8_t*>(srcs[t]) + (size_t)l * src_layer_pitch,

@@ -420,7 +420,7 @@ def _uniform_runs(spec, row_bytes: int) -> list[tuple[int, int]]:
 
 
 def _stream_in(spec, rot: np.ndarray, n_rows: int, k_store: torch.Tensor, v_store: torch.Tensor,
-               rope: RopeParams, groups: dict) -> list:
+               rope: RopeParams, groups: dict, v_layers: int | None = None) -> list:
     """Host-resident (pinned) chunk caches -> k_store / v_store
     ([L][cap][H][D]): per layer group, the copy engines DMA every segment's
     rows on a dedicated copy stream (no SM is spent on the transfer) — runs of
@@ -429,7 +429,8 @@ def _stream_in(spec, rot: np.ndarray, n_rows: int, k_store: torch.Tensor, v_stor
     (chunk, K|V) over the group's layers (cc_h2d_segments) — then the current
     stream rotates the group's keys in place (cc_rope_rows_inplace, segments
     ``rot`` give each row's position). Returns one event per layer, recorded
-    on the current stream after its rotation."""
+    on the current stream after its rotation. ``v_layers``: values are
+    copied for layers < v_layers only (the scoring layer reads no values)."""
     for i, item in enumerate(spec):
         c = item[0]
         if not (c.k.is_pinned() and c.v.is_pinned()):
@@ -448,19 +449,26 @@ def _stream_in(spec, rot: np.ndarray, n_rows: int, k_store: torch.Tensor, v_stor
     v_store.record_stream(cp)
     inv = rope.inv_freq
     ready = []
+    v_end = L if v_layers is None else v_layers
     for l0, l1 in _layer_groups(L, **groups):
-        if singles:
-            _lib.call("cc_h2d_segments", host_segs.ctypes.data, len(singles), l0, l1 - l0, H, D, dt,
-                      k_store.data_ptr(), v_store.data_ptr(), cap, cp.cuda_stream)
-        for i, j in runs:
-            if j - i == 1:
+        # [l0, lv) with values, [lv, l1) keys only
+        for a, b, with_v in ((l0, min(l1, v_end), True), (max(l0, v_end), l1, False)):
+            if a >= b:
                 continue
-            c, s0, d0, n = spec[i][:4]
-            step = spec[i + 1][0].k.data_ptr() - c.k.data_ptr()
-            lstride = c.k.stride(0) * c.k.element_size()
-            _lib.call("cc_h2d_uniform", c.k.data_ptr() + s0 * row_bytes, c.v.data_ptr() + s0 * row_bytes, step,
-                      lstride, k_store.data_ptr() + d0 * row_bytes, v_store.data_ptr() + d0 * row_bytes,
-                      n * row_bytes, cap * row_bytes, n * row_bytes, j - i, l0, l1 - l0, cp.cuda_stream)
+            vdst = v_store.data_ptr() if with_v else None
+            if singles:
+                _lib.call("cc_h2d_segments", host_segs.ctypes.data, len(singles), a, b - a, H, D, dt,
+                          k_store.data_ptr(), vdst, cap, cp.cuda_stream)
+            for i, j in runs:
+                if j - i == 1:
+                    continue
+                c, s0, d0, n = spec[i][:4]
+                step = spec[i + 1][0].k.data_ptr() - c.k.data_ptr()
+                lstride = c.k.stride(0) * c.k.element_size()
+                _lib.call("cc_h2d_uniform", c.k.data_ptr() + s0 * row_bytes, c.v.data_ptr() + s0 * row_bytes,
+                          step, lstride, k_store.data_ptr() + d0 * row_bytes,
+                          v_store.data_ptr() + d0 * row_bytes if with_v else None, n * row_bytes,
+                          cap * row_bytes, n * row_bytes, j - i, a, b - a, cp.cuda_stream)
         copied = torch.cuda.Event()
         copied.record(cp)
         cur.wait_event(copied)
@@ -530,7 +538,8 @@ def stream_local_banks(chunks: Sequence[ChunkCache], rope: RopeParams, device):
     K = torch.empty(L, total, H, D, dtype=first.k.dtype, device=dev)
     V = torch.empty_like(K)
     spec = [(c, 0, int(o), c.n_rows, 0) for c, o in zip(chunks, offs[:-1])]  # pos0 = 0: local positions
-    ready = _stream_in(spec, _segments(spec), total, K, V, rope, SCORING_GROUPS)
+    # the scoring layer (the last) reads no values: its V never crosses PCIe
+    ready = _stream_in(spec, _segments(spec), total, K, V, rope, SCORING_GROUPS, v_layers=L - 1)
     return K, V, offs[:-1], ready
 
 
