@@ -112,12 +112,22 @@ def tensor_shapes(cfg: OracleConfig) -> list[tuple[str, tuple[int, ...]]]:
     return table
 
 
-def seeded_params(cfg: OracleConfig, seed: int, bias_std: float = 0.0) -> dict[str, np.ndarray]:
+def seeded_params(cfg: OracleConfig, seed: int, bias_std: float = 0.0, *,
+                  fast: bool = False) -> dict[str, np.ndarray]:
     """The reference's init recipe (model.py:178-201): N(0, 1/fan_in) weights,
     N(0,1) embedding, N(0, 1/d_model) lm_head, unit gains, zero biases.
     ``bias_std`` > 0 draws non-zero biases afterwards (a test-only knob so the
-    bias path is actually exercised)."""
+    bias path is actually exercised). ``fast`` draws float32 standard normals
+    scaled in float32 (same distribution, different stream; ~2x faster, used
+    for the full-size golden workloads that the GPU box must regenerate)."""
     rng = np.random.default_rng(seed)
+    if fast:
+        def normal(_mean, std, shape):
+            return rng.standard_normal(shape, dtype=F32) * F32(std)
+        rng_normal = normal
+    else:
+        def rng_normal(mean, std, shape):
+            return rng.normal(mean, std, shape).astype(F32)
     fan_in = {"wq": cfg.d_model, "wk": cfg.d_model, "wv": cfg.d_model, "wo": cfg.q_width,
               "w_gate": cfg.d_model, "w_in": cfg.d_model, "w_out": cfg.d_ff}
     params: dict[str, np.ndarray] = {}
@@ -128,11 +138,11 @@ def seeded_params(cfg: OracleConfig, seed: int, bias_std: float = 0.0) -> dict[s
         elif name.endswith(".bias"):
             params[name] = np.zeros(shape, F32)
         elif name == "embed.weight":
-            params[name] = rng.normal(0.0, 1.0, shape).astype(F32)
+            params[name] = rng_normal(0.0, 1.0, shape)
         elif name == "lm_head.weight":
-            params[name] = rng.normal(0.0, cfg.d_model ** -0.5, shape).astype(F32)
+            params[name] = rng_normal(0.0, cfg.d_model ** -0.5, shape)
         else:
-            params[name] = rng.normal(0.0, fan_in[parts[-2]] ** -0.5, shape).astype(F32)
+            params[name] = rng_normal(0.0, fan_in[parts[-2]] ** -0.5, shape)
     if bias_std > 0:
         brng = np.random.default_rng(seed + 1_000_003)
         for name in sorted(params):

@@ -284,11 +284,7 @@ extern "C" int cc_sparse_row_attention_mma(const void* q, int64_t ldq, const int
   cudaStream_t st = as_stream(stream);
   ProfScope ps(st, OP_ATTENTION_MMA, 0);
   if (head_dim == 128) {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(sparse_row_attention_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      set = true;
-    }
+    set_smem_once<sparse_row_attention_kernel<128>>(smem);
     sparse_row_attention_kernel<128><<<grid, kAttnThreads, smem, st>>>(
         (const __nv_bfloat16*)q, ldq, positions, m, (const __nv_bfloat16*)k_cache, (const __nv_bfloat16*)v_cache,
         n_keys, n_q_heads, n_kv_heads, factor, row_factor, (__nv_bfloat16*)out, ldo);

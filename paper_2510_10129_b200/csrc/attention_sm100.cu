@@ -552,11 +552,7 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const
   if (rc) return rc;
   rc = make_kv_map(&tv, v_cache, n_keys, hkv, D);
   if (rc) return rc;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fa_sparse_row_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, FaCfg<D>::SMEM);
-    attr = true;
-  }
+  set_smem_once<fa_sparse_row_kernel<D>>(FaCfg<D>::SMEM);
   const int G = hq / hkv;
   const int n_ctas = (int)((m * G + 2 * kFaTileRows - 1) / (2 * kFaTileRows));
   dim3 grid(n_ctas, hkv, n_splits);
@@ -633,9 +629,10 @@ extern "C" int cc_debug_fa_trace(long long* out) {
 }
 #endif
 
-// algorithmic work of the next attention launch (set by the executor, which
-// knows sum(pos+1) on the host; 0 when unknown)
-double g_attn_flops = 0.0;
+// algorithmic work of the next attention launch, for the launch profiler (set
+// by the executor, which knows sum(pos+1) on the host; 0 when unknown).
+// Thread-local: each host thread driving the library has its own.
+thread_local double g_attn_flops = 0.0;
 
 extern "C" int cc_sparse_row_attention_ranged(const void* q, int64_t ldq, const int64_t* positions,
                                               const int64_t* key_start, int64_t m, const void* k_cache,

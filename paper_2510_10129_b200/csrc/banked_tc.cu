@@ -453,20 +453,12 @@ extern "C" int cc_banked_attention_f32(const cc_bank_seq* seqs_dev, int32_t n_se
   cudaStream_t st = as_stream(stream);
   ProfScope ps(st, OP_BANKED, 0);
   if (head_dim == 64) {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(banked_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, BtCfg<64>::SMEM);
-      set = true;
-    }
+    set_smem_once<banked_tc_kernel<64>>(BtCfg<64>::SMEM);
     banked_tc_kernel<64><<<grid, kBtThreads, BtCfg<64>::SMEM, st>>>(seqs_dev, q, k_new, v_new, n_q_heads,
                                                                       n_kv_heads, factor, qpb, out, out_mode,
                                                                       weights_out, w_col0, w_ld);
   } else {
-    static bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(banked_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, BtCfg<128>::SMEM);
-      set = true;
-    }
+    set_smem_once<banked_tc_kernel<128>>(BtCfg<128>::SMEM);
     banked_tc_kernel<128><<<grid, kBtThreads, BtCfg<128>::SMEM, st>>>(seqs_dev, q, k_new, v_new, n_q_heads,
                                                                         n_kv_heads, factor, qpb, out, out_mode,
                                                                         weights_out, w_col0, w_ld);

@@ -9,7 +9,7 @@
 #include <cstdint>
 #include <vector>
 
-extern double g_attn_flops;
+extern thread_local double g_attn_flops;
 
 namespace cc {
 
@@ -193,8 +193,10 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
     const int64_t r0 = (l == md->n_layers - 1) ? R - tail_rows : 0;
     const int64_t Rl = R - r0;
     if (Rl > 0) {
-      g_attn_flops = 4.0 * md->n_heads * md->head_dim *
-                     (r0 == 0 ? attn_pairs : (attn_pairs < 0 ? -1.0 : (double)n_keys * Rl));
+      // profiler work: the full layer's pairs (-1 = known only after the
+      // selection read-back, filled in by cc_profile_fill_work); a last-layer
+      // tail launch runs only the final row, which sees the whole bank
+      g_attn_flops = 4.0 * md->n_heads * md->head_dim * (r0 == 0 ? attn_pairs : (double)n_keys * Rl);
       const int n_splits = o_parts ? cc_attention_splits(Rl, md->n_heads, md->n_kv_heads, n_keys) : 1;
       CC_TRY(cc_sparse_row_attention_split(q + r0 * qw, qw, positions + r0,
                                            plan->key_start ? plan->key_start + r0 : nullptr, Rl,

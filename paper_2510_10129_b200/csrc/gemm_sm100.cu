@@ -733,11 +733,7 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   if (rc) return rc;
   rc = make_map(&tb, a->B, kTF32, kop, a->N, a->ldb, Cfg::BK, BN / 2);
   if (rc) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm_kernel<BN, kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    attr_set = true;
-  }
+  set_smem_once<gemm_kernel<BN, kTF32>>(Cfg::SMEM_BYTES);
   const int num_m = (int)((a->M + kBM - 1) / kBM);
   const int num_n = (int)((a->N + BN - 1) / BN);
   // 3xTF32 iterates the original K (hi/lo sub-tiles per stage)
@@ -758,11 +754,7 @@ static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, 
   if (rc) return rc;
   rc = make_map(&tb, a->B, kTF32, kop, a->N, a->ldb, Cfg::BK, BN / 2);
   if (rc) return rc;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(gemm2_kernel<BN, kTF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
-    attr_set = true;
-  }
+  set_smem_once<gemm2_kernel<BN, kTF32>>(Cfg::SMEM_BYTES);
   const int num_m2 = (int)((a->M + 255) / 256);
   const int num_n = (int)((a->N + BN - 1) / BN);
   // 3xTF32 iterates the original K (hi/lo sub-tiles per stage)

@@ -120,6 +120,18 @@ def _layer_stride_rows(t: torch.Tensor) -> int:
     return t.stride(0) // (t.shape[2] * t.shape[3]) if t.shape[0] > 1 else t.shape[1]
 
 
+def require_cache_dtype(caches, dtype: torch.dtype, what: str = "cache") -> None:
+    """Every cache's K/V tensors must have the dtype the consuming model
+    computes in (bf16 primary, fp32 scoring model): the kernels read the
+    stores as that type. Raised before any device work (CacheConsistencyError,
+    a ValueError). Reference v1 (.cclp) files are fp32: load them with
+    ``load_cache(path, dtype=torch.bfloat16)`` for a bf16 primary."""
+    for i, c in enumerate(caches):
+        t = c.k_store if isinstance(c, MergedCache) else c.k
+        if t.dtype != dtype:
+            raise CacheConsistencyError(f"{what} {i} holds {t.dtype} K/V but the model computes in {dtype}")
+
+
 class ChunkCache:
     """One chunk processed against the shared prefix, keys position-free."""
 

@@ -18,7 +18,7 @@ from . import _lib
 from .config import ModelConfig
 from .errors import DimensionError
 from .flops import PipelineTrace, trace_layer
-from .kv_store import ChunkCache, MergedCache, host_to_device
+from .kv_store import ChunkCache, MergedCache, host_to_device, require_cache_dtype
 from .runtime import KvPlan, bank_tables, final_logits, forward_banked, forward_rows
 from .weights import Model, from_params, init_model  # noqa: F401  (re-export)
 
@@ -209,6 +209,7 @@ def _check_cache(model: Model, cache) -> None:
                         f"{type(cache).__name__}")
     if cache.k_store.shape[0] != model.config.n_layers:
         raise DimensionError(f"cache has {cache.k_store.shape[0]} layers, model has {model.config.n_layers}")
+    require_cache_dtype([cache], model.wdtype, "merged cache")
 
 
 def _row_factor(model: Model, knobs, n: int, n_plain: int = 0, device=None):
@@ -239,6 +240,7 @@ def forward_on_merged(model: Model, cache: MergedCache, sel_idx: np.ndarray | No
     ``finish_selection`` once the indices are read back."""
     c = model.config
     dev = model.device
+    require_cache_dtype([cache], model.wdtype, "merged cache")
     deferred = sel_idx is None and n_sel is not None
     m = int(n_sel) if deferred else (0 if sel_idx is None else int(sel_idx.size))
     nq = 0 if query_ids is None else len(query_ids)

@@ -70,9 +70,12 @@ def save_cache(cache, path) -> None:
         f.write(bytes(blob))
 
 
-def load_cache(path, *, device=None, pin: bool = True):
+def load_cache(path, *, device=None, pin: bool = True, dtype: torch.dtype | None = None):
     """Read a .cclp file (reference v1 fp32 or v2 bf16). Tensors land on
-    ``device`` if given, else in (pinned) host memory."""
+    ``device`` if given, else in (pinned) host memory. ``dtype`` converts the
+    payload (round-to-nearest-even for fp32 -> bf16), e.g. a reference v1
+    file for a bf16 primary; without it the cache keeps the file's dtype and
+    a model of another dtype rejects it (CacheConsistencyError)."""
     with open(path, "rb") as f:
         blob = f.read()
     if len(blob) < 16:
@@ -105,6 +108,10 @@ def load_cache(path, *, device=None, pin: bool = True):
     if bf16:
         t = t.view(torch.bfloat16)
     k, v = t[:, 0].contiguous(), t[:, 1].contiguous()
+    if dtype is not None and dtype != k.dtype:
+        if dtype not in (torch.float32, torch.bfloat16):
+            raise CacheFormatError(f"unsupported cache dtype {dtype}")
+        k, v = k.to(dtype), v.to(dtype)
     if device is not None:
         k, v = k.to(device), v.to(device)
     elif pin and torch.cuda.is_available():

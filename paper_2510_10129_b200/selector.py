@@ -23,7 +23,7 @@ import torch
 
 from . import _lib
 from .flops import PipelineTrace, trace_layer
-from .kv_store import ChunkCache, host_to_device
+from .kv_store import ChunkCache, host_to_device, require_cache_dtype
 from .runtime import KvPlan, ScoreSpec, bank_tables, forward_banked, forward_rows
 from .tokenizers import TokenSpan, align_spans
 from .weights import Model
@@ -292,6 +292,7 @@ def aux_score_tokens(aux_model: Model, aux_chunk_caches: Sequence[ChunkCache], q
     c = aux_model.config
     if c.dtype != "fp32":
         raise ValueError("the scoring model must run in fp32 mode (exact selection)")
+    require_cache_dtype(aux_chunk_caches, aux_model.wdtype, "aux chunk")
     q = np.asarray(list(query_ids), dtype=np.int64)
     if q.min() < 0 or q.max() >= c.vocab_size:
         raise ValueError(f"token id outside vocab of size {c.vocab_size}")

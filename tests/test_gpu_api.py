@@ -108,3 +108,27 @@ def test_merge_layout_fields(env):
                         chunks[1].model_fingerprint)
     with pytest.raises(cc.CacheConsistencyError):
         cc.merge_caches([chunks[0], bad], model.config.rope)
+
+
+def test_cache_dtype_must_match_model(env, tmp_path):
+    """fp32 chunk caches (a reference v1 .cclp file) given to
+    the bf16 primary raise CacheConsistencyError before any device work, and
+    bf16 caches given to the fp32 scoring model are rejected the same way;
+    ``load_cache(dtype=torch.bfloat16)`` makes the v1 file usable, bitwise
+    equal to the original bf16 caches (bf16 -> fp32 -> bf16 is lossless)."""
+    cc, model, _, prefix, chunk_ids, chunks = env
+    path = tmp_path / "c0.cclp"
+    c0 = chunks[0]
+    cc.save_cache(cc.ChunkCache(c0.k.float().cpu(), c0.v.float().cpu(), c0.token_ids, c0.prefix_len,
+                                c0.tokenizer_id, c0.model_fingerprint), path)
+    assert int.from_bytes(path.read_bytes()[4:8], "little") == 1  # reference format v1 (fp32)
+    v1 = cc.load_cache(path, device="cuda")
+    with pytest.raises(cc.CacheConsistencyError):
+        cc.direct_reuse_prefill(model, [v1] + list(chunks[1:]), [1, 2, 3])
+    with pytest.raises(cc.CacheConsistencyError):
+        cc.cacheclip_prefill(model, model, [v1], [v1], [1, 2, 3], cc.SelectionConfig(0.2))
+    conv = cc.load_cache(path, device="cuda", dtype=torch.bfloat16)
+    assert torch.equal(conv.k, c0.k) and torch.equal(conv.v, c0.v)
+    a = cc.direct_reuse_prefill(model, [conv] + list(chunks[1:]), [1, 2, 3])
+    b = cc.direct_reuse_prefill(model, list(chunks), [1, 2, 3])
+    np.testing.assert_array_equal(a.logits, b.logits)

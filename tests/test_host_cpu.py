@@ -232,17 +232,37 @@ def test_request_validation_raises_before_any_device_work():
 
 def test_bench_reference_arm_json_contract():
     """`bench.py --impl reference` (the CPU reference path, no GPU needed)
-    prints one JSON line with the contract's keys."""
+    prints one JSON line with the contract's keys and the SAME metric string,
+    unit and direction as our arm (so the driver can form the ratio). C1 keeps
+    it fast; the stock reference from oracle/_ref when installed."""
     import json
     import subprocess
     import sys
-    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2510_10129_b200.workloads import WORKLOADS
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
+                        "--steps", "1", "--warmup", "1"], capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "scaling", "dtype", "config", "impl", "cpu_baseline", "e2e"):
         assert key in line, key
     assert line["impl"] == "reference" and line["value"] > 0
-    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["metric"] == bench.metric_name(WORKLOADS["c1"], 0.2)
+    assert line["unit"] == "tok/s" and line["higher_is_better"] is True
+    kind = "reference" if os.path.isdir(os.path.join(ROOT, "oracle", "_ref", "cacheclip")) else "port"
+    assert line["cpu_baseline"]["kind"] == kind and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["value"] == line["value"]
+    if kind == "reference":
+        assert line["c1_check"]["request_ms"] > 0 and line["stages_ms"]["recompute"] > 0
+
+
+def test_bench_metric_matches_baseline():
+    import json
+    import sys
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2510_10129_b200.workloads import WORKLOADS
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        assert bench.metric_name(WORKLOADS["c3"], 0.2) == json.load(f)["metric"]

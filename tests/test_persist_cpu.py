@@ -107,3 +107,21 @@ def test_cache_validation_errors():
     with pytest.raises(CacheConsistencyError):
         MergedCache(keys=keys, values=values, token_ids=[1, 2, 3], layout=MergeLayout(1, (2,)), source=[(0, 0)],
                     tokenizer_id="t", model_fingerprint="m")
+
+
+def test_dtype_conversion_on_load_and_model_dtype_guard():
+    """a reference v1 (fp32) file loads as fp32 and is
+    rejected by a bf16 consumer's dtype guard; ``dtype=`` converts it on load
+    (round-to-nearest-even, bitwise torch's .to(bfloat16))."""
+    from paper_2510_10129_b200.kv_store import require_cache_dtype
+    c = load_cache(os.path.join(GOLDEN, "ref_chunk.cclp"), pin=False)
+    assert c.k.dtype == torch.float32
+    with pytest.raises(CacheConsistencyError):
+        require_cache_dtype([c], torch.bfloat16, "chunk")
+    require_cache_dtype([c], torch.float32, "chunk")
+    b = load_cache(os.path.join(GOLDEN, "ref_chunk.cclp"), pin=False, dtype=torch.bfloat16)
+    assert b.k.dtype == torch.bfloat16 and torch.equal(b.k, c.k.to(torch.bfloat16))
+    assert torch.equal(b.v, c.v.to(torch.bfloat16)) and b.token_ids == c.token_ids
+    require_cache_dtype([b], torch.bfloat16, "chunk")
+    with pytest.raises(CacheFormatError):
+        load_cache(os.path.join(GOLDEN, "ref_chunk.cclp"), pin=False, dtype=torch.float16)
