@@ -171,6 +171,17 @@ typedef struct {
   const int64_t* dst_rows;     /* [M] cache row per GEMM row (NULL: identity)    */
   void* k_raw;                 /* optional position-free K (chunk precompute)    */
   const int64_t* raw_rows;     /* [M] row in k_raw (NULL: identity)              */
+  /* RMSNorm fused across GEMMs (bf16 kind only; rms_norm, tensor_core.py:99-106):
+   * the RESIDUAL epilogue that writes h also writes the next GEMM's A operand
+   * xn = bf16(h * norm_gain) and per-row partial sums of h^2, one per 32-column
+   * chunk: ssq_out[(col / 32) * ld_ssq + m] (N % 32 == 0). A consumer GEMM
+   * (QKV / GLU epilogue) given ssq_in scales each accumulator row by
+   * 1 / sqrt(sum_p ssq_in[p * ld_ssq + m] / norm_d + norm_eps) before the bias:
+   * (h * g) @ W / rms(h) == rms_norm(h) @ W. */
+  void* xn_out; int64_t ldxn; const float* norm_gain;
+  float* ssq_out;
+  const float* ssq_in; int32_t ssq_parts; int32_t norm_d; float norm_eps;
+  int64_t ld_ssq;
 } cc_gemm_args;
 
 int cc_gemm(const cc_gemm_args* args, void* stream);

@@ -53,6 +53,10 @@ class GemmArgs(ctypes.Structure):
         ("dst_rows", vp),
         ("k_raw", vp),
         ("raw_rows", vp),
+        ("xn_out", vp), ("ldxn", i64), ("norm_gain", vp),
+        ("ssq_out", vp),
+        ("ssq_in", vp), ("ssq_parts", i32), ("norm_d", i32), ("norm_eps", f32),
+        ("ld_ssq", i64),
     ]
 
 

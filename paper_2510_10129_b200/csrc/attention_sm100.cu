@@ -132,6 +132,9 @@ __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, float* v) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr)
       : "memory");
+#ifdef CC_SYNC_TMEM_LD  // sanitizer builds: no register is pending an async TMEM load across other code
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#endif
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
@@ -305,7 +308,9 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   }
 
   if (warp < 4) {
+#ifndef CC_NO_SETMAXNREG  // sanitizer builds: no register reallocation under instrumentation
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kFaCtlRegs));
+#endif
     if (warp == 0) {
       // ---------------- TMA producer ----------------
       if (lane == 0 && n_tiles > 0) {
@@ -382,7 +387,9 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       }
     }
   } else {
+#ifndef CC_NO_SETMAXNREG
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kFaSoftmaxRegs));
+#endif
     // ---------------- softmax + epilogue (row per thread) ----------------
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + Cfg::s_col(tq);

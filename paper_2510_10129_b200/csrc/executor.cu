@@ -36,6 +36,7 @@ static size_t rows_ws_bytes(const cc_model_desc* md, int64_t R) {
   s += align256(R * ff * 2);         // act
   s += 2 * align256(R * (md->head_dim / 2) * 4);  // cos, sin
   s += align256(64);                 // head workspace
+  s += align256((size_t)((d + 31) / 32) * R * 4);  // fused RMSNorm partial sums
   // split-KV partials for launches of few rows (decode, the last layer's head
   // row): sized for the largest split count any key count can ask for
   const int S = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
@@ -90,6 +91,92 @@ static int gemm_call(int kind, int epi, int64_t M, int64_t N, int64_t K, const v
     if (rc_) return rc_;   \
   } while (0)
 
+// Fused RMSNorm (bf16 pass): the residual epilogue that writes h also writes
+// the next GEMM's operand bf16(h * gain) and per-row partial sums of h^2; the
+// consumer's epilogue scales rows by 1/rms. CC_FUSED_NORM=0: standalone
+// RMSNorm launches (A/B runs).
+struct NormFuse {
+  void* xn;         // bf16 [rows][d], row-aligned with h
+  float* ssq;       // [d/32][ld]
+  int64_t ld;       // rows of the pass
+  int parts, d;
+  float eps;
+};
+
+static bool fused_norm_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CC_FUSED_NORM");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+static void norm_produce(cc_gemm_args& a, const NormFuse& nf, int64_t r0, const float* gain) {
+  a.xn_out = (uint8_t*)nf.xn + (size_t)r0 * nf.d * 2;
+  a.ldxn = nf.d;
+  a.norm_gain = gain;
+  a.ssq_out = nf.ssq + r0;
+  a.ld_ssq = nf.ld;
+}
+
+static void norm_consume(cc_gemm_args& a, const NormFuse& nf, int64_t r0) {
+  a.ssq_in = nf.ssq + r0;
+  a.ssq_parts = nf.parts;
+  a.norm_d = nf.d;
+  a.norm_eps = nf.eps;
+  a.ld_ssq = nf.ld;
+}
+
+// gate/up on xn (written by the o-proj epilogue, rows scaled by 1/rms in the
+// GLU epilogue) -> down + residual, whose epilogue prepares the next layer's
+// QKV operand (next_gain = next layer's attn_norm; NULL after the last layer)
+static int run_mlp_fused(const cc_model_desc* md, const cc_layer_weights& lw, float* h, void* act, int64_t R,
+                         int64_t r0, const NormFuse& nf, const float* next_gain, void* stream) {
+  const int64_t d = md->d_model, ff = md->d_ff;
+  cc_gemm_args a{};
+  a.kind = CC_GEMM_BF16;
+  a.M = R;
+  a.K = d;
+  a.A = (uint8_t*)nf.xn + (size_t)r0 * d * 2;
+  a.lda = d;
+  a.B = lw.w_up;
+  a.ldb = d;
+  a.bias = lw.b_up;
+  a.C = act;
+  a.ldc = ff;
+  a.c_mode = CC_BF16;
+  a.act = md->act;
+  a.glu_block = 128;
+  if (md->mlp_gated) {
+    a.epilogue = CC_EPI_GLU;
+    a.N = lw.n_up;
+    a.n_out = ff;
+  } else {
+    a.epilogue = CC_EPI_ACT;
+    a.N = ff;
+  }
+  norm_consume(a, nf, r0);
+  if (!md->mlp_gated) return fail(CC_ERR_UNSUPPORTED, "fused RMSNorm needs the gated MLP");
+  CC_TRY(cc_gemm(&a, stream));
+  cc_gemm_args b{};
+  b.kind = CC_GEMM_BF16;
+  b.epilogue = CC_EPI_RESIDUAL;
+  b.M = R;
+  b.N = d;
+  b.K = ff;
+  b.A = act;
+  b.lda = ff;
+  b.B = lw.w_down;
+  b.ldb = ff;
+  b.bias = lw.b_down;
+  b.C = h;
+  b.ldc = d;
+  b.c_mode = CC_F32;
+  if (next_gain) norm_produce(b, nf, r0, next_gain);
+  return cc_gemm(&b, stream);
+}
+
 // RMSNorm -> gate/up (fused activation) -> down + residual
 static int run_mlp(const cc_model_desc* md, const cc_layer_weights& lw, float* h, void* x, void* act, int64_t R,
                    int kind, int x_mode, void* stream) {
@@ -141,6 +228,9 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
   float* cs = cv.take<float>(R * (md->head_dim / 2));
   float* sn = cv.take<float>(R * (md->head_dim / 2));
   void* hws = cv.take<uint8_t>(64);
+  float* ssq = cv.take<float>((size_t)((d + 31) / 32) * R);
+  const bool fuse = fused_norm_enabled() && d % 32 == 0 && md->mlp_gated;
+  const NormFuse nf{x, ssq, R, (int)(d / 32), (int)d, md->norm_eps};
   const int s_max = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
   float* o_parts = s_max > 1 ? cv.take<float>((size_t)s_max * R * qw) : nullptr;
   float* lse_parts = s_max > 1 ? cv.take<float>((size_t)s_max * R * md->n_heads) : nullptr;
@@ -158,7 +248,7 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
     if (l == 0)
       CC_TRY(cc_embed_rmsnorm(ids, R, md->embed, CC_BF16, md->vocab, (int)d, h, lw.attn_norm, md->norm_eps, x,
                               CC_BF16, stream));
-    else
+    else if (!fuse)
       CC_TRY(cc_rmsnorm(h, R, (int)d, d, lw.attn_norm, md->norm_eps, x, CC_BF16, stream));
     cc_gemm_args a{};
     a.kind = CC_GEMM_BF16;
@@ -185,6 +275,7 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
     a.dst_rows = plan->dst_rows;
     a.k_raw = lp(plan->k_raw, plan->k_raw_stride, l);
     a.raw_rows = plan->raw_rows;
+    if (fuse && l > 0) norm_consume(a, nf, 0);  // x = bf16(h * attn_norm) from the previous down epilogue
     CC_TRY(cc_gemm(&a, stream));
     // Last layer: every row's K/V are in the cache now (the QKV epilogue
     // scattered them); its attention output, o-proj and MLP feed nothing but
@@ -206,9 +297,30 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
                                            row_factor ? row_factor + r0 : nullptr, n_splits, o_parts, lse_parts,
                                            ctx + r0 * qw, qw, stream));
       g_attn_flops = 0.0;
-      CC_TRY(gemm_call(CC_GEMM_BF16, CC_EPI_RESIDUAL, Rl, d, qw, ctx + r0 * qw, qw, lw.w_o, qw, lw.b_o, h + r0 * d,
-                       d, CC_F32, 0, 0, stream));
-      CC_TRY(run_mlp(md, lw, h + r0 * d, x, act, Rl, CC_GEMM_BF16, CC_BF16, stream));
+      if (fuse) {
+        cc_gemm_args o{};
+        o.kind = CC_GEMM_BF16;
+        o.epilogue = CC_EPI_RESIDUAL;
+        o.M = Rl;
+        o.N = d;
+        o.K = qw;
+        o.A = ctx + r0 * qw;
+        o.lda = qw;
+        o.B = lw.w_o;
+        o.ldb = qw;
+        o.bias = lw.b_o;
+        o.C = h + r0 * d;
+        o.ldc = d;
+        o.c_mode = CC_F32;
+        norm_produce(o, nf, r0, lw.mlp_norm);
+        CC_TRY(cc_gemm(&o, stream));
+        const float* next_gain = l + 1 < md->n_layers ? md->layers[l + 1].attn_norm : nullptr;
+        CC_TRY(run_mlp_fused(md, lw, h + r0 * d, act, Rl, r0, nf, next_gain, stream));
+      } else {
+        CC_TRY(gemm_call(CC_GEMM_BF16, CC_EPI_RESIDUAL, Rl, d, qw, ctx + r0 * qw, qw, lw.w_o, qw, lw.b_o, h + r0 * d,
+                         d, CC_F32, 0, 0, stream));
+        CC_TRY(run_mlp(md, lw, h + r0 * d, x, act, Rl, CC_GEMM_BF16, CC_BF16, stream));
+      }
     }
   }
   (void)kw;

@@ -28,6 +28,12 @@ constexpr int kBM = 128;
 constexpr int kEpiWarps = 8;  // two per TMEM lane quarter (column halves)
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiStageBytes = 32 * 32 * 4;
+// 3xTF32: K-blocks (32 K each) accumulated in TMEM before the epilogue folds
+// the partial into fp32 registers (see the MMA loop)
+#ifndef CC_TF32_KB_PER_PHASE
+#define CC_TF32_KB_PER_PHASE 4
+#endif
+constexpr int kTf32KbPerPhase = CC_TF32_KB_PER_PHASE;
 
 template <int BN, bool kTF32>
 struct GemmCfg {
@@ -81,7 +87,35 @@ struct EpiParams {
   const int64_t* dst_rows;
   void* k_raw;
   const int64_t* raw_rows;
+  // fused RMSNorm (see cc_gemm_args)
+  void* xn_out;
+  int64_t ldxn;
+  const float* norm_gain;
+  float* ssq_out;
+  const float* ssq_in;
+  int ssq_parts;
+  float inv_norm_d;
+  float norm_eps;
+  int64_t ld_ssq;
 };
+
+// 1 / sqrt(mean(h^2) + eps) of GEMM row m from the producer's per-chunk
+// partial sums (fixed summation order: deterministic)
+__device__ __forceinline__ float row_inv_rms(const EpiParams& ep, int64_t m) {
+  if (m >= ep.M) return 0.f;
+  const float* p = ep.ssq_in + m;
+  float s = 0.f;
+  int i = 0;
+  for (; i + 8 <= ep.ssq_parts; i += 8) {
+    float t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = __ldg(p + (int64_t)(i + j) * ep.ld_ssq);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = __fadd_rn(s, t[j]);
+  }
+  for (; i < ep.ssq_parts; ++i) s = __fadd_rn(s, __ldg(p + (int64_t)i * ep.ld_ssq));
+  return 1.0f / sqrtf(__fadd_rn(__fmul_rn(s, ep.inv_norm_d), ep.norm_eps));
+}
 
 __device__ __forceinline__ float act_apply(int act, float x) {
   return act == CC_ACT_SILU ? silu_f(x) : gelu_tanh_f(x);
@@ -163,34 +197,69 @@ __device__ __forceinline__ void acc_ld16(uint32_t taddr, float* v) {
   }
 }
 
+// gate/up -> act(gate + b_gate) * (up + b_up) for 16 accumulator columns
+// [c, c + 16) of a GLU tile (lane-per-row layout)
+template <int BN>
+__device__ __forceinline__ void glu16(const EpiParams& ep, int nb, int c, float* g16, const float* u16) {
+  const int64_t gcol = b_row<BN>(ep, nb, 0) + c;  // interleaved gate row of column c
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    float g = g16[j], up = u16[j];
+    if (ep.bias) {
+      g += ep.bias[gcol + j];
+      up += ep.bias[gcol + ep.glu_block + j];
+    }
+    g16[j] = __fmul_rn(act_apply(ep.act, g), up);
+  }
+}
+
+template <int BN>
+__device__ __forceinline__ void epilogue_tail(const EpiParams& ep, float* v, int c0, int64_t row0, int nb,
+                                              float* stg, int lane);
+
 template <int BN, bool kTF32>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tbase, int c0, int64_t row0, int nb,
                                                float* stg, int lane) {
   float v[32];
-  int64_t colbase;  // global output column of the chunk's column 0
-  int64_t width;    // logical output width (column bound)
+  const bool scaled = ep.ssq_in != nullptr;
+  const float rs = scaled ? row_inv_rms(ep, row0 + lane) : 1.f;
   if (ep.epilogue == CC_EPI_GLU) {
-    const int64_t gcol = b_row<BN>(ep, nb, 0) + c0;  // interleaved gate row of column c0
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {  // 16 columns at a time (register budget)
       float u[16];
       acc_ld16<BN, kTF32>(tbase + c0 + 16 * hh, v + 16 * hh);
       acc_ld16<BN, kTF32>(tbase + c0 + 16 * hh + BN / 2, u);
+      if (scaled) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float g = v[16 * hh + j], up = u[j];
-        if (ep.bias) {
-          g += ep.bias[gcol + 16 * hh + j];
-          up += ep.bias[gcol + ep.glu_block + 16 * hh + j];
+        for (int j = 0; j < 16; ++j) {
+          v[16 * hh + j] = __fmul_rn(v[16 * hh + j], rs);
+          u[j] = __fmul_rn(u[j], rs);
         }
-        v[16 * hh + j] = __fmul_rn(act_apply(ep.act, g), up);
       }
+      glu16<BN>(ep, nb, c0 + 16 * hh, v + 16 * hh, u);
     }
-    colbase = (int64_t)nb * (BN / 2) + c0;
-    width = ep.n_out;
   } else {
     acc_ld16<BN, kTF32>(tbase + c0, v);
     acc_ld16<BN, kTF32>(tbase + c0 + 16, v + 16);
+    if (scaled) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], rs);
+    }
+  }
+  epilogue_tail<BN>(ep, v, c0, row0, nb, stg, lane);
+}
+
+// v: the 32 output values of accumulator columns [c0, c0 + 32) of this lane's
+// row (GLU: already combined); staged through smem and stored coalesced
+template <int BN>
+__device__ __forceinline__ void epilogue_tail(const EpiParams& ep, float* v, int c0, int64_t row0, int nb,
+                                              float* stg, int lane) {
+  int64_t colbase;  // global output column of the chunk's column 0
+  int64_t width;    // logical output width (column bound)
+  if (ep.epilogue == CC_EPI_GLU) {
+    colbase = (int64_t)nb * (BN / 2) + c0;
+    width = ep.n_out;
+  } else {
     colbase = (int64_t)nb * BN + c0;
     width = ep.N;
   }
@@ -242,17 +311,31 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tba
 #pragma unroll
       for (int ps = 0; ps < 8; ++ps)
         if (ps * 4 + rl < m_left) o[ps] = *reinterpret_cast<const float4*>(hb + (ps * 4 + rl) * ep.ldc);
+      const bool fuse = ep.ssq_out != nullptr;  // next RMSNorm's operand + partial sums
+      const float4 gn = fuse ? *reinterpret_cast<const float4*>(ep.norm_gain + col) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
       for (int ps = 0; ps < 8; ++ps) {
         const int r = ps * 4 + rl;
-        if (r >= m_left) continue;
-        const float4 x = unstage4(stg, r, g);
-        float4 y = o[ps];
-        y.x = __fadd_rn(y.x, x.x + b.x);
-        y.y = __fadd_rn(y.y, x.y + b.y);
-        y.z = __fadd_rn(y.z, x.z + b.z);
-        y.w = __fadd_rn(y.w, x.w + b.w);
-        *reinterpret_cast<float4*>(hb + r * ep.ldc) = y;
+        float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r < m_left) {
+          const float4 x = unstage4(stg, r, g);
+          y = o[ps];
+          y.x = __fadd_rn(y.x, x.x + b.x);
+          y.y = __fadd_rn(y.y, x.y + b.y);
+          y.z = __fadd_rn(y.z, x.z + b.z);
+          y.w = __fadd_rn(y.w, x.w + b.w);
+          *reinterpret_cast<float4*>(hb + r * ep.ldc) = y;
+          if (fuse)
+            store4(ep.xn_out, CC_BF16, row0 + r, ep.ldxn, col, width,
+                   make_float4(__fmul_rn(y.x, gn.x), __fmul_rn(y.y, gn.y), __fmul_rn(y.z, gn.z), __fmul_rn(y.w, gn.w)));
+        }
+        if (fuse) {  // warp-uniform: the 8 lanes of a row reduce their 4 columns in a fixed order
+          float ss = __fmaf_rn(y.w, y.w, __fmaf_rn(y.z, y.z, __fmaf_rn(y.y, y.y, __fmul_rn(y.x, y.x))));
+          ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, 1));
+          ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, 2));
+          ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, 4));
+          if (g == 0 && r < m_left) ep.ssq_out[(colbase >> 5) * ep.ld_ssq + row0 + r] = ss;
+        }
       }
       break;
     }
@@ -317,7 +400,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tba
 template <int BN, bool kTF32>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
-                int num_m, int num_n, int num_kb, int k_orig) {
+                int num_m, int num_n, int num_kb, int k_orig, int kb_per_phase) {
   using Cfg = GemmCfg<BN, kTF32>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -385,11 +468,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    // 3xTF32: the accumulator buffer rotates every kb_per_phase K-blocks (a
+    // "phase"); the epilogue folds each finished phase into fp32 registers with
+    // round-to-nearest adds. The tensor core's accumulation truncates once per
+    // MMA, a bias that grows linearly with the K steps it accumulates; phases
+    // bound that to kb_per_phase * KSTEPS steps (parity at depth).
+    // bf16: one phase per tile (the whole K in one accumulator).
+    const int per_phase = kTF32 ? kb_per_phase : num_kb;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + acc * Cfg::ACC_STRIDE;
+      uint32_t d_tmem = 0;
       for (int kb = 0; kb < num_kb; ++kb) {
+        const int kp = kb % per_phase;
+        if (kp == 0) {
+          mbar_wait(&tempty[acc], acc_phase ^ 1);
+          tc_fence_after();
+          d_tmem = tmem_base + acc * Cfg::ACC_STRIDE;
+        }
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
@@ -403,26 +497,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               // accumulators adjacent TMEM columns, so A_hi is read once; then
               // lo*hi into the correction accumulator
               tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC2,
-                            (kb | k) != 0 ? 1u : 0u);
+                            (kp | k) != 0 ? 1u : 0u);
               tc_mma<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + Cfg::A_SUB + k * 32), umma_desc_sw128(b0 + k * 32),
                             Cfg::IDESC, 1u);
             } else {
               tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
-                            (kb | k) != 0 ? 1u : 0u);
+                            (kp | k) != 0 ? 1u : 0u);
             }
           }
           tc_commit(&empty[stage]);
-          if (kb == num_kb - 1) tc_commit(&tfull[acc]);
+          if (kp == per_phase - 1 || kb == num_kb - 1) tc_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == Cfg::STAGES) {
           stage = 0;
           phase ^= 1;
         }
-      }
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
+        if (kp == per_phase - 1 || kb == num_kb - 1) {
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
       }
     }
   } else {
@@ -434,22 +530,67 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     // GLU tiles produce BN/2 output columns (gate/up pairs), others BN
-    const int cols = (ep.epilogue == CC_EPI_GLU) ? BN / 2 : BN;
+    const bool glu = ep.epilogue == CC_EPI_GLU;
+    const int cols = glu ? BN / 2 : BN;
     const int c_begin = chalf * (cols / 2), c_end = c_begin + cols / 2;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
       const int mb = t % num_m, nb = t / num_m;
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t tbase = tmem_base + acc * Cfg::ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
       const int64_t row0 = (int64_t)mb * kBM + quarter * 32;
-      for (int c0 = c_begin; c0 < c_end; c0 += 32)
-        epilogue_chunk<BN, kTF32>(ep, tbase, c0, row0, nb, stg, lane);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
+      if constexpr (kTF32) {
+        // this warp's accumulator columns, BN/2 per row (GLU: its gate columns
+        // then the matching up columns), summed over the phases in registers
+        constexpr int NV = BN / 2;
+        float run[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) run[j] = 0.f;
+        const int n_phases = (num_kb + kb_per_phase - 1) / kb_per_phase;
+        for (int ph = 0; ph < n_phases; ++ph) {
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t tb = tmem_base + acc * Cfg::ACC_STRIDE + lane_off;
+#pragma unroll
+          for (int j = 0; j < NV; j += 16) {
+            const int col = (glu && j >= NV / 2) ? c_begin + BN / 2 + (j - NV / 2) : c_begin + j;
+            float m16[16], c16[16];
+            tmem_ld16(tb + col, m16);
+            tmem_ld16(tb + BN + col, c16);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) run[j + i] = __fadd_rn(run[j + i], __fadd_rn(m16[i], c16[i]));
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+        if (glu) {
+          // NV/2 = BN/4 output columns: one 32-column chunk (BN = 128)
+#pragma unroll
+          for (int cc = 0; cc < NV / 2; cc += 32) {
+            glu16<BN>(ep, nb, c_begin + cc, run + cc, run + NV / 2 + cc);
+            glu16<BN>(ep, nb, c_begin + cc + 16, run + cc + 16, run + NV / 2 + cc + 16);
+            epilogue_tail<BN>(ep, run + cc, c_begin + cc, row0, nb, stg, lane);
+          }
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < NV; cc += 32) epilogue_tail<BN>(ep, run + cc, c_begin + cc, row0, nb, stg, lane);
+        }
+      } else {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t tbase = tmem_base + acc * Cfg::ACC_STRIDE + lane_off;
+        for (int c0 = c_begin; c0 < c_end; c0 += 32)
+          epilogue_chunk<BN, kTF32>(ep, tbase, c0, row0, nb, stg, lane);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       }
     }
   }
@@ -587,6 +728,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   }
   tc_fence_before();
   cluster_sync_all();
+  __syncthreads();  // also a CTA barrier for tools that do not model barrier.cluster (racecheck)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -741,7 +883,8 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   const int tiles = num_m * num_n;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
-  gemm_kernel<BN, kTF32><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb, (int)a->K);
+  gemm_kernel<BN, kTF32><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb, (int)a->K,
+                                                                      kTF32 ? kTf32KbPerPhase : num_kb);
   CC_LAUNCH_CHECK("gemm");
   return CC_OK;
 }
@@ -774,18 +917,6 @@ static bool pair_enabled() {
   if (on < 0) {
     const char* e = getenv("CC_GEMM_PAIR");
     on = (e && e[0] == '0') ? 0 : 1;
-  }
-  return on == 1;
-}
-
-// CC_GEMM_PAIR_TF32=1 runs the large 3xTF32 GEMMs on CTA pairs. Off by default:
-// bitwise equal to the single-CTA kernel but measured no faster (C3 scoring
-// GEMMs 11.29 vs 10.98 ms/step), so operand traffic is not what bounds them.
-static bool tf32_pair_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("CC_GEMM_PAIR_TF32");
-    on = (e && e[0] == '1') ? 1 : 0;
   }
   return on == 1;
 }
@@ -840,6 +971,29 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   ep.dst_rows = a->dst_rows;
   ep.k_raw = a->k_raw;
   ep.raw_rows = a->raw_rows;
+  ep.xn_out = a->xn_out;
+  ep.ldxn = a->ldxn;
+  ep.norm_gain = a->norm_gain;
+  ep.ssq_out = a->ssq_out;
+  ep.ssq_in = a->ssq_in;
+  ep.ssq_parts = a->ssq_parts;
+  ep.inv_norm_d = a->norm_d > 0 ? 1.0f / (float)a->norm_d : 0.f;
+  ep.norm_eps = a->norm_eps;
+  ep.ld_ssq = a->ld_ssq;
+  if (a->ssq_out || a->ssq_in) {
+    CC_CHECK_ARG(!tf32, CC_ERR_UNSUPPORTED, "fused RMSNorm runs on bf16 GEMMs");
+    CC_CHECK_ARG(a->ld_ssq >= a->M, CC_ERR_DIMENSION, "ld_ssq %lld < M %lld", (long long)a->ld_ssq,
+                 (long long)a->M);
+  }
+  if (a->ssq_out) {
+    CC_CHECK_ARG(a->epilogue == CC_EPI_RESIDUAL && a->N % 32 == 0 && a->xn_out && a->norm_gain &&
+                     a->ldxn % 4 == 0 && ((uintptr_t)a->xn_out % 16) == 0 && ((uintptr_t)a->norm_gain % 16) == 0,
+                 CC_ERR_UNSUPPORTED, "RMSNorm partials come from a RESIDUAL epilogue with N %% 32 == 0, xn and gain");
+  }
+  if (a->ssq_in) {
+    CC_CHECK_ARG((a->epilogue == CC_EPI_QKV_ROPE || a->epilogue == CC_EPI_GLU) && a->ssq_parts > 0 && a->norm_d > 0,
+                 CC_ERR_UNSUPPORTED, "row RMS scaling applies to QKV / GLU epilogues with ssq_parts, norm_d");
+  }
   bool wide;
   if (a->epilogue == CC_EPI_GLU) {
     CC_CHECK_ARG(a->glu_block == 128 && a->N % 256 == 0, CC_ERR_UNSUPPORTED,
@@ -859,7 +1013,6 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   cudaStream_t st = as_stream(stream);
   // 3xTF32 runs 128-wide tiles: two accumulators (hi*hi, corrections) x two buffers fill TMEM
   if (tf32) {
-    if (tf32_pair_enabled() && a->M >= 1024 && a->N % 128 == 0) return launch_pair<128, true>(a, ep, kop, st);
     // small-M scoring GEMMs (few chunks): 64-wide tiles double the CTAs when
     // 128-wide tiles would leave over half the SMs idle (GLU tiles need >= 128)
     const int64_t t128 = ((a->M + kBM - 1) / kBM) * ((a->N + 127) / 128);

@@ -123,12 +123,13 @@ class RowPlan:
     own: list[np.ndarray]    # per rank: indices into pos of its rows (ascending)
 
     @classmethod
-    def build(cls, plan: ShardPlan, selected: np.ndarray) -> "RowPlan":
+    def build(cls, plan: ShardPlan, selected: np.ndarray, parts: int = 1) -> "RowPlan":
         q = np.arange(plan.total, plan.total + plan.query_len, dtype=np.int64)
         pos = np.concatenate([np.asarray(selected, dtype=np.int64), q])
         owner = plan.owner_of_positions(pos)
         own = [np.flatnonzero(owner == r) for r in range(plan.world)]
         r_max = max(1, max(len(o) for o in own))
+        r_max = -(-r_max // parts) * parts   # slots split evenly into the pipeline's parts
         packed = np.full(plan.world * r_max, -1, dtype=np.int64)
         for r, o in enumerate(own):
             packed[r * r_max:r * r_max + len(o)] = pos[o]
@@ -138,31 +139,83 @@ class RowPlan:
 # ---------------------------------------------------------------------------
 # collectives
 # ---------------------------------------------------------------------------
+def _wire(t: torch.Tensor) -> torch.Tensor:
+    """bf16 payloads travel as int16 (same bytes) over backends without bf16."""
+    return t.view(torch.int16) if t.dtype == torch.bfloat16 else t
+
+
+class _Done:
+    """Handle of a collective that already completed (world 1, host-staged)."""
+
+    def __init__(self, t: torch.Tensor) -> None:
+        self.t = t
+
+    def wait(self) -> torch.Tensor:
+        return self.t
+
+
+class _Pending:
+    """Handle of an in-flight NCCL collective: ``wait()`` orders the current
+    stream after it (no host block) and returns the output tensor."""
+
+    def __init__(self, work, t: torch.Tensor) -> None:
+        self.work, self.t = work, t
+
+    def wait(self) -> torch.Tensor:
+        self.work.wait()
+        return self.t
+
+
 class Exchange:
-    """The three collectives of the sharded path over torch.distributed
-    (world 1: local copies)."""
+    """The collectives of the sharded path over torch.distributed (world 1:
+    local copies). NCCL moves device tensors directly and can run
+    asynchronously (``async_op=True``: the collective runs on NCCL's stream
+    while the caller launches more work; ``wait()`` on the handle orders the
+    compute stream after it). A gloo group (the CPU tests, or several ranks
+    sharing one GPU) stages device tensors through host memory."""
 
     def __init__(self, world: int, group=None) -> None:
         self.world = world
         self.group = group
+        self._gloo = None
 
-    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+    def _host_staged(self, t: torch.Tensor) -> bool:
+        if not t.is_cuda:
+            return False
+        if self._gloo is None:
+            import torch.distributed as dist
+            self._gloo = dist.get_backend(self.group) == "gloo"
+        return self._gloo
+
+    def all_gather(self, t: torch.Tensor, async_op: bool = False):
         """[n, ...] on every rank -> [W * n, ...] in rank order."""
         if self.world == 1:
-            return t
+            return _Done(t) if async_op else t
         import torch.distributed as dist
+        if self._host_staged(t):
+            src = _wire(t.detach().cpu().contiguous())
+            out = torch.empty((self.world * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype)
+            dist.all_gather_into_tensor(out, src, group=self.group)
+            res = out.view(t.dtype).to(t.device)
+            return _Done(res) if async_op else res
         out = torch.empty((self.world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
-        return out
+        work = dist.all_gather_into_tensor(out, t.contiguous(), group=self.group, async_op=async_op)
+        return _Pending(work, out) if async_op else out
 
-    def all_to_all(self, t: torch.Tensor) -> torch.Tensor:
+    def all_to_all(self, t: torch.Tensor, async_op: bool = False):
         """[W * n, ...]: slot s goes to rank s; returns [W * n, ...] with slot w from rank w."""
         if self.world == 1:
-            return t
+            return _Done(t) if async_op else t
         import torch.distributed as dist
+        if self._host_staged(t):
+            src = _wire(t.detach().cpu().contiguous())
+            out = torch.empty_like(src)
+            dist.all_to_all_single(out, src, group=self.group)
+            res = out.view(t.dtype).to(t.device)
+            return _Done(res) if async_op else res
         out = torch.empty_like(t)
-        dist.all_to_all_single(out, t.contiguous(), group=self.group)
-        return out
+        work = dist.all_to_all_single(out, t.contiguous(), group=self.group, async_op=async_op)
+        return _Pending(work, out) if async_op else out
 
 
 # ---------------------------------------------------------------------------
@@ -189,10 +242,18 @@ class ShardedOutcome:
 
 def cacheclip_prefill_sharded(compute: ShardCompute, exchange: Exchange, plan: ShardPlan, chunks_local: list,
                               aux_chunks_local: list, chunk_token_ids: dict, query_ids: Sequence[int],
-                              config: SelectionConfig, *, n_layers: int, knobs=None) -> ShardedOutcome:
+                              config: SelectionConfig, *, n_layers: int, knobs=None,
+                              pipeline: int = 2) -> ShardedOutcome:
     """One sequence-sharded CacheClip request. chunks_local / aux_chunks_local
     are this rank's chunk caches (plan.local_chunks() order); chunk_token_ids
-    maps each local chunk to its body token ids (for the recompute rows)."""
+    maps each local chunk to its body token ids (for the recompute rows).
+
+    ``pipeline=2`` (computes with ``supports_parts``): each rank's exchange
+    slots are split in two halves that flow through the layer independently,
+    so the Q all_gather of half 1 overlaps the partial attention of half 0,
+    the partial all_to_all of half 0 overlaps the partial attention of half
+    1, and that of half 1 overlaps the LSE merge + o-proj + MLP of half 0
+    (async NCCL collectives; the compute stream waits per half)."""
     W, r = plan.world, plan.rank
     # 1. shard assembly at global positions (no communication)
     compute.assemble(chunks_local, plan)
@@ -214,7 +275,8 @@ def cacheclip_prefill_sharded(compute: ShardCompute, exchange: Exchange, plan: S
     scores = gathered.index_select(0, perm)
     selected = compute.select(scores, plan.chunk_lens, config, plan.prefix_len)
     # 3. row plan (same on every rank) and the recompute + query pass
-    rows = RowPlan.build(plan, selected)
+    parts = 2 if pipeline >= 2 and getattr(compute, "supports_parts", False) else 1
+    rows = RowPlan.build(plan, selected, parts)
     own_pos = rows.pos[rows.own[r]]
     starts = plan.chunk_start
     own_ids = np.empty(own_pos.size, dtype=np.int64)
@@ -225,13 +287,23 @@ def cacheclip_prefill_sharded(compute: ShardCompute, exchange: Exchange, plan: S
             c = int(np.searchsorted(starts, p, side="right") - 1)
             own_ids[k] = chunk_token_ids[c][p - starts[c]]
     compute.begin(rows, plan, own_ids, knobs)
+    H = rows.r_max // parts
     for layer in range(n_layers):
         q_local = compute.pre_attention(layer)                  # [r_max, Hq*D], own rows first
-        q_all = exchange.all_gather(q_local)                     # [W * r_max, Hq*D]
-        o_part, lse = compute.partial_attention(layer, q_all)    # vs this shard's keys
-        o_recv = exchange.all_to_all(o_part)                     # slot w: partials of my rows from rank w
-        lse_recv = exchange.all_to_all(lse)
-        compute.post_attention(layer, o_recv, lse_recv)          # LSE merge, o-proj, MLP
+        if parts == 1:
+            q_all = exchange.all_gather(q_local)                     # [W * r_max, Hq*D]
+            o_part, lse = compute.partial_attention(layer, q_all)    # vs this shard's keys
+            o_recv = exchange.all_to_all(o_part)                     # slot w: partials of my rows from rank w
+            lse_recv = exchange.all_to_all(lse)
+            compute.post_attention(layer, o_recv, lse_recv)          # LSE merge, o-proj, MLP
+            continue
+        gathers = [exchange.all_gather(q_local[p * H:(p + 1) * H], async_op=True) for p in range(parts)]
+        sends = []
+        for p in range(parts):
+            o_part, lse = compute.partial_attention(layer, gathers[p].wait(), part=p)
+            sends.append((exchange.all_to_all(o_part, async_op=True), exchange.all_to_all(lse, async_op=True)))
+        for p, (o_h, l_h) in enumerate(sends):
+            compute.post_attention(layer, o_h.wait(), l_h.wait(), part=p)
     logits = first = None
     if r == plan.head_rank:
         lg = compute.logits()
@@ -243,6 +315,8 @@ def cacheclip_prefill_sharded(compute: ShardCompute, exchange: Exchange, plan: S
 class DeviceShardCompute:
     """The sm_100a kernels behind the sharded orchestration (bf16 primary,
     fp32 scoring model)."""
+
+    supports_parts = True   # pipelined halves (cacheclip_prefill_sharded pipeline=2)
 
     def __init__(self, primary, aux) -> None:
         self.p = primary
@@ -329,6 +403,20 @@ class DeviceShardCompute:
         # bf16 partials: half the all_to_all and merge bytes (merged in fp32)
         self.o_part = torch.empty(W * R, c.n_heads, c.d_head, dtype=torch.bfloat16, device=self.dev)
         self.lse = torch.empty(W * R, c.n_heads, dtype=torch.float32, device=self.dev)
+        # pipelined halves: per-part limits / factors in [W][R/2] order and
+        # separate partial buffers (half 0 is in flight while half 1 computes)
+        self.part_rows = R // 2 if R % 2 == 0 else 0
+        if self.part_rows:
+            Hh = self.part_rows
+            lim = self.limits.view(W, R)
+            self.part_limits = [lim[:, p * Hh:(p + 1) * Hh].reshape(-1).contiguous() for p in range(2)]
+            self.part_factor = None
+            if self.row_factor is not None:
+                rf = self.row_factor.view(W, R)
+                self.part_factor = [rf[:, p * Hh:(p + 1) * Hh].reshape(-1).contiguous() for p in range(2)]
+            self.part_o = [torch.empty(W * Hh, c.n_heads, c.d_head, dtype=torch.bfloat16, device=self.dev)
+                           for _ in range(2)]
+            self.part_lse = [torch.empty(W * Hh, c.n_heads, dtype=torch.float32, device=self.dev) for _ in range(2)]
 
     def _s(self) -> int:
         return torch.cuda.current_stream().cuda_stream
@@ -352,29 +440,43 @@ class DeviceShardCompute:
                  heads=(c.n_heads, c.kv_heads, c.d_head))
         return self.q
 
-    def partial_attention(self, layer: int, q_all: torch.Tensor):
+    def partial_attention(self, layer: int, q_all: torch.Tensor, part: int | None = None):
         c = self.p.config
         qw = c.attn_width
         factor = float(np.float32(1.0 / math.sqrt(c.d_head)))
-        _lib.call("cc_sparse_row_attention_partial", q_all.data_ptr(), qw, self.limits.data_ptr(), q_all.shape[0],
+        if part is None:
+            lim, rf, o, lse = self.limits, self.row_factor, self.o_part, self.lse
+        else:
+            lim, o, lse = self.part_limits[part], self.part_o[part], self.part_lse[part]
+            rf = self.part_factor[part] if self.part_factor is not None else None
+        _lib.call("cc_sparse_row_attention_partial", q_all.data_ptr(), qw, lim.data_ptr(), q_all.shape[0],
                   self.k[layer].data_ptr(), self.v[layer].data_ptr(), self.local_pos.numel(), c.n_heads, c.kv_heads,
-                  c.d_head, factor, self.row_factor.data_ptr() if self.row_factor is not None else None,
-                  self.o_part.data_ptr(), _lib.CC_BF16, self.lse.data_ptr(), self._s())
-        return self.o_part, self.lse
+                  c.d_head, factor, rf.data_ptr() if rf is not None else None,
+                  o.data_ptr(), _lib.CC_BF16, lse.data_ptr(), self._s())
+        return o, lse
 
-    def post_attention(self, layer: int, o_recv: torch.Tensor, lse_recv: torch.Tensor) -> None:
+    def post_attention(self, layer: int, o_recv: torch.Tensor, lse_recv: torch.Tensor,
+                       part: int | None = None) -> None:
         from .runtime import _mlp, gemm
         c = self.p.config
         lw = self.p.layers[layer]
-        n, d, qw = self.n_own, c.d_model, c.attn_width
-        if not n:
+        d, qw = c.d_model, c.attn_width
+        W = self.plan.world
+        if part is None:
+            a, b, stride = 0, self.n_own, self.rows.r_max
+        else:
+            stride = self.part_rows
+            a, b = part * stride, min(self.n_own, (part + 1) * stride)
+        n = b - a
+        if n <= 0:
             return
-        W, R = self.plan.world, self.rows.r_max
-        _lib.call("cc_lse_merge", o_recv.data_ptr(), _lib.CC_BF16, lse_recv.data_ptr(), W, R, n, c.n_heads, c.d_head,
-                  self.ctx.data_ptr(), qw, _lib.CC_BF16, self._s())
-        gemm(_lib.CC_GEMM_BF16, _lib.CC_EPI_RESIDUAL, n, d, qw, self.ctx, lw.w_o, bias=lw.b_o, C=self.h, ldc=d,
+        ctx = self.ctx[a:b]
+        _lib.call("cc_lse_merge", o_recv.data_ptr(), _lib.CC_BF16, lse_recv.data_ptr(), W, stride, n, c.n_heads,
+                  c.d_head, ctx.data_ptr(), qw, _lib.CC_BF16, self._s())
+        h = self.h[a:b]
+        gemm(_lib.CC_GEMM_BF16, _lib.CC_EPI_RESIDUAL, n, d, qw, ctx, lw.w_o, bias=lw.b_o, C=h, ldc=d,
              c_mode=_lib.CC_F32)
-        _mlp(self.p, lw, self.h[:n], self.x[:n], self.act[:n], _lib.CC_GEMM_BF16, _lib.CC_BF16)
+        _mlp(self.p, lw, h, self.x[a:b], self.act[a:b], _lib.CC_GEMM_BF16, _lib.CC_BF16)
 
     def logits(self) -> torch.Tensor:
         from .runtime import final_logits

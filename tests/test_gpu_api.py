@@ -132,3 +132,53 @@ def test_cache_dtype_must_match_model(env, tmp_path):
     a = cc.direct_reuse_prefill(model, [conv] + list(chunks[1:]), [1, 2, 3])
     b = cc.direct_reuse_prefill(model, list(chunks), [1, 2, 3])
     np.testing.assert_array_equal(a.logits, b.logits)
+
+
+_FUSE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2510_10129_b200 as cc
+from oracle import cacheclip_oracle as orc
+from oracle.synth import C1
+w = C1
+oc = w.primary
+cfg = cc.ModelConfig(n_layers=oc.n_layers, n_heads=oc.n_heads, d_model=oc.d_model, d_head=oc.d_head, d_ff=oc.d_ff,
+                     vocab_size=oc.vocab_size, rope_base=oc.rope_base, norm_eps=oc.norm_eps,
+                     activation=oc.activation, mlp_gated=oc.mlp_gated, n_kv_heads=oc.kv_heads, dtype="bf16",
+                     tokenizer_id="chars")
+p = orc.seeded_params(oc, 0)
+rng = np.random.default_rng(3)
+for k in p:   # non-trivial norm gains so the folding is exercised
+    if k.endswith(".gain"):
+        p[k] = (1.0 + 0.25 * rng.standard_normal(p[k].shape)).astype(np.float32)
+model = cc.from_params(cfg, p)
+prefix, chunk_ids, query = w.token_ids(0)
+ids = prefix + sum(chunk_ids, []) + query
+out = cc.full_attention_prefill(model, ids)
+np.save(sys.argv[2], out.logits)
+"""
+
+
+def test_fused_rmsnorm_matches_standalone(tmp_path):
+    """The bf16 pass folds RMSNorm into the GEMMs (the residual epilogue writes
+    bf16(h * gain) and per-row partial sums of h^2, the QKV / GLU epilogues
+    scale rows by 1/rms). Against standalone RMSNorm launches
+    (CC_FUSED_NORM=0) the dense prefill's logits agree within bf16 rounding,
+    and both agree with the fp32 oracle at the same tolerance."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for flag in ("1", "0"):
+        f = tmp_path / f"logits_{flag}.npy"
+        r = subprocess.run([sys.executable, "-c", _FUSE_SCRIPT, root, str(f)], env=dict(os.environ, CC_FUSED_NORM=flag),
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[flag] = np.load(f)
+    fused, plain = outs["1"], outs["0"]
+    std = plain.std()
+    d = np.abs(fused - plain).max()
+    print(f"fused vs standalone RMSNorm: max|dlogits| {d:.3e} (std {std:.3f})")
+    assert d < 2e-2 * std
+    assert not np.array_equal(fused, plain)  # the fused path really ran

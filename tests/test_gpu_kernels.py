@@ -63,19 +63,21 @@ def test_gemm_tf32x3_is_fp32_faithful(M, N, K):
     fp32 = (a @ b.t()).double()
     err32 = ((fp32 - ref).abs() / ref.abs().clamp_min(1.0)).max().item()
     print(f"tf32x3 M={M} N={N} K={K}: max rel err {err:.2e} (fp32 sgemm {err32:.2e})")
-    # tensor-core fp32 accumulation truncates once per MMA step (K=8 slice):
-    # worst case ~ (3K/8) * 2^-23 relative, same order as cuBLAS fp32 here
-    assert err < 5 * (3 * K / 8) * 2.0 ** -23, (err, err32)
+    # tensor-core fp32 accumulation truncates once per MMA step (K=8 slice);
+    # the phased accumulation folds every 128 K into fp32 registers (round to
+    # nearest), so the truncation bias is bounded per phase, not per K
+    phase_k = min(K, 128)
+    assert err < 5 * (3 * phase_k / 8) * 2.0 ** -23 + 4 * err32, (err, err32)
 
 
-_PAIR_SCRIPT = r"""
-import math, sys, torch
-sys.path.insert(0, sys.argv[1])
-from paper_2510_10129_b200 import _lib as L, runtime
-L.load()
-DEV = "cuda"
-M, K = 2048, 896
-for epi in ("store", "glu", "residual"):
+@pytest.mark.parametrize("epi", ["store", "glu", "residual"])
+def test_gemm_tf32x3_row_blocks_bitwise_equal(epi):
+    """Every output element of the phased 3xTF32 GEMM accumulates the same
+    MMAs, phases and register sums whatever the tiling: an M=2048 GEMM equals
+    its four 512-row blocks bitwise (128- vs 64-wide tiles for store/residual;
+    the GLU register epilogue)."""
+    from paper_2510_10129_b200 import _lib as L, runtime
+    M, K = 2048, 896
     N = 2 * 1024 if epi == "glu" else 1152
     n_out = N // 2 if epi == "glu" else N
     g = torch.Generator(device=DEV).manual_seed(11)
@@ -97,29 +99,16 @@ for epi in ("store", "glu", "residual"):
         runtime.gemm(L.CC_GEMM_TF32X3, e, r1 - r0, N, K, A[r0:r1], B, **kw)
         return C
 
-    whole = run(0, M)                                           # CTA-pair kernel (M >= 1024)
-    blocks = torch.cat([run(r, r + 512) for r in range(0, M, 512)])  # single-CTA kernel
+    whole = run(0, M)
+    blocks = torch.cat([run(r, r + 512) for r in range(0, M, 512)])
     torch.cuda.synchronize()
     assert torch.equal(whole, blocks), epi
-print("pair == single")
-"""
-
-
-def test_gemm_tf32x3_pair_bitwise_equals_single_cta():
-    """With CC_GEMM_PAIR_TF32=1, M >= 1024 runs the 3xTF32 GEMM on CTA pairs
-    (cta_group::2; off by default, measured no faster). Every output element
-    accumulates the same MMAs in the same order as the single-CTA kernel, so
-    the pair result must equal the stacked 512-row blocks bitwise (store,
-    GLU and residual epilogues). The env var is read once per process: the
-    check runs in a subprocess."""
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CC_GEMM_PAIR_TF32="1")
-    r = subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root], env=env, capture_output=True, text=True,
-                       timeout=300)
-    assert r.returncode == 0 and "pair == single" in r.stdout, r.stderr[-2000:]
+    if epi == "glu":   # and the GLU math against fp64
+        ref = (a.double() @ b.double().t()).view(M, -1, 2, 128)
+        gt, up = ref[:, :, 0].reshape(M, -1), ref[:, :, 1].reshape(M, -1)
+        want = torch.nn.functional.silu(gt) * up
+        err = ((whole.double() - want).abs() / want.abs().clamp_min(1.0)).max().item()
+        assert err < 1e-5, err
 
 
 @pytest.mark.parametrize("epi", ["store", "residual"])

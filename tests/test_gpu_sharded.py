@@ -79,6 +79,14 @@ def _cfg(oc, dtype):
                        mlp_bias=oc.mlp_bias, tokenizer_id="chars", n_kv_heads=oc.kv_heads, dtype=dtype)
 
 
+class _Done:
+    def __init__(self, t):
+        self.t = t
+
+    def wait(self):
+        return self.t
+
+
 class ThreadExchange:
     """In-process stand-in for torch.distributed collectives between rank threads."""
 
@@ -93,7 +101,9 @@ class ThreadExchange:
         class _E:
             world = ex.world
 
-            def all_gather(self, t):
+            def all_gather(self, t, async_op=False):
+                if async_op:
+                    return _Done(self.all_gather(t))
                 torch.cuda.current_stream().synchronize()
                 ex.slots[r] = t
                 ex.bar.wait()
@@ -102,7 +112,9 @@ class ThreadExchange:
                 ex.bar.wait()
                 return out
 
-            def all_to_all(self, t):
+            def all_to_all(self, t, async_op=False):
+                if async_op:
+                    return _Done(self.all_to_all(t))
                 torch.cuda.current_stream().synchronize()
                 ex.slots[r] = t
                 ex.bar.wait()
@@ -172,3 +184,60 @@ def test_sharded_matches_single_gpu(setup, W):
     print(f"W={W}: |dlogits| vs unsharded {err:.3e} (std {std:.3f})")
     assert err < 3e-2 * std
     assert head.first_token == ref.first_token
+
+
+def _dist_worker(rank, world, port, outdir, pipeline):
+    import os as _os
+
+    import torch.distributed as dist
+
+    import paper_2510_10129_b200 as cc
+    from paper_2510_10129_b200.sharded import DeviceShardCompute, Exchange, cacheclip_prefill_sharded, plan_shards
+    _os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        w = C1_EXACT
+        primary = cc.from_params(_cfg(w.primary, "bf16"), orc.seeded_params(w.primary, 0))
+        aux = cc.from_params(_cfg(w.aux, "fp32"), orc.seeded_params(w.aux, 1))
+        prefix, chunk_ids, query = w.token_ids(0)
+        plan = plan_shards([len(c) for c in chunk_ids], len(prefix), len(query), world, rank)
+        mine = plan.local_chunks()   # each rank precomputes only its own chunks
+        chunks = [cc.prefill_chunk(primary, prefix, chunk_ids[c]) for c in mine]
+        aux_chunks = [cc.prefill_chunk(aux, prefix, chunk_ids[c]) for c in mine]
+        res = cacheclip_prefill_sharded(DeviceShardCompute(primary, aux), Exchange(world), plan, chunks, aux_chunks,
+                                        {c: chunk_ids[c] for c in mine}, query,
+                                        cc.SelectionConfig(w.ratio, w.window_len, w.window_threshold),
+                                        n_layers=primary.config.n_layers, pipeline=pipeline)
+        torch.cuda.synchronize()
+        np.savez(_os.path.join(outdir, f"r{rank}.npz"), indices=np.asarray(res.indices),
+                 logits=res.logits if res.logits is not None else np.zeros(0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,pipeline", [(2, 2), (2, 1), (3, 2)])
+def test_multiprocess_sharded_over_torch_distributed(setup, tmp_path, world, pipeline):
+    """W processes (gloo, sharing cuda:0) run DeviceShardCompute
+    and the real torch.distributed Exchange on CUDA tensors: score all_gather,
+    identical selection, per-layer Q all_gather, partial attention, all_to_all,
+    LSE merge — pipelined in two halves (async collectives) or not. Every rank
+    selects the unsharded plan; the head rank's logits match the single-GPU
+    pipeline."""
+    import os
+    import socket
+
+    import torch.multiprocessing as mp
+    ref = setup[-1]
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    mp.spawn(_dist_worker, args=(world, port, str(tmp_path), pipeline), nprocs=world, join=True)
+    outs = [dict(np.load(os.path.join(tmp_path, f"r{r}.npz"))) for r in range(world)]
+    for o in outs:
+        assert tuple(o["indices"].tolist()) == ref.plan.indices
+    std = ref.logits.std()
+    err = np.abs(outs[0]["logits"] - ref.logits).max()
+    print(f"W={world} pipeline={pipeline}: |dlogits| vs unsharded {err:.3e} (std {std:.3f})")
+    assert err < 3e-2 * std
+    assert int(np.argmax(outs[0]["logits"])) == ref.first_token

@@ -95,10 +95,18 @@ class OracleShardCompute:
             out[:self.n] = orc.rope_rotate(q, self.pos, c.d_head, c.rope_base).reshape(self.n, -1)
         return torch.from_numpy(out)
 
-    def partial_attention(self, layer, q_all):
+    def _part_pos(self, part):
+        ppos = self.rows.packed_pos
+        if part is None:
+            return ppos
+        W, R = self.plan.world, self.rows.r_max
+        H = R // 2
+        return ppos.reshape(W, R)[:, part * H:(part + 1) * H].reshape(-1)
+
+    def partial_attention(self, layer, q_all, part=None):
         c = self.p.cfg
         q = q_all.numpy().reshape(-1, c.n_heads, c.d_head)
-        ppos = self.rows.packed_pos
+        ppos = self._part_pos(part)
         lim = np.searchsorted(self.lp, ppos, side="right")        # visible local keys per row
         o = np.zeros(q.shape, np.float32)
         lse = np.full(q.shape[:2], -np.inf, np.float32)
@@ -117,20 +125,30 @@ class OracleShardCompute:
                 lse[i, h] = (mx + np.log(l)) * LOG2E
         return torch.from_numpy(o), torch.from_numpy(lse)
 
-    def post_attention(self, layer, o_recv, lse_recv):
-        if not self.n:
-            return
+    def post_attention(self, layer, o_recv, lse_recv, part=None):
         W, R = self.plan.world, self.rows.r_max
-        o = o_recv.numpy().reshape(W, R, *o_recv.shape[1:])[:, :self.n]
-        lse = lse_recv.numpy().reshape(W, R, -1)[:, :self.n]
+        if part is None:
+            lo, hi, S = 0, self.n, R
+        else:
+            S = R // 2
+            lo, hi = part * S, min(self.n, (part + 1) * S)
+        if hi <= lo:
+            return
+        o = o_recv.numpy().reshape(W, S, *o_recv.shape[1:])[:, :hi - lo]
+        lse = lse_recv.numpy().reshape(W, S, -1)[:, :hi - lo]
         m = lse.max(axis=0)
         a = np.where(np.isinf(lse), 0.0, np.exp2(lse - m))
         ctx = (a[..., None] * o).sum(0) / a.sum(0)[..., None]
-        self.h = self.h + orc.out_project(self.p, layer, ctx.astype(np.float32))
-        self.h = self.h + orc.mlp(self.p, layer, self.h)
+        h = self.h[lo:hi] + orc.out_project(self.p, layer, ctx.astype(np.float32))
+        self.h[lo:hi] = h + orc.mlp(self.p, layer, h)
 
     def logits(self):
         return torch.from_numpy(orc.final_logits(self.p, self.h[:self.n]))
+
+
+class OracleShardComputeParts(OracleShardCompute):
+    """The same math through the pipelined two-half exchange."""
+    supports_parts = True
 
 
 def _free_port():
@@ -141,7 +159,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, wname, outdir):
+def _worker(rank, world, port, wname, outdir, pipeline=1):
     import torch.distributed as dist
 
     from oracle.synth import WORKLOADS
@@ -158,22 +176,26 @@ def _worker(rank, world, port, wname, outdir):
         mine = plan.local_chunks()   # each rank precomputes only its own chunks
         chunks = [orc.prefill_chunk(prim, prefix, chunk_ids[c]) for c in mine]
         aux_chunks = [orc.prefill_chunk(aux, prefix, chunk_ids[c]) for c in mine]
-        res = cacheclip_prefill_sharded(OracleShardCompute(prim, aux), Exchange(world), plan, chunks, aux_chunks,
+        compute = (OracleShardComputeParts if pipeline == 2 else OracleShardCompute)(prim, aux)
+        res = cacheclip_prefill_sharded(compute, Exchange(world), plan, chunks, aux_chunks,
                                         {c: chunk_ids[c] for c in mine}, query,
                                         SelectionConfig(w.ratio, w.window_len, w.window_threshold),
-                                        n_layers=w.primary.n_layers)
+                                        n_layers=w.primary.n_layers, pipeline=pipeline)
         np.savez(os.path.join(outdir, f"r{rank}.npz"), indices=np.asarray(res.indices),
                  logits=res.logits if res.logits is not None else np.zeros(0))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,wname", [(2, "c1_exact"), (3, "b1")])
-def test_gloo_sharded_matches_oracle(tmp_path, world, wname):
+@pytest.mark.parametrize("world,wname,pipeline", [(2, "c1_exact", 1), (3, "b1", 1), (2, "c1_exact", 2),
+                                                  (3, "b1", 2)])
+def test_gloo_sharded_matches_oracle(tmp_path, world, wname, pipeline):
+    """pipeline=2: each rank's exchange slots flow through the layer as two
+    halves with async collectives (overlap); results identical to pipeline=1."""
     import torch.multiprocessing as mp
 
     from oracle.synth import WORKLOADS
-    mp.spawn(_worker, args=(world, _free_port(), wname, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), wname, str(tmp_path), pipeline), nprocs=world, join=True)
     w = WORKLOADS[wname]
     prim = orc.OracleModel(w.primary, orc.seeded_params(w.primary, w.primary_seed, w.bias_std))
     aux = orc.OracleModel(w.aux, orc.seeded_params(w.aux, w.aux_seed, w.bias_std))
