@@ -142,6 +142,18 @@ int cc_embed_rmsnorm(const int64_t* ids, int64_t rows, const void* embed, int32_
                      void* x_out, int32_t x_mode, void* stream);
 int cc_rmsnorm(const float* h, int64_t rows, int32_t d, int64_t ld_h, const float* gain,
                float eps, void* x_out, int32_t x_mode, void* stream);
+/* The fused-RMSNorm operand of cc_gemm_args (xn = bf16(h * gain) and per-32-
+ * column partial sums of h^2 at ssq_out[(col/32) * ld_ssq + row]) for rows
+ * whose producer GEMM did not emit it, bit-identical to the RESIDUAL
+ * epilogue's; d % 32 == 0. */
+int cc_norm_prep(const float* h, int64_t rows, int32_t d, int64_t ld_h, const float* gain, void* xn_out,
+                 float* ssq_out, int64_t ld_ssq, void* stream);
+/* inv_rms[m] = 1 / sqrt((sum over the d/32 partials in order) / d + eps). */
+int cc_norm_finalize(const float* ssq, int64_t rows, int32_t d, int64_t ld_ssq, float eps, float* inv_rms,
+                     void* stream);
+/* 1 when the bf16 layer executor folds RMSNorm into its GEMMs (default; the
+ * environment variable CC_FUSED_NORM=0 selects standalone RMSNorm launches). */
+int cc_fused_norm(void);
 /* Weight preparation: fp32 [rows, cols] -> CC_BF16 or split layout
  * (split_mode 0 = activation [hi|hi|lo], 1 = weight [hi|lo|hi]). */
 int cc_convert_matrix(const float* src, int64_t rows, int64_t cols, void* dst, int32_t dst_mode,
@@ -174,13 +186,14 @@ typedef struct {
   /* RMSNorm fused across GEMMs (bf16 kind only; rms_norm, tensor_core.py:99-106):
    * the RESIDUAL epilogue that writes h also writes the next GEMM's A operand
    * xn = bf16(h * norm_gain) and per-row partial sums of h^2, one per 32-column
-   * chunk: ssq_out[(col / 32) * ld_ssq + m] (N % 32 == 0). A consumer GEMM
-   * (QKV / GLU epilogue) given ssq_in scales each accumulator row by
-   * 1 / sqrt(sum_p ssq_in[p * ld_ssq + m] / norm_d + norm_eps) before the bias:
-   * (h * g) @ W / rms(h) == rms_norm(h) @ W. */
+   * chunk: ssq_out[(col / 32) * ld_ssq + m] (N % 32 == 0); cc_norm_finalize
+   * reduces them to inv_rms[m] = 1 / sqrt(sum_p ssq / d + eps). A consumer
+   * GEMM (QKV / GLU / STORE / ACT epilogue) given inv_rms scales each
+   * accumulator row by it before the bias: (h * g) @ W / rms(h) ==
+   * rms_norm(h) @ W. */
   void* xn_out; int64_t ldxn; const float* norm_gain;
   float* ssq_out;
-  const float* ssq_in; int32_t ssq_parts; int32_t norm_d; float norm_eps;
+  const float* inv_rms;
   int64_t ld_ssq;
 } cc_gemm_args;
 

@@ -55,7 +55,7 @@ class GemmArgs(ctypes.Structure):
         ("raw_rows", vp),
         ("xn_out", vp), ("ldxn", i64), ("norm_gain", vp),
         ("ssq_out", vp),
-        ("ssq_in", vp), ("ssq_parts", i32), ("norm_d", i32), ("norm_eps", f32),
+        ("inv_rms", vp),
         ("ld_ssq", i64),
     ]
 
@@ -98,6 +98,9 @@ _SIGS = {
     "cc_rope_table": ([vp, i64, vp, i32, vp, vp, vp], i32),
     "cc_embed_rmsnorm": ([vp, i64, vp, i32, i64, i32, vp, vp, f32, vp, i32, vp], i32),
     "cc_rmsnorm": ([vp, i64, i32, i64, vp, f32, vp, i32, vp], i32),
+    "cc_norm_prep": ([vp, i64, i32, i64, vp, vp, vp, i64, vp], i32),
+    "cc_norm_finalize": ([vp, i64, i32, i64, f32, vp, vp], i32),
+    "cc_fused_norm": ([], i32),
     "cc_convert_matrix": ([vp, i64, i64, vp, i32, i32, vp], i32),
     "cc_gemm": ([ctypes.POINTER(GemmArgs), vp], i32),
     "cc_sparse_row_attention": ([vp, i64, vp, i64, vp, vp, i64, i32, i32, i32, f32, vp, vp, i64, vp], i32),

@@ -248,6 +248,10 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     *s_kmin = 0x7fffffff;
     fence_barrier_init();
   }
+  // the key-range bounds are initialised before the prologue's atomics (found
+  // by compute-sanitizer: under its serialisation the init could land after
+  // some warps' atomicMax/atomicMin and reset them)
+  __syncthreads();
   if (warp == 1) tmem_alloc(tmem_slot, 512);
 
   // ---- prologue: softmax warps gather their Q rows into swizzled smem ----

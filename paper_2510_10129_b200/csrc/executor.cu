@@ -37,6 +37,7 @@ static size_t rows_ws_bytes(const cc_model_desc* md, int64_t R) {
   s += 2 * align256(R * (md->head_dim / 2) * 4);  // cos, sin
   s += align256(64);                 // head workspace
   s += align256((size_t)((d + 31) / 32) * R * 4);  // fused RMSNorm partial sums
+  s += align256((size_t)R * 4);                     // and 1/rms per row
   // split-KV partials for launches of few rows (decode, the last layer's head
   // row): sized for the largest split count any key count can ask for
   const int S = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
@@ -98,6 +99,7 @@ static int gemm_call(int kind, int epi, int64_t M, int64_t N, int64_t K, const v
 struct NormFuse {
   void* xn;         // bf16 [rows][d], row-aligned with h
   float* ssq;       // [d/32][ld]
+  float* inv;       // [ld]: 1/rms per row (cc_norm_finalize)
   int64_t ld;       // rows of the pass
   int parts, d;
   float eps;
@@ -120,12 +122,12 @@ static void norm_produce(cc_gemm_args& a, const NormFuse& nf, int64_t r0, const 
   a.ld_ssq = nf.ld;
 }
 
-static void norm_consume(cc_gemm_args& a, const NormFuse& nf, int64_t r0) {
-  a.ssq_in = nf.ssq + r0;
-  a.ssq_parts = nf.parts;
-  a.norm_d = nf.d;
-  a.norm_eps = nf.eps;
-  a.ld_ssq = nf.ld;
+// reduce the partials of rows [r0, r0 + n) to 1/rms, then point the
+// consumer GEMM at them
+static int norm_consume(cc_gemm_args& a, const NormFuse& nf, int64_t r0, int64_t n, void* stream) {
+  CC_TRY(cc_norm_finalize(nf.ssq + r0, n, nf.d, nf.ld, nf.eps, nf.inv + r0, stream));
+  a.inv_rms = nf.inv + r0;
+  return CC_OK;
 }
 
 // gate/up on xn (written by the o-proj epilogue, rows scaled by 1/rms in the
@@ -156,8 +158,8 @@ static int run_mlp_fused(const cc_model_desc* md, const cc_layer_weights& lw, fl
     a.epilogue = CC_EPI_ACT;
     a.N = ff;
   }
-  norm_consume(a, nf, r0);
   if (!md->mlp_gated) return fail(CC_ERR_UNSUPPORTED, "fused RMSNorm needs the gated MLP");
+  CC_TRY(norm_consume(a, nf, r0, R, stream));
   CC_TRY(cc_gemm(&a, stream));
   cc_gemm_args b{};
   b.kind = CC_GEMM_BF16;
@@ -200,6 +202,8 @@ using namespace cc;
 
 extern "C" {
 
+int cc_fused_norm(void) { return fused_norm_enabled() ? 1 : 0; }
+
 int64_t cc_forward_rows_workspace_bytes(const cc_model_desc* md, int64_t rows) {
   return (int64_t)rows_ws_bytes(md, rows);
 }
@@ -229,8 +233,9 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
   float* sn = cv.take<float>(R * (md->head_dim / 2));
   void* hws = cv.take<uint8_t>(64);
   float* ssq = cv.take<float>((size_t)((d + 31) / 32) * R);
+  float* inv_rms = cv.take<float>((size_t)R);
   const bool fuse = fused_norm_enabled() && d % 32 == 0 && md->mlp_gated;
-  const NormFuse nf{x, ssq, R, (int)(d / 32), (int)d, md->norm_eps};
+  const NormFuse nf{x, ssq, inv_rms, R, (int)(d / 32), (int)d, md->norm_eps};
   const int s_max = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
   float* o_parts = s_max > 1 ? cv.take<float>((size_t)s_max * R * qw) : nullptr;
   float* lse_parts = s_max > 1 ? cv.take<float>((size_t)s_max * R * md->n_heads) : nullptr;
@@ -275,7 +280,7 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
     a.dst_rows = plan->dst_rows;
     a.k_raw = lp(plan->k_raw, plan->k_raw_stride, l);
     a.raw_rows = plan->raw_rows;
-    if (fuse && l > 0) norm_consume(a, nf, 0);  // x = bf16(h * attn_norm) from the previous down epilogue
+    if (fuse && l > 0) CC_TRY(norm_consume(a, nf, 0, R, stream));  // x = bf16(h * attn_norm), previous down
     CC_TRY(cc_gemm(&a, stream));
     // Last layer: every row's K/V are in the cache now (the QKV epilogue
     // scattered them); its attention output, o-proj and MLP feed nothing but

@@ -92,29 +92,13 @@ struct EpiParams {
   int64_t ldxn;
   const float* norm_gain;
   float* ssq_out;
-  const float* ssq_in;
-  int ssq_parts;
-  float inv_norm_d;
-  float norm_eps;
+  const float* ssq_in;  // inv_rms [M]
   int64_t ld_ssq;
 };
 
-// 1 / sqrt(mean(h^2) + eps) of GEMM row m from the producer's per-chunk
-// partial sums (fixed summation order: deterministic)
+// 1 / rms of GEMM row m (cc_norm_finalize reduced the producer's partial sums)
 __device__ __forceinline__ float row_inv_rms(const EpiParams& ep, int64_t m) {
-  if (m >= ep.M) return 0.f;
-  const float* p = ep.ssq_in + m;
-  float s = 0.f;
-  int i = 0;
-  for (; i + 8 <= ep.ssq_parts; i += 8) {
-    float t[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) t[j] = __ldg(p + (int64_t)(i + j) * ep.ld_ssq);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) s = __fadd_rn(s, t[j]);
-  }
-  for (; i < ep.ssq_parts; ++i) s = __fadd_rn(s, __ldg(p + (int64_t)i * ep.ld_ssq));
-  return 1.0f / sqrtf(__fadd_rn(__fmul_rn(s, ep.inv_norm_d), ep.norm_eps));
+  return m < ep.M ? __ldg(ep.ssq_in + m) : 0.f;
 }
 
 __device__ __forceinline__ float act_apply(int act, float x) {
@@ -975,25 +959,19 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   ep.ldxn = a->ldxn;
   ep.norm_gain = a->norm_gain;
   ep.ssq_out = a->ssq_out;
-  ep.ssq_in = a->ssq_in;
-  ep.ssq_parts = a->ssq_parts;
-  ep.inv_norm_d = a->norm_d > 0 ? 1.0f / (float)a->norm_d : 0.f;
-  ep.norm_eps = a->norm_eps;
+  ep.ssq_in = a->inv_rms;
   ep.ld_ssq = a->ld_ssq;
-  if (a->ssq_out || a->ssq_in) {
-    CC_CHECK_ARG(!tf32, CC_ERR_UNSUPPORTED, "fused RMSNorm runs on bf16 GEMMs");
-    CC_CHECK_ARG(a->ld_ssq >= a->M, CC_ERR_DIMENSION, "ld_ssq %lld < M %lld", (long long)a->ld_ssq,
-                 (long long)a->M);
-  }
+  if (a->ssq_out || a->inv_rms) CC_CHECK_ARG(!tf32, CC_ERR_UNSUPPORTED, "fused RMSNorm runs on bf16 GEMMs");
+  if (a->ssq_out)
+    CC_CHECK_ARG(a->ld_ssq >= a->M, CC_ERR_DIMENSION, "ld_ssq %lld < M %lld", (long long)a->ld_ssq, (long long)a->M);
   if (a->ssq_out) {
     CC_CHECK_ARG(a->epilogue == CC_EPI_RESIDUAL && a->N % 32 == 0 && a->xn_out && a->norm_gain &&
                      a->ldxn % 4 == 0 && ((uintptr_t)a->xn_out % 16) == 0 && ((uintptr_t)a->norm_gain % 16) == 0,
                  CC_ERR_UNSUPPORTED, "RMSNorm partials come from a RESIDUAL epilogue with N %% 32 == 0, xn and gain");
   }
-  if (a->ssq_in) {
-    CC_CHECK_ARG((a->epilogue == CC_EPI_QKV_ROPE || a->epilogue == CC_EPI_GLU) && a->ssq_parts > 0 && a->norm_d > 0,
-                 CC_ERR_UNSUPPORTED, "row RMS scaling applies to QKV / GLU epilogues with ssq_parts, norm_d");
-  }
+  if (a->inv_rms)
+    CC_CHECK_ARG(a->epilogue != CC_EPI_RESIDUAL, CC_ERR_UNSUPPORTED,
+                 "row RMS scaling applies to QKV / GLU / STORE / ACT epilogues");
   bool wide;
   if (a->epilogue == CC_EPI_GLU) {
     CC_CHECK_ARG(a->glu_block == 128 && a->N % 256 == 0, CC_ERR_UNSUPPORTED,

@@ -511,6 +511,59 @@ __global__ void gather_i64_kernel(const int64_t* __restrict__ src, const int64_t
 
 using namespace cc;
 
+// Fused-RMSNorm operand for rows whose producer GEMM did not emit it (a
+// truncated pass that continues outside the executor): xn = bf16(h * gain)
+// and the per-32-column partial sums of h^2 in exactly the arithmetic of the
+// GEMM residual epilogue (gemm_sm100.cu, CC_EPI_RESIDUAL with ssq_out), so a
+// consumer GEMM reproduces the executor's values bit for bit. Warp per row;
+// lane l covers 4 columns, 8-lane groups = one 32-column chunk.
+// thread per row: the partials in a fixed order (deterministic), then
+// 1 / sqrt(mean + eps) with correctly rounded sqrt and division
+__global__ void __launch_bounds__(256) norm_finalize_kernel(const float* __restrict__ ssq, int64_t rows, int parts,
+                                                            int64_t ld, float inv_d, float eps,
+                                                            float* __restrict__ inv_rms) {
+  const int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  if (r >= rows) return;
+  float s = 0.f;
+  int i = 0;
+  for (; i + 8 <= parts; i += 8) {
+    float t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = __ldg(ssq + (int64_t)(i + j) * ld + r);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = __fadd_rn(s, t[j]);
+  }
+  for (; i < parts; ++i) s = __fadd_rn(s, __ldg(ssq + (int64_t)i * ld + r));
+  inv_rms[r] = __frcp_rn(__fsqrt_rn(__fadd_rn(__fmul_rn(s, inv_d), eps)));
+}
+
+__global__ void __launch_bounds__(256) norm_prep_kernel(const float* __restrict__ h, int64_t rows, int d, int64_t ld_h,
+                                                        const float* __restrict__ gain, __nv_bfloat16* __restrict__ xn,
+                                                        float* __restrict__ ssq, int64_t ld_ssq) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  for (int c0 = 0; c0 < d; c0 += 128) {
+    const int col = c0 + 4 * lane;
+    float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (col < d) {
+      y = *reinterpret_cast<const float4*>(h + row * ld_h + col);
+      const float4 g = *reinterpret_cast<const float4*>(gain + col);
+      __nv_bfloat162 a = __floats2bfloat162_rn(__fmul_rn(y.x, g.x), __fmul_rn(y.y, g.y));
+      __nv_bfloat162 b = __floats2bfloat162_rn(__fmul_rn(y.z, g.z), __fmul_rn(y.w, g.w));
+      uint2 u;
+      u.x = *reinterpret_cast<uint32_t*>(&a);
+      u.y = *reinterpret_cast<uint32_t*>(&b);
+      *reinterpret_cast<uint2*>(xn + row * d + col) = u;
+    }
+    float ss = __fmaf_rn(y.w, y.w, __fmaf_rn(y.z, y.z, __fmaf_rn(y.y, y.y, __fmul_rn(y.x, y.x))));
+    ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, 1));
+    ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, 2));
+    ss = __fadd_rn(ss, __shfl_xor_sync(0xffffffffu, ss, 4));
+    if ((lane & 7) == 0 && col < d) ssq[(int64_t)(col >> 5) * ld_ssq + row] = ss;
+  }
+}
+
 extern "C" {
 
 int cc_abi_version(void) { return CC_ABI_VERSION; }
@@ -711,6 +764,29 @@ int cc_embed_rmsnorm(const int64_t* ids, int64_t rows, const void* embed, int32_
   ProfScope ps(as_stream(stream), OP_NORM, 0);
   launch_rmsnorm(ids, embed, embed_dtype, d, h_out, gain, eps, x_out, x_mode, nullptr, 0, rows, as_stream(stream));
   CC_LAUNCH_CHECK("embed_rmsnorm");
+  return CC_OK;
+}
+
+int cc_norm_prep(const float* h, int64_t rows, int32_t d, int64_t ld_h, const float* gain, void* xn_out,
+                 float* ssq_out, int64_t ld_ssq, void* stream) {
+  CC_CHECK_ARG(h && gain && xn_out && ssq_out, CC_ERR_VALUE, "null norm_prep argument");
+  CC_CHECK_ARG(d > 0 && d % 32 == 0 && ld_h % 4 == 0 && ld_ssq >= rows, CC_ERR_UNSUPPORTED,
+               "norm_prep needs d %% 32 == 0 (d=%d), ld_h %% 4 == 0 and ld_ssq >= rows", d);
+  if (rows <= 0) return CC_OK;
+  norm_prep_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, as_stream(stream)>>>(
+      h, rows, d, ld_h, gain, reinterpret_cast<__nv_bfloat16*>(xn_out), ssq_out, ld_ssq);
+  CC_LAUNCH_CHECK("norm_prep");
+  return CC_OK;
+}
+
+int cc_norm_finalize(const float* ssq, int64_t rows, int32_t d, int64_t ld_ssq, float eps, float* inv_rms,
+                     void* stream) {
+  CC_CHECK_ARG(ssq && inv_rms, CC_ERR_VALUE, "null norm_finalize argument");
+  CC_CHECK_ARG(d > 0 && d % 32 == 0 && ld_ssq >= rows, CC_ERR_UNSUPPORTED, "norm_finalize needs d %% 32 == 0");
+  if (rows <= 0) return CC_OK;
+  norm_finalize_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, as_stream(stream)>>>(ssq, rows, d / 32, ld_ssq,
+                                                                                      1.0f / (float)d, eps, inv_rms);
+  CC_LAUNCH_CHECK("norm_finalize");
   return CC_OK;
 }
 

@@ -45,7 +45,8 @@ def gemm(kind: int, epilogue: int, M: int, N: int, K: int, A: torch.Tensor, B: t
          bias=None, C=None, ldc: int = 0, c_mode: int = _lib.CC_BF16, act: int = 0, n_out: int = 0,
          lda: int | None = None, rope=None, q_out=None, ldq: int = 0, q_mode: int = _lib.CC_BF16,
          k_cache=None, v_cache=None, cache_dtype: int = _lib.CC_BF16, dst_rows=None, k_raw=None,
-         raw_rows=None, heads=(0, 0, 0)) -> None:
+         raw_rows=None, heads=(0, 0, 0), inv_rms=None, ld_ssq: int = 0, xn_out=None, ldxn: int = 0,
+         norm_gain=None, ssq_out=None) -> None:
     """Direct cc_gemm call (kernel tests and one-off GEMMs)."""
     a = _lib.GemmArgs()
     a.kind, a.epilogue = kind, epilogue
@@ -61,6 +62,8 @@ def gemm(kind: int, epilogue: int, M: int, N: int, K: int, A: torch.Tensor, B: t
     a.q_out, a.ldq, a.q_mode = _p(q_out), ldq, q_mode
     a.k_cache, a.v_cache, a.cache_dtype = _p(k_cache), _p(v_cache), cache_dtype
     a.dst_rows, a.k_raw, a.raw_rows = _p(dst_rows), _p(k_raw), _p(raw_rows)
+    a.xn_out, a.ldxn, a.norm_gain, a.ssq_out = _p(xn_out), ldxn, _p(norm_gain), _p(ssq_out)
+    a.inv_rms, a.ld_ssq = _p(inv_rms), ld_ssq
     _lib.call("cc_gemm", ctypes.byref(a), _s())
 
 

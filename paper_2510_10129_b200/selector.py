@@ -370,17 +370,30 @@ def _cacheblend_device(primary_model: Model, merged, ratio: float, trace: Pipeli
     lw = primary_model.layers[1]
     s = torch.cuda.current_stream().cuda_stream
     x = torch.empty(total, c.d_model, dtype=torch.bfloat16, device=dev)
-    _lib.call("cc_rmsnorm", res.h.data_ptr(), total, c.d_model, c.d_model, lw.attn_norm.data_ptr(), c.norm_eps,
-              x.data_ptr(), _lib.CC_BF16, s)
     qw, kw = c.attn_width, c.kv_width
     from .runtime import gemm
-    # values in the cache's own precision (bf16 rounding, as the QKV epilogue
-    # stores them), so a row whose context did not change drifts by exactly 0
+    # layer 1's values in the arithmetic of the executor that built the
+    # caches: with fused RMSNorm, bf16(h * gain) with per-row 1/rms applied in
+    # the GEMM epilogue (cc_norm_prep = the residual epilogue's operand); the
+    # cache's own precision (bf16 rounding, as the QKV epilogue stores them),
+    # so a row whose context did not change drifts by exactly 0
+    norm = {}
+    if _lib.load().cc_fused_norm() and c.d_model % 32 == 0 and c.mlp_gated:
+        ssq = torch.empty(c.d_model // 32, total, dtype=torch.float32, device=dev)
+        inv = torch.empty(total, dtype=torch.float32, device=dev)
+        _lib.call("cc_norm_prep", res.h.data_ptr(), total, c.d_model, c.d_model, lw.attn_norm.data_ptr(),
+                  x.data_ptr(), ssq.data_ptr(), total, s)
+        _lib.call("cc_norm_finalize", ssq.data_ptr(), total, c.d_model, total, c.norm_eps, inv.data_ptr(), s)
+        norm = dict(inv_rms=inv)
+    else:
+        _lib.call("cc_rmsnorm", res.h.data_ptr(), total, c.d_model, c.d_model, lw.attn_norm.data_ptr(), c.norm_eps,
+                  x.data_ptr(), _lib.CC_BF16, s)
     cached = merged.v_store[1][sink:total]
     v_global = torch.empty(total, kw, dtype=cached.dtype, device=dev)
     vmode = _lib.CC_BF16 if cached.dtype == torch.bfloat16 else _lib.CC_F32
     gemm(_lib.CC_GEMM_BF16, _lib.CC_EPI_STORE, total, kw, c.d_model, x, lw.w_qkv[qw + kw:qw + 2 * kw],
-         bias=None if lw.b_qkv is None else lw.b_qkv[qw + kw:qw + 2 * kw], C=v_global, ldc=kw, c_mode=vmode)
+         bias=None if lw.b_qkv is None else lw.b_qkv[qw + kw:qw + 2 * kw], C=v_global, ldc=kw, c_mode=vmode,
+         **norm)
     disc = torch.empty(n, dtype=torch.float32, device=dev)
     _lib.call("cc_row_l2_diff", v_global[sink:].data_ptr(), vmode, kw, cached.data_ptr(), vmode, kw, n, kw,
               disc.data_ptr(), s)

@@ -83,6 +83,26 @@ def shapes(kind, M, d, hq, hkv, dh, ff):
         kind, L.CC_EPI_GLU, M, 2 * ff, d, x, w_up, C=act, ldc=ff, c_mode=amode, n_out=ff), 2.0 * M * 2 * ff * d)
     out[f"{tag} down M={M} N={d} K={ff}"] = (lambda: gemm(
         kind, L.CC_EPI_RESIDUAL, M, d, ff, act, w_down, C=h, ldc=d, c_mode=L.CC_F32), 2.0 * M * d * ff)
+    if not f32:  # the fused-RMSNorm epilogues of the layer executor
+        xn = torch.empty(M, d, device=DEV, dtype=torch.bfloat16)
+        ssq = torch.zeros(d // 32, M, device=DEV)
+        inv = torch.ones(M, device=DEV)
+        gain = torch.ones(d, device=DEV)
+        nrm = dict(xn_out=xn, ldxn=d, norm_gain=gain, ssq_out=ssq, ld_ssq=M)
+        out[f"{tag} qkv+rms M={M} N={n_qkv} K={d}"] = (lambda: gemm(
+            kind, L.CC_EPI_QKV_ROPE, M, n_qkv, d, x, w_qkv, bias=b_qkv, rope=(cos, sin), q_out=q, ldq=qw,
+            q_mode=mode, k_cache=kc, v_cache=vc, cache_dtype=mode, dst_rows=rows, heads=(hq, hkv, dh),
+            inv_rms=inv), 2.0 * M * n_qkv * d)
+        out[f"{tag} o+norm M={M} N={d} K={qw}"] = (lambda: gemm(
+            kind, L.CC_EPI_RESIDUAL, M, d, qw, ctx, w_o, C=h, ldc=d, c_mode=L.CC_F32, **nrm), 2.0 * M * d * qw)
+        out[f"{tag} up+rms M={M} N={2 * ff} K={d}"] = (lambda: gemm(
+            kind, L.CC_EPI_GLU, M, 2 * ff, d, x, w_up, C=act, ldc=ff, c_mode=amode, n_out=ff, inv_rms=inv),
+            2.0 * M * 2 * ff * d)
+        out[f"{tag} down+norm M={M} N={d} K={ff}"] = (lambda: gemm(
+            kind, L.CC_EPI_RESIDUAL, M, d, ff, act, w_down, C=h, ldc=d, c_mode=L.CC_F32, **nrm), 2.0 * M * d * ff)
+        out[f"{tag} finalize M={M}"] = (lambda: L.call(
+            "cc_norm_finalize", ssq.data_ptr(), M, d, M, 1e-6, inv.data_ptr(),
+            torch.cuda.current_stream().cuda_stream), 1.0)
     return out
 
 
