@@ -140,8 +140,9 @@ class RowPlan:
 # collectives
 # ---------------------------------------------------------------------------
 def _wire(t: torch.Tensor) -> torch.Tensor:
-    """bf16 payloads travel as int16 (same bytes) over backends without bf16."""
-    return t.view(torch.int16) if t.dtype == torch.bfloat16 else t
+    """bf16 payloads travel as raw bytes (uint8 view, last dim doubled) over
+    backends without bf16 (gloo rejects both bf16 and int16)."""
+    return t.view(torch.uint8) if t.dtype == torch.bfloat16 else t
 
 
 class _Done:
@@ -180,8 +181,7 @@ class Exchange:
         self._gloo = None
 
     def _host_staged(self, t: torch.Tensor) -> bool:
-        if not t.is_cuda:
-            return False
+        """gloo: payloads move as host tensors in a dtype gloo carries."""
         if self._gloo is None:
             import torch.distributed as dist
             self._gloo = dist.get_backend(self.group) == "gloo"

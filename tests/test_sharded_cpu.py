@@ -208,3 +208,38 @@ def test_gloo_sharded_matches_oracle(tmp_path, world, wname, pipeline):
     for o in outs:
         assert tuple(o["indices"].tolist()) == ref.indices
     np.testing.assert_allclose(outs[0]["logits"], ref.logits, rtol=0, atol=5e-5)
+
+
+def _bf16_worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_10129_b200.sharded import Exchange
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(rank)
+        x = torch.randn(4, 3, 8, generator=g).to(torch.bfloat16)
+        ex = Exchange(world)
+        gathered = ex.all_gather(x, async_op=True).wait()
+        swapped = ex.all_to_all(torch.cat([x] * world), async_op=False)
+        np.savez(os.path.join(outdir, f"b{rank}.npz"), g=gathered.view(torch.int16).numpy(),
+                 s=swapped.view(torch.int16).numpy(), dt=str(gathered.dtype) + str(swapped.dtype))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_exchange_carries_bf16_bytewise(tmp_path):
+    """gloo has neither bf16 nor int16: the Exchange moves bf16 payloads as
+    raw bytes and hands back bf16 tensors bit-identical to what was sent."""
+    import torch
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_bf16_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    sent = [torch.randn(4, 3, 8, generator=torch.Generator().manual_seed(r)).to(torch.bfloat16).view(torch.int16)
+            .numpy() for r in range(world)]
+    for r in range(world):
+        o = np.load(os.path.join(tmp_path, f"b{r}.npz"))
+        assert str(o["dt"]) == "torch.bfloat16torch.bfloat16"
+        np.testing.assert_array_equal(o["g"], np.concatenate(sent))
+        np.testing.assert_array_equal(o["s"], np.concatenate(sent))
