@@ -671,6 +671,20 @@ def run_sharded(args, rank: int, world: int):
         t = torch.tensor([ttft], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ttft = float(t.item())
+    # full-attention prefill denominator of the whole context on ONE GPU (the
+    # paper's speed-up, pipeline.py:77-84); measured once, in the W=1 run
+    # where every chunk is local (for W>1 the ratio uses that W=1 number)
+    full_ms = None
+    if world == 1 and not args.skip_full:
+        ids = cc.reuse_context_ids(chunks, query)
+        cc.full_attention_prefill(primary, ids)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        cc.full_attention_prefill(primary, ids)
+        b.record()
+        torch.cuda.synchronize()
+        full_ms = float(a.elapsed_time(b))
     if rank != 0:
         return
     m_sel = len(out.indices)
@@ -684,6 +698,7 @@ def run_sharded(args, rank: int, world: int):
                    "split-KV + LSE merge over NCCL)",
                    "window_rule": f"window_len=8, threshold={args.window_threshold}"},
         "ttft_ms": ttft, "first_token": out.first_token, "clocks": clocks.summary(), "setup_s": setup_s,
+        "full_prefill_ms": full_ms, "speedup_vs_full": (full_ms / ttft) if full_ms else None,
     }
     print(json.dumps(line), flush=True)
 

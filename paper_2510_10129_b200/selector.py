@@ -302,8 +302,22 @@ def aux_score_tokens(aux_model: Model, aux_chunk_caches: Sequence[ChunkCache], q
     prefix = aux_chunk_caches[0].prefix_len
     chunk_lens = n_rows - np.array([ch.prefix_len for ch in aux_chunk_caches], dtype=np.int64)
     if any(ch.prefix_len != prefix for ch in aux_chunk_caches):
-        # columns start at each chunk's own prefix_len; the kernel uses one col0
-        raise ValueError("aux chunks must share one prefix length")
+        # the reference scores each chunk against its own prefix_len; one
+        # banked launch takes one score column offset, so chunks are scored in
+        # groups of equal prefix length (a chunk's scores depend on that chunk
+        # and the query only) and reassembled in chunk order
+        if _banks is not None:
+            raise ValueError("streamed aux banks must share one prefix length")
+        groups: dict[int, list[int]] = {}
+        for i, ch in enumerate(aux_chunk_caches):
+            groups.setdefault(ch.prefix_len, []).append(i)
+        parts: list = [None] * len(aux_chunk_caches)
+        for idxs in groups.values():
+            sub = aux_score_tokens(aux_model, [aux_chunk_caches[i] for i in idxs], query_ids, trace=trace)
+            offs = np.concatenate([[0], np.cumsum(sub.chunk_lens)])
+            for k, i in enumerate(idxs):
+                parts[i] = sub.device_scores[int(offs[k]):int(offs[k + 1])]
+        return ImportanceScores(torch.cat(parts), tuple(int(x) for x in chunk_lens))
     ids = np.tile(q, S)
     pos = (n_rows[:, None] + np.arange(Q, dtype=np.int64)[None, :]).reshape(-1)
     col_off = np.concatenate([[0], np.cumsum(chunk_lens)[:-1]]).astype(np.int64)

@@ -41,6 +41,32 @@ class GreedyTokenizer:
         self._table = table
         self._lengths = sorted({len(t) for t in vocab}, reverse=True)
         self.tokenizer_id = tokenizer_id
+        self._digest: str | None = None
+        self._canonical: set[tuple[int, ...]] = set()  # id sequences known to re-encode to themselves
+
+    @property
+    def vocab_digest(self) -> str:
+        """SHA-256 of the vocabulary contents (two tokenizers with equal
+        digests tokenize every text identically)."""
+        if self._digest is None:
+            import hashlib
+            h = hashlib.sha256()
+            for tok in self._vocab:
+                h.update(tok.encode("utf-8", "surrogatepass"))
+                h.update(b"\n")  # tokens never contain a newline
+            self._digest = h.hexdigest()
+        return self._digest
+
+    def is_canonical(self, ids: Sequence[int]) -> bool:
+        """True when decode(ids) re-encodes to exactly ids (memoised: a
+        cached chunk's ids are checked once per tokenizer, not per request)."""
+        key = tuple(int(i) for i in ids)
+        if key in self._canonical:
+            return True
+        ok = self.encode(self.decode(key)) == list(key)
+        if ok:
+            self._canonical.add(key)
+        return ok
 
     @property
     def vocab_size(self) -> int:

@@ -235,3 +235,23 @@ def test_cross_tokenizer_prefill_matches_reference():
     ref = g["x_clip_logits"]
     assert np.abs(out.logits - ref).max() < BF16_LOGIT_TOL * ref.std()
     assert out.first_token == int(np.argmax(out.logits))
+
+
+def test_scoring_mixed_prefix_lengths():
+    """Chunks precomputed behind different prefixes are each scored against
+    their own prefix_len, as the reference does (selector.py:132-179):
+    grouped banked launches reassembled in chunk order, rtol 1e-5 vs the oracle."""
+    import paper_2510_10129_b200 as cc
+    w = C1
+    a_params = orc.seeded_params(w.aux, w.aux_seed, w.bias_std)
+    aux = cc.from_params(_cfg(w.aux, "fp32"), a_params)
+    o_aux = orc.OracleModel(w.aux, a_params)
+    prefix, chunk_ids, query = w.token_ids(0)
+    prefixes = [prefix, prefix[: max(1, len(prefix) // 2)], prefix, list(prefix) + list(prefix[:3])]
+    chunks = chunk_ids[: len(prefixes)]
+    d = [cc.prefill_chunk(aux, p, c) for p, c in zip(prefixes, chunks)]
+    o = [orc.prefill_chunk(o_aux, p, c) for p, c in zip(prefixes, chunks)]
+    got = cc.aux_score_tokens(aux, d, query)
+    want = orc.aux_scores(o_aux, o, query)
+    assert got.chunk_lens == tuple(len(c) for c in chunks)
+    np.testing.assert_allclose(got.scores, want, rtol=1e-5, atol=1e-9)

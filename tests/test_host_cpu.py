@@ -266,3 +266,32 @@ def test_bench_metric_matches_baseline():
     from paper_2510_10129_b200.workloads import WORKLOADS
     with open(os.path.join(ROOT, "BASELINE.json")) as f:
         assert bench.metric_name(WORKLOADS["c3"], 0.2) == json.load(f)["metric"]
+
+
+def test_chunk_spans_identity_needs_equal_vocab_contents():
+    """the identity-alignment shortcut keys on the vocabulary
+    contents, not on tokenizer_id + vocab_size, and still applies the
+    reference's re-encode check (pipeline.py:118-153)."""
+    from types import SimpleNamespace
+
+    from paper_2510_10129_b200 import GreedyTokenizer
+    from paper_2510_10129_b200.pipeline import chunk_spans
+
+    va = ["a", "b", "ab", "c"]
+    vb = ["a", "b", "ba", "c"]  # same id, same size, different contents
+    ta, tb = GreedyTokenizer(va, "tok"), GreedyTokenizer(vb, "tok")
+    assert ta.vocab_digest != tb.vocab_digest
+    assert GreedyTokenizer(list(va), "other").vocab_digest == ta.vocab_digest
+    mk = lambda ids: SimpleNamespace(chunk_ids=list(ids), chunk_len=len(ids))  # noqa: E731
+    # equal contents: identity alignment
+    spans, n = chunk_spans([mk([2, 3])], [mk([2, 3])], ta, GreedyTokenizer(list(va), "x"))
+    assert spans is None and n == 2
+    # non-canonical cached ids ("a","b" re-encodes to "ab") raise as in the reference
+    with pytest.raises(ValueError, match="re-encode"):
+        chunk_spans([mk([0, 1])], [mk([0, 1])], ta, ta)
+    # colliding id/size but different vocabularies take the full alignment path:
+    # "ab" under ta is [2]; under tb the text "ab" encodes to [0, 1]
+    spans, n = chunk_spans([mk([2])], [mk([0, 1])], ta, tb)
+    assert n is None
+    p, a = spans
+    assert [s.token_id for s in p] == [2] and [s.token_id for s in a] == [0, 1]
