@@ -246,8 +246,11 @@ int cc_sparse_row_attention_split(const void* q, int64_t ldq, const int64_t* pos
                                   int32_t n_q_heads, int32_t n_kv_heads, int32_t head_dim, float factor,
                                   const float* row_factor, int32_t n_splits, float* o_parts, float* lse_parts,
                                   void* out, int64_t ldo, void* stream);
-/* The split count cc_forward_rows uses: > 1 only for m * (Hq / Hkv) <= 256
- * packed rows over >= 4096 keys (up to 32 parts); 1 otherwise. */
+/* The split count cc_forward_rows uses: > 1 only when the launch's
+ * ceil(m * (Hq / Hkv) / 256) * Hkv CTAs are under two waves of the SMs and
+ * the keys are >= 4096 (up to 32 parts, at least 1024 keys each); 1
+ * otherwise. Inside the kernel a CTA uses one part per 8 key tiles of its
+ * own range at most (unused parts report LSE = -inf). */
 int32_t cc_attention_splits(int64_t m, int32_t n_q_heads, int32_t n_kv_heads, int64_t n_keys);
 /* Log-sum-exp merge of n_parts partial attentions (parts stride
  * part_stride rows): out[i][h*D..] = sum_w 2^(lse_w - M) O_w / sum_w 2^(lse_w - M). */

@@ -54,6 +54,7 @@ constexpr int kFaCtlRegs = 56;    // setmaxnreg budgets: 128*56 + 256*224 <= 64K
 constexpr int kFaSoftmaxRegs = 224;
 constexpr float kFaRescaleThreshold = 8.0f;  // log2 domain
 constexpr int kMaxAttnSplits = 32;
+constexpr int kFaMinSplitTiles = 8;  // a split part covers at least this many key tiles (1024 keys)
 
 template <int D>
 struct FaCfg {
@@ -254,35 +255,24 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   __syncthreads();
   if (warp == 1) tmem_alloc(tmem_slot, 512);
 
-  // ---- prologue: softmax warps gather their Q rows into swizzled smem ----
+  // ---- prologue: row ranges -> the CTA's key tiles; then the Q gather ----
   const int tq = warp >= 4 ? (warp - 4) >> 2 : 0;  // query tile of this softmax warp
   const int quarter = warp & 3;                     // TMEM lane quarter
   const int r = quarter * 32 + lane;                // row within the tile
   int lim = 0, ks = 0x7fffffff;  // this row sees keys [ks, lim)
   float scale2 = 0.f;
-  int64_t out_off = -1, part_row = -1;
+  int64_t qrow = -1;  // selected row of this thread's packed row (-1: padding)
+  int qhead = 0;
   if (warp >= 4) {
     const int64_t p = p0 + tq * kFaTileRows + r;
-    const uint4 zero = make_uint4(0, 0, 0, 0);
-    const uint4* src = nullptr;
     if (p < packed_total) {
       const int64_t i = p / G;
-      const int head = kvh * G + (int)(p % G);
-      part_row = i * n_q_heads + head;
+      qhead = kvh * G + (int)(p % G);
+      qrow = i;
       ks = kstart ? (int)kstart[i] : 0;
       lim = (int)min(ks + pos[i] + 1, n_keys);
       scale2 = (row_factor ? row_factor[i] : factor) * 1.4426950408889634f;
-      src = reinterpret_cast<const uint4*>(q + i * ldq + (int64_t)head * D);
-      out_off = i * ldo + (int64_t)head * D;
     }
-    uint8_t* qt = sQ + tq * Cfg::QT_BYTES;
-#pragma unroll
-    for (int c = 0; c < D / 8; ++c) {
-      const uint4 v = src ? __ldg(src + c) : zero;
-      const int kb = c >> 3, cc = c & 7;
-      *reinterpret_cast<uint4*>(qt + kb * (kFaTileRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
-    }
-    fence_proxy_async_smem();
     int mx = lim, mn = ks;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -302,14 +292,47 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   // CTA's ranges are nearly contiguous; tiles outside a row's range are masked)
   int j0 = *s_kmax > 0 ? *s_kmin / kFaKeys : 0;
   int n_tiles = (*s_kmax + kFaKeys - 1) / kFaKeys - j0;
-  if (gridDim.z > 1) {  // split-KV (few rows, long keys): this CTA takes part blockIdx.z of the tile range
-    const int per = (n_tiles + (int)gridDim.z - 1) / (int)gridDim.z;
-    const int a = min(n_tiles, (int)blockIdx.z * per), b = min(n_tiles, a + per);
+  if (gridDim.z > 1) {
+    // split-KV: this CTA takes part blockIdx.z of its tile range. Work-aware:
+    // a CTA uses at most one part per kFaMinSplitTiles tiles, so short ranges
+    // (early-position rows) stay whole and only the long ones are cut; the
+    // unused parts leave LSE = -inf, which the merge skips.
+    const int parts = min((int)gridDim.z, max(1, n_tiles / kFaMinSplitTiles));
+    const int per = (n_tiles + parts - 1) / parts;
+    const int z = (int)blockIdx.z;
+    const int a = z < parts ? min(n_tiles, z * per) : n_tiles;
+    const int b = z < parts ? min(n_tiles, a + per) : n_tiles;
     j0 += a;
     n_tiles = b - a;
     o_part = static_cast<uint8_t*>(o_part) + (size_t)blockIdx.z * m * n_q_heads * D * (part_bf16 ? 2 : 4);
     lse_part += (int64_t)blockIdx.z * m * n_q_heads;
+    if (n_tiles == 0) {  // an unused part: no keys, LSE = -inf for every row (O is never read)
+      if (qrow >= 0) lse_part[qrow * n_q_heads + qhead] = -INFINITY;
+      tc_fence_before();
+      __syncthreads();
+      if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+      }
+      return;
+    }
   }
+  if (warp >= 4) {  // softmax warps gather their Q rows into swizzled smem
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    const uint4* src = qrow >= 0 ? reinterpret_cast<const uint4*>(q + qrow * ldq + (int64_t)qhead * D) : nullptr;
+    uint8_t* qt = sQ + tq * Cfg::QT_BYTES;
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+      const uint4 v = src ? __ldg(src + c) : zero;
+      const int kb = c >> 3, cc = c & 7;
+      *reinterpret_cast<uint4*>(qt + kb * (kFaTileRows * 128) + r * 128 + ((cc ^ (r & 7)) << 4)) = v;
+    }
+    fence_proxy_async_smem();
+  }
+  // Q is in shared memory before the first S = Q K^T issue: the MMA warp and
+  // the softmax warps meet on named barrier 1 (the TMA producer is already
+  // streaming the first K/V tiles)
+  if (warp == 1 || warp >= 4) asm volatile("bar.sync 1, %0;" ::"n"(kFaThreads - 96) : "memory");
 
   if (warp < 4) {
 #ifndef CC_NO_SETMAXNREG  // sanitizer builds: no register reallocation under instrumentation
@@ -398,7 +421,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
     const uint32_t lane_base = (uint32_t)(quarter * 32) << 16;
     const uint32_t s_addr = tmem + lane_base + Cfg::s_col(tq);
     const uint32_t o_addr = tmem + lane_base + Cfg::o_col(tq);
-    int warp_min = out_off >= 0 ? lim : 0x7fffffff, warp_ks = out_off >= 0 ? ks : 0;
+    int warp_min = qrow >= 0 ? lim : 0x7fffffff, warp_ks = qrow >= 0 ? ks : 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       warp_min = min(warp_min, __shfl_xor_sync(0xffffffffu, warp_min, o));
@@ -481,6 +504,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       tc_fence_after();
     }
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    const int64_t part_row = qrow >= 0 ? qrow * n_q_heads + qhead : -1;
+    const int64_t out_off = qrow >= 0 ? qrow * ldo + (int64_t)qhead * D : -1;
     if (o_part && part_row >= 0)  // split-KV partial: log2-domain LSE of this shard's keys
       lse_part[part_row] = (l_run > 0.f && m_run != -INFINITY) ? m_run + __log2f(l_run) : -INFINITY;
 #pragma unroll
@@ -488,8 +513,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       float ov[32];
       tmem_ld32(o_addr + c * 32, ov);
       if (o_part) {
-        if (part_row >= 0) {
-          const bool live = l_run > 0.f && n_tiles > 0;
+        if (part_row >= 0 && l_run > 0.f) {  // rows with no visible key here: LSE -inf, O never read
+          const bool live = n_tiles > 0;
           const float sc = live ? inv : 0.f;
           if (part_bf16) {  // bf16 partials: half the exchange and merge bytes
             uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(o_part) + part_row * D + c * 32);
@@ -668,12 +693,15 @@ extern "C" int cc_sparse_row_attention_ranged(const void* q, int64_t ldq, const 
                        row_factor, out, ldo, st, g_attn_flops);
 }
 
-// Split-KV count for a launch of m rows over n_keys keys: > 1 only when the
-// rows fit one query-tile pair per KV head (decode steps, the last layer's
-// head row) and the keys are long, so a handful of CTAs would otherwise walk
-// the whole key range alone; then each CTA takes 1/S of the key tiles and
-// the parts are merged by log-sum-exp. Larger launches are never split
-// (measured: the per-CTA fixed costs outweigh a fuller grid there).
+// Split-KV count for a launch of m rows over n_keys keys. A launch of G*m
+// packed rows runs ceil(G*m / 256) x Hkv CTAs; when that is under two waves
+// of the SMs (decode steps, the last layer's head row, low recompute ratios,
+// the default 8/5 window rule's few hundred rows) and the keys are long, the
+// grid gets S parts per CTA, S bringing it to about two waves. Inside the
+// kernel a CTA uses only as many parts as its own key range has 8-tile
+// blocks, so the long (late-position) ranges are cut and the short ones stay
+// whole; the parts are merged by log-sum-exp. Grids of two waves or more are
+// never split: the heavy-first order already balances them.
 extern "C" int32_t cc_attention_splits(int64_t m, int32_t n_q_heads, int32_t n_kv_heads, int64_t n_keys) {
   static int enabled = -1;  // CC_ATTN_SPLIT=0 in the environment: never split (A/B runs)
   if (enabled < 0) {
@@ -681,8 +709,15 @@ extern "C" int32_t cc_attention_splits(int64_t m, int32_t n_q_heads, int32_t n_k
     enabled = (e && e[0] == '0') ? 0 : 1;
   }
   if (!enabled || m <= 0 || n_kv_heads <= 0 || n_q_heads % n_kv_heads) return 1;
-  if (m * (n_q_heads / n_kv_heads) > 2 * kFaTileRows || n_keys < 4096) return 1;
-  return (int32_t)std::min<int64_t>(kMaxAttnSplits, n_keys / 1024);
+  if (n_keys < 4096) return 1;
+  const int64_t G = n_q_heads / n_kv_heads;
+  const int64_t ctas = (m * G + 2 * kFaTileRows - 1) / (2 * kFaTileRows) * n_kv_heads;
+  const int64_t waves2 = 2 * (int64_t)num_sms();
+  if (ctas >= waves2) return 1;
+  int64_t s = (waves2 + ctas - 1) / ctas;
+  s = std::min<int64_t>(s, kMaxAttnSplits);
+  s = std::min<int64_t>(s, n_keys / (kFaMinSplitTiles * kFaKeys));
+  return (int32_t)std::max<int64_t>(1, s);
 }
 
 extern "C" int cc_sparse_row_attention_split(const void* q, int64_t ldq, const int64_t* positions,

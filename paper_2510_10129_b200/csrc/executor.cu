@@ -6,6 +6,7 @@
 // validation, error codes and the launch profiler are shared.
 #include "cc_common.cuh"
 
+#include <algorithm>
 #include <cstdint>
 #include <vector>
 
@@ -26,6 +27,15 @@ struct Carve {
   }
 };
 
+// Rows of split-KV partials a pass of R rows needs: the full-layer launches
+// (R rows, small grids) and the last layer's single head row, each at the
+// largest split count any key count can ask for.
+static int64_t split_part_rows(const cc_model_desc* md, int64_t R) {
+  const int64_t a = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
+  const int64_t b = cc_attention_splits(1, md->n_heads, md->n_kv_heads, INT64_MAX);
+  return std::max<int64_t>(a > 1 ? a * R : 0, b > 1 ? b : 0);
+}
+
 static size_t rows_ws_bytes(const cc_model_desc* md, int64_t R) {
   const size_t d = md->d_model, qw = (size_t)md->n_heads * md->head_dim, ff = md->d_ff;
   size_t s = 0;
@@ -38,12 +48,11 @@ static size_t rows_ws_bytes(const cc_model_desc* md, int64_t R) {
   s += align256(64);                 // head workspace
   s += align256((size_t)((d + 31) / 32) * R * 4);  // fused RMSNorm partial sums
   s += align256((size_t)R * 4);                     // and 1/rms per row
-  // split-KV partials for launches of few rows (decode, the last layer's head
-  // row): sized for the largest split count any key count can ask for
-  const int S = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
-  if (S > 1) {
-    s += align256((size_t)S * R * qw * 4);
-    s += align256((size_t)S * R * md->n_heads * 4);
+  // split-KV partials (small grids: decode, low ratios, the last layer's head row)
+  const int64_t pr = split_part_rows(md, R);
+  if (pr > 0) {
+    s += align256((size_t)pr * qw * 4);
+    s += align256((size_t)pr * md->n_heads * 4);
   }
   return s;
 }
@@ -236,9 +245,9 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
   float* inv_rms = cv.take<float>((size_t)R);
   const bool fuse = fused_norm_enabled() && d % 32 == 0 && md->mlp_gated;
   const NormFuse nf{x, ssq, inv_rms, R, (int)(d / 32), (int)d, md->norm_eps};
-  const int s_max = cc_attention_splits(R, md->n_heads, md->n_kv_heads, INT64_MAX);
-  float* o_parts = s_max > 1 ? cv.take<float>((size_t)s_max * R * qw) : nullptr;
-  float* lse_parts = s_max > 1 ? cv.take<float>((size_t)s_max * R * md->n_heads) : nullptr;
+  const int64_t part_rows = split_part_rows(md, R);
+  float* o_parts = part_rows > 0 ? cv.take<float>((size_t)part_rows * qw) : nullptr;
+  float* lse_parts = part_rows > 0 ? cv.take<float>((size_t)part_rows * md->n_heads) : nullptr;
   CC_TRY(cc_rope_table(positions, R, md->inv_freq, md->head_dim, cs, sn, stream));
   const float factor = (float)(1.0 / sqrt((double)md->head_dim));  // np.float32(1/sqrt(d))
   auto lp = [](const void* base, int64_t stride, int l) -> void* {
@@ -293,7 +302,12 @@ int cc_forward_rows(const cc_model_desc* md, const int64_t* ids, const int64_t* 
       // selection read-back, filled in by cc_profile_fill_work); a last-layer
       // tail launch runs only the final row, which sees the whole bank
       g_attn_flops = 4.0 * md->n_heads * md->head_dim * (r0 == 0 ? attn_pairs : (double)n_keys * Rl);
-      const int n_splits = o_parts ? cc_attention_splits(Rl, md->n_heads, md->n_kv_heads, n_keys) : 1;
+      // never more part rows than the workspace holds
+      const int n_splits =
+          o_parts ? (int)std::max<int64_t>(1, std::min<int64_t>(cc_attention_splits(Rl, md->n_heads,
+                                                                                     md->n_kv_heads, n_keys),
+                                                                 part_rows / Rl))
+                  : 1;
       CC_TRY(cc_sparse_row_attention_split(q + r0 * qw, qw, positions + r0,
                                            plan->key_start ? plan->key_start + r0 : nullptr, Rl,
                                            lp(plan->attn_k, plan->attn_k_stride, l),

@@ -22,6 +22,11 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
+
 namespace cc {
 
 constexpr int kBM = 128;
@@ -201,9 +206,32 @@ template <int BN>
 __device__ __forceinline__ void epilogue_tail(const EpiParams& ep, float* v, int c0, int64_t row0, int nb,
                                               float* stg, int lane);
 
+// split-K: the other K-slices' fp32 partial accumulators of this lane's row,
+// [n_parts][128 rows][BN], added onto the owner's own in slice order (fixed,
+// so the result is deterministic)
+struct SplitParts {
+  const float* p;  // this tile's first partial, row 0 of the CTA (nullptr: no split)
+  int n;           // partials to add
+  int lrow;        // this lane's row within the 128-row tile
+};
+template <int BN>
+__device__ __forceinline__ void add_parts16(const SplitParts& sp, int col, float* v) {
+  for (int s = 0; s < sp.n; ++s) {
+    const float4* src = reinterpret_cast<const float4*>(sp.p + ((size_t)s * kBM + sp.lrow) * BN + col);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 x = __ldcg(src + i);
+      v[4 * i] += x.x;
+      v[4 * i + 1] += x.y;
+      v[4 * i + 2] += x.z;
+      v[4 * i + 3] += x.w;
+    }
+  }
+}
+
 template <int BN, bool kTF32>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tbase, int c0, int64_t row0, int nb,
-                                               float* stg, int lane) {
+                                               float* stg, int lane, const SplitParts& sp = SplitParts{nullptr, 0, 0}) {
   float v[32];
   const bool scaled = ep.ssq_in != nullptr;
   const float rs = scaled ? row_inv_rms(ep, row0 + lane) : 1.f;
@@ -213,6 +241,10 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tba
       float u[16];
       acc_ld16<BN, kTF32>(tbase + c0 + 16 * hh, v + 16 * hh);
       acc_ld16<BN, kTF32>(tbase + c0 + 16 * hh + BN / 2, u);
+      if (sp.p) {
+        add_parts16<BN>(sp, c0 + 16 * hh, v + 16 * hh);
+        add_parts16<BN>(sp, c0 + 16 * hh + BN / 2, u);
+      }
       if (scaled) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -225,6 +257,10 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tba
   } else {
     acc_ld16<BN, kTF32>(tbase + c0, v);
     acc_ld16<BN, kTF32>(tbase + c0 + 16, v + 16);
+    if (sp.p) {
+      add_parts16<BN>(sp, c0, v);
+      add_parts16<BN>(sp, c0 + 16, v + 16);
+    }
     if (scaled) {
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[j] = __fmul_rn(v[j], rs);
@@ -586,6 +622,155 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Split-K variant for bf16 GEMMs whose output tiles cannot fill the SMs (few
+// rows: decode steps, the default 8/5 window rule's tens of recomputed rows).
+// Such GEMMs stream the weights once and are HBM-bound, but tiles << SMs
+// leave most of the machine idle. Work unit u = (tile u / S, K-slice u % S),
+// one unit per CTA (grid <= SMs, so every CTA is resident). Slices 0..S-2
+// write their raw fp32 accumulator to a per-stream workspace and bump the
+// tile's counter (release); slice S-1, the owner, waits for the count
+// (acquire), adds the partials in slice order and runs the normal fused
+// epilogue, then re-arms the counter. Owners are at most tiles < SMs / 2, so
+// the slices they wait for always find an SM.
+// ---------------------------------------------------------------------------
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_splitk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                       EpiParams ep, int num_m, int num_kb, int S, float* __restrict__ parts,
+                       int* __restrict__ counters) {
+  using Cfg = GemmCfg<BN, false>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + Cfg::STAGES * Cfg::A_BYTES;
+  uint8_t* smem_epi = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_epi + kEpiWarps * kEpiStageBytes);
+  uint64_t* empty = full + Cfg::STAGES;
+  uint64_t* tfull = empty + Cfg::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x / S, ks = blockIdx.x % S;
+  const int mb = tile % num_m, nb = tile / num_m;
+  const int per = (num_kb + S - 1) / S;
+  const int kb0 = min(num_kb, ks * per), kb1 = min(num_kb, kb0 + per);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int st = 0; st < Cfg::STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+        uint8_t* sa = smem_a + stage * Cfg::A_BYTES;
+        uint8_t* sb = smem_b + stage * Cfg::B_BYTES;
+        tma_load_2d(sa, &tmA, &full[stage], kb * Cfg::BK, mb * kBM);
+        tma_load_2d(sb, &tmB, &full[stage], kb * Cfg::BK, b_row<BN>(ep, nb, 0));
+        tma_load_2d(sb + Cfg::B_SUB / 2, &tmB, &full[stage], kb * Cfg::BK, b_row<BN>(ep, nb, 1));
+        if (++stage == Cfg::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(smem_a + stage * Cfg::A_BYTES);
+        const uint32_t b0 = smem_u32(smem_b + stage * Cfg::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < Cfg::KSTEPS; ++k)
+          tc_mma<false>(tmem_base, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
+                        (kb > kb0 || k > 0) ? 1u : 0u);
+        tc_commit(&empty[stage]);
+        if (kb == kb1 - 1) tc_commit(tfull);
+      }
+      __syncwarp();
+      if (++stage == Cfg::STAGES) {
+        stage = 0;
+        phase ^= 1;
+      }
+    }
+  } else {
+    const int ew = warp - 2, quarter = warp & 3, chalf = ew >> 2;
+    const int lrow = quarter * 32 + lane;
+    float* stg = reinterpret_cast<float*>(smem_epi + ew * kEpiStageBytes);
+    const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    const int64_t row0 = (int64_t)mb * kBM + quarter * 32;
+    const bool rows_live = row0 < ep.M;  // warp-uniform: this lane quarter holds output rows
+    float* tile_parts = parts + (size_t)tile * (S - 1) * kBM * BN;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+    if (ks < S - 1) {
+      // a K-slice: raw accumulator columns [chalf * BN/2, +BN/2) of this lane's row
+      if (rows_live) {
+        float* dst = tile_parts + ((size_t)ks * kBM + lrow) * BN;
+        for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 16) {
+          float v[16];
+          tmem_ld16(tbase + c, v);
+          if (row0 + lane < ep.M) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              __stcg(reinterpret_cast<float4*>(dst + c) + i,
+                     make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]));
+          }
+        }
+      }
+      __threadfence();
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      if (ew == 0 && lane == 0)
+        asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(counters + tile) : "memory");
+    } else {
+      // the owner: wait for the S-1 slices, add them in order, fused epilogue
+      if (ew == 0 && lane == 0) {
+        int seen = 0;
+        while (true) {
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(counters + tile) : "memory");
+          if (seen >= S - 1) break;
+          __nanosleep(64);
+        }
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      if (rows_live) {
+        const bool glu = ep.epilogue == CC_EPI_GLU;
+        const int cols = glu ? BN / 2 : BN;
+        const int c_begin = chalf * (cols / 2), c_end = c_begin + cols / 2;
+        const SplitParts sp{tile_parts, S - 1, lrow};
+        for (int c0 = c_begin; c0 < c_end; c0 += 32) epilogue_chunk<BN, false>(ep, tbase, c0, row0, nb, stg, lane, sp);
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
+      if (ew == 0 && lane == 0) counters[tile] = 0;  // re-armed for the next launch on this stream
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, BN);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // CTA-pair (cta_group::2) variant for large bf16 GEMMs: a cluster of two CTAs
 // on one TPC owns a 256 x BN tile. Each CTA TMA-loads its own 128 rows of A
 // and one BN/2-row half of B; the leader issues M=256 tcgen05.mma for the
@@ -895,6 +1080,70 @@ static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, 
   return CC_OK;
 }
 
+// Split-K workspace per (device, stream): fp32 partials for every unit of a
+// grid of <= num_sms units, and one counter per tile (zeroed once; each owner
+// re-arms its counter). Per stream, so concurrent streams never share one.
+struct SplitKWs {
+  float* parts = nullptr;
+  int* counters = nullptr;
+};
+constexpr int kSplitKMaxTiles = 1024;
+static int splitk_ws(cudaStream_t st, SplitKWs* out) {
+  static std::mutex mu;
+  static std::map<std::pair<int, cudaStream_t>, SplitKWs> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find({dev, st});
+  if (it == cache.end()) {
+    SplitKWs w;
+    if (cudaMalloc(&w.parts, (size_t)num_sms() * kBM * 256 * sizeof(float)) != cudaSuccess ||
+        cudaMalloc(&w.counters, kSplitKMaxTiles * sizeof(int)) != cudaSuccess ||
+        cudaMemset(w.counters, 0, kSplitKMaxTiles * sizeof(int)) != cudaSuccess)
+      return fail(CC_ERR_CUDA, "split-K workspace allocation failed");
+    it = cache.emplace(std::make_pair(dev, st), w).first;
+  }
+  *out = it->second;
+  return CC_OK;
+}
+
+// K-slices for a bf16 GEMM of `tiles` output tiles over num_kb K-blocks: > 1
+// only when the tiles fill under half the SMs and each slice keeps >= 8
+// K-blocks (CC_GEMM_SPLITK=0 in the environment: never, for A/B runs)
+static int splitk_count(int64_t tiles, int num_kb) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CC_GEMM_SPLITK");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!on || tiles <= 0 || 2 * tiles > num_sms() || tiles > kSplitKMaxTiles) return 1;
+  int s = (int)std::min<int64_t>(num_sms() / tiles, num_kb / 8);
+  s = std::min(s, 16);
+  return s >= 2 ? s : 1;
+}
+
+template <int BN>
+static int launch_splitk(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, int S, cudaStream_t st) {
+  using Cfg = GemmCfg<BN, false>;
+  CUtensorMap ta, tb;
+  int rc = make_map(&ta, a->A, false, kop, a->M, a->lda, Cfg::BK, kBM);
+  if (rc) return rc;
+  rc = make_map(&tb, a->B, false, kop, a->N, a->ldb, Cfg::BK, BN / 2);
+  if (rc) return rc;
+  SplitKWs ws;
+  rc = splitk_ws(st, &ws);
+  if (rc) return rc;
+  set_smem_once<gemm_splitk_kernel<BN>>(Cfg::SMEM_BYTES);
+  const int num_m = (int)((a->M + kBM - 1) / kBM);
+  const int num_n = (int)((a->N + BN - 1) / BN);
+  const int num_kb = (int)((kop + Cfg::BK - 1) / Cfg::BK);
+  ProfScope ps(st, OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
+  gemm_splitk_kernel<BN><<<num_m * num_n * S, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_kb, S,
+                                                                                 ws.parts, ws.counters);
+  CC_LAUNCH_CHECK("gemm (split-K)");
+  return CC_OK;
+}
+
 // CC_GEMM_PAIR=0 in the environment keeps every bf16 GEMM on single-CTA tiles (A/B runs)
 static bool pair_enabled() {
   static int on = -1;
@@ -996,6 +1245,12 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
     const int64_t t128 = ((a->M + kBM - 1) / kBM) * ((a->N + 127) / 128);
     if (a->epilogue != CC_EPI_GLU && 2 * t128 <= num_sms()) return launch<64, true>(a, ep, kop, st);
     return launch<128, true>(a, ep, kop, st);
+  }
+  // bf16 GEMMs of few tiles (few rows): 128-wide tiles cut along K
+  if (a->N % 128 == 0) {
+    const int64_t t128 = ((a->M + kBM - 1) / kBM) * (a->N / 128);
+    const int S = splitk_count(t128, (int)((kop + 63) / 64));
+    if (S > 1) return launch_splitk<128>(a, ep, kop, S, st);
   }
   // large bf16 GEMMs on CTA pairs: 256-row tiles, half the B traffic per SM
   if (pair_enabled() && a->M >= 512 && a->N % 256 == 0) return launch_pair<256, false>(a, ep, kop, st);

@@ -164,12 +164,52 @@ def test_gemm_residual_and_glu():
     assert (h.double() - ref).abs().max().item() < 2e-3
 
 
-def test_gemm_qkv_rope_scatter():
+@pytest.mark.parametrize("M,N,K", [(1, 3584, 3584), (43, 1024, 1024), (128, 3584, 18944), (43, 4608, 3584)])
+def test_gemm_bf16_split_k(M, N, K):
+    """Few-row bf16 GEMMs (decode, the default window rule) run split along K:
+    slices' fp32 partials summed in slice order by the tile owner, then the
+    fused epilogue. Against fp64; bitwise repeatable across launches (the
+    per-tile counters re-arm); residual and GLU epilogues too."""
+    from paper_2510_10129_b200 import _lib as L
+    from paper_2510_10129_b200.weights import _interleave_bias, _interleave_glu
+    g = torch.Generator(device=DEV).manual_seed(M + N + K)
+    A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device=DEV, generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(N, device=DEV, generator=g)
+    ref = A.double() @ B.double().t() + bias.double()
+    outs = []
+    for _ in range(3):
+        C = torch.empty(M, N, device=DEV, dtype=torch.float32)
+        _gemm(L.CC_GEMM_BF16, L.CC_EPI_STORE, A, B, bias=bias, C=C, ldc=N, c_mode=L.CC_F32)
+        outs.append(C)
+    err = (outs[0].double() - ref).abs().max().item()
+    assert err < 1e-4 * math.sqrt(K), err
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    h = torch.randn(M, N, device=DEV, generator=g) if K == N else None
+    if h is not None:  # residual epilogue
+        h0 = h.clone()
+        _gemm(L.CC_GEMM_BF16, L.CC_EPI_RESIDUAL, A, B, C=h, ldc=N, c_mode=L.CC_F32)
+        assert (h.double() - (h0.double() + A.double() @ B.double().t())).abs().max().item() < 1e-4 * math.sqrt(K)
+    if N % 256 == 0:  # GLU (gate/up interleaved in 128-row blocks)
+        FF = N // 2
+        wg, wu = B[:FF].float(), B[FF:].float()
+        W = _interleave_glu(wg, wu).to(torch.bfloat16)
+        b = _interleave_bias(bias[:FF], bias[FF:])
+        out = torch.empty(M, FF, device=DEV, dtype=torch.float32)
+        _gemm(L.CC_GEMM_BF16, L.CC_EPI_GLU, A, W, bias=b, C=out, ldc=FF, c_mode=L.CC_F32, act=L.CC_ACT_SILU,
+              n_out=FF)
+        gate = A.double() @ wg.double().t() + bias[:FF].double()
+        up = A.double() @ wu.double().t() + bias[FF:].double()
+        glu = gate / (1 + torch.exp(-gate)) * up
+        assert (out.double() - glu).abs().max().item() < 2e-4 * math.sqrt(K) * (1 + glu.abs().max().item())
+
+
+@pytest.mark.parametrize("M,d,Hq,Hkv,dh", [(77, 256, 4, 2, 64), (43, 2048, 16, 2, 128)])  # the second splits K
+def test_gemm_qkv_rope_scatter(M, d, Hq, Hkv, dh):
     from paper_2510_10129_b200 import _lib as L
     from paper_2510_10129_b200.config import RopeParams
     from paper_2510_10129_b200.runtime import gemm
     g = torch.Generator(device=DEV).manual_seed(5)
-    M, d, Hq, Hkv, dh = 77, 256, 4, 2, 64
     N = (Hq + 2 * Hkv) * dh
     x = torch.randn(M, d, device=DEV, generator=g).to(torch.bfloat16)
     W = (torch.randn(N, d, device=DEV, generator=g) * 0.05).to(torch.bfloat16)
@@ -320,6 +360,37 @@ def test_split_kv_attention_few_rows(m, S):
         assert lib.cc_attention_splits(1, Hq, Hkv, 32800) == 32
     assert lib.cc_attention_splits(1, Hq, Hkv, 2000) == 1       # short key ranges: never split
     assert lib.cc_attention_splits(6586, Hq, Hkv, 32800) == 1   # full grids: never split
+
+
+@pytest.mark.parametrize("m,n,spread", [(43, 32800, "tail32"), (300, 9000, "sorted"), (557, 32800, "sorted")])
+def test_split_kv_attention_small_grids(m, n, spread):
+    """Low-ratio / default-rule launches (a few hundred rows over a long key
+    bank) take the library's split count; the work-aware parts (long ranges
+    cut, short ones whole, unused parts LSE = -inf) merge to the fp64 reference."""
+    from paper_2510_10129_b200 import _lib as L
+    D, Hq, Hkv = 128, 28, 4
+    g = torch.Generator(device=DEV).manual_seed(m)
+    q = torch.randn(m, Hq, D, device=DEV, generator=g).to(torch.bfloat16)
+    k = (torch.randn(n, Hkv, D, device=DEV, generator=g) * 2).to(torch.bfloat16)
+    v = torch.randn(n, Hkv, D, device=DEV, generator=g).to(torch.bfloat16)
+    if spread == "tail32":  # selected rows spread out, then 32 query rows at the end
+        sel = torch.sort(torch.randperm(n - 32, generator=torch.Generator().manual_seed(3))[:m - 32]).values
+        pos = torch.cat([sel, torch.arange(n - 32, n)]).to(DEV)
+    else:
+        pos = torch.sort(torch.randperm(n, generator=torch.Generator().manual_seed(2))[:m]).values.to(DEV)
+    S = L.load().cc_attention_splits(m, Hq, Hkv, n)
+    assert S > 1
+    out = torch.zeros(m, Hq * D, device=DEV, dtype=torch.bfloat16)
+    o_parts = torch.full((S, m, Hq, D), float("nan"), device=DEV)  # unused parts must never be read
+    lse = torch.empty(S, m, Hq, device=DEV)
+    factor = 1.0 / math.sqrt(D)
+    L.call("cc_sparse_row_attention_split", q.data_ptr(), Hq * D, pos.data_ptr(), None, m, k.data_ptr(),
+           v.data_ptr(), n, Hq, Hkv, D, factor, None, S, o_parts.data_ptr(), lse.data_ptr(), out.data_ptr(),
+           Hq * D, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    _check_attn(out, _attn_ref(q, k, v, pos + 1, factor))
+    # rows whose keys end early leave their late parts empty
+    assert torch.isinf(lse).any()
 
 
 def test_sparse_row_attention_row_factor():
