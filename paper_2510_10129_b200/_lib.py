@@ -136,7 +136,8 @@ _SIGS = {
 }
 
 PROFILE_OPS = ("gemm_bf16", "gemm_3xtf32", "attention_tcgen05", "attention_mma", "banked_attention_f32",
-               "rmsnorm", "assemble_kv", "select_topk", "score_reduce", "lm_head", "rope_table")
+               "rmsnorm", "assemble_kv", "select_topk", "score_reduce", "lm_head", "rope_table", "other",
+               "lse_merge")
 
 
 def profile_enable(on: bool) -> None:

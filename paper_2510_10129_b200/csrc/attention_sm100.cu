@@ -600,40 +600,63 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const
   return CC_OK;
 }
 
-// Split-KV merge: one warp per (row, head), lanes over head_dim.
-template <typename P>
+// Split-KV merge: one warp per (row, head). Lane w reads part w's LSE (parts
+// beyond 32 folded in a second pass), the warp reduces the max, and each lane
+// keeps its part's weight; then every lane owns 4 (D=128) or 2 (D=64) head-dim
+// columns and walks the parts with the weights broadcast by shuffle, four
+// parts' loads in flight at a time (the merge is latency-bound otherwise).
+template <typename P, int D>
 __global__ void lse_merge_kernel(const P* __restrict__ o_parts, const float* __restrict__ lse_parts, int n_parts,
-                                 int64_t part_stride, int64_t m, int hq, int d, void* __restrict__ out, int64_t ldo,
+                                 int64_t part_stride, int64_t m, int hq, void* __restrict__ out, int64_t ldo,
                                  int out_dtype) {
+  constexpr int C = D / 32;  // columns per lane
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= m * hq) return;
   const int64_t i = gw / hq;
   const int h = (int)(gw % hq);
+  const int64_t pstride = part_stride * hq;  // rows of (row, head) between consecutive parts
   float mx = -INFINITY;
-  for (int w = 0; w < n_parts; ++w) mx = fmaxf(mx, lse_parts[(w * part_stride + i) * hq + h]);
-  float wsum = 0.f;
-  float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // d <= 256
-  for (int w = 0; w < n_parts; ++w) {
-    const float l = lse_parts[(w * part_stride + i) * hq + h];
-    if (l == -INFINITY) continue;
-    const float a = exp2f(l - mx);
-    wsum += a;
-    const P* o = o_parts + ((w * part_stride + i) * hq + h) * (int64_t)d;
+  for (int w = lane; w < n_parts; w += 32) mx = fmaxf(mx, lse_parts[w * pstride + i * hq + h]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-      if (lane + 32 * k < d) acc[k] = fmaf(a, static_cast<float>(o[lane + 32 * k]), acc[k]);
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  float acc[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) acc[c] = 0.f;
+  float wsum = 0.f;
+  for (int w0 = 0; w0 < n_parts; w0 += 32) {
+    const int w = w0 + lane;
+    const float l = w < n_parts ? lse_parts[w * pstride + i * hq + h] : -INFINITY;
+    const float a = (l == -INFINITY || mx == -INFINITY) ? 0.f : exp2f(l - mx);
+    const int n = min(32, n_parts - w0);
+    for (int k = 0; k < n; k += 4) {
+      float aw[4];
+      float v[4][C];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        aw[u] = __shfl_sync(0xffffffffu, a, (k + u) & 31);
+        const bool live = k + u < n && aw[u] != 0.f;  // -inf parts are never read (their O is not written)
+        const P* src = o_parts + ((int64_t)(w0 + k + u) * pstride + i * hq + h) * D + lane * C;
+#pragma unroll
+        for (int c = 0; c < C; ++c) v[u][c] = live ? static_cast<float>(src[c]) : 0.f;
+        if (!(k + u < n)) aw[u] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        wsum += aw[u];
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[c] = fmaf(aw[u], v[u][c], acc[c]);
+      }
+    }
   }
   const float inv = wsum > 0.f ? 1.f / wsum : 0.f;
 #pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const int c = lane + 32 * k;
-    if (c >= d) continue;
-    const int64_t off = i * ldo + (int64_t)h * d + c;
+  for (int c = 0; c < C; ++c) {
+    const int64_t off = i * ldo + (int64_t)h * D + lane * C + c;
     if (out_dtype == CC_BF16)
-      reinterpret_cast<__nv_bfloat16*>(out)[off] = __float2bfloat16_rn(acc[k] * inv);
+      reinterpret_cast<__nv_bfloat16*>(out)[off] = __float2bfloat16_rn(acc[c] * inv);
     else
-      reinterpret_cast<float*>(out)[off] = acc[k] * inv;
+      reinterpret_cast<float*>(out)[off] = acc[c] * inv;
   }
 }
 
@@ -774,6 +797,7 @@ extern "C" int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const
   if (n_keys <= 0) {  // an empty shard contributes nothing: O = 0, LSE = -inf
     cudaMemsetAsync(o_part, 0, (size_t)m * n_q_heads * head_dim * (part_bf16 ? 2 : 4), st);
     const int64_t n = m * n_q_heads;
+    ProfScope ps(st, OP_OTHER, 0);
     fill_neg_inf_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(lse, n);
     CC_LAUNCH_CHECK("partial attention (empty shard)");
     return CC_OK;
@@ -788,6 +812,7 @@ extern "C" int cc_sparse_row_attention_partial(const void* q, int64_t ldq, const
 extern "C" int cc_local_limits(const int64_t* row_pos, int64_t m, const int64_t* local_pos, int64_t n_local,
                                int64_t* limits, void* stream) {
   if (m <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_OTHER, 0);
   local_limits_kernel<<<(unsigned)((m + 255) / 256), 256, 0, as_stream(stream)>>>(row_pos, m, local_pos, n_local,
                                                                                   limits);
   CC_LAUNCH_CHECK("local_limits");
@@ -797,19 +822,22 @@ extern "C" int cc_local_limits(const int64_t* row_pos, int64_t m, const int64_t*
 extern "C" int cc_lse_merge(const void* o_parts, int32_t part_dtype, const float* lse_parts, int32_t n_parts,
                             int64_t part_stride, int64_t m, int32_t n_q_heads, int32_t head_dim, void* out,
                             int64_t ldo, int32_t out_dtype, void* stream) {
-  CC_CHECK_ARG(head_dim > 0 && head_dim <= 256, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
+  CC_CHECK_ARG(head_dim == 64 || head_dim == 128, CC_ERR_UNSUPPORTED, "head_dim %d unsupported", head_dim);
   CC_CHECK_ARG(part_dtype == CC_F32 || part_dtype == CC_BF16, CC_ERR_UNSUPPORTED, "partial dtype %d", part_dtype);
   if (m <= 0 || n_parts <= 0) return CC_OK;
   const int64_t warps = m * n_q_heads;
   const unsigned grid = (unsigned)((warps * 32 + 255) / 256);
-  if (part_dtype == CC_BF16)
-    lse_merge_kernel<__nv_bfloat16><<<grid, 256, 0, as_stream(stream)>>>(
-        static_cast<const __nv_bfloat16*>(o_parts), lse_parts, n_parts, part_stride, m, n_q_heads, head_dim, out,
-        ldo, out_dtype);
-  else
-    lse_merge_kernel<float><<<grid, 256, 0, as_stream(stream)>>>(static_cast<const float*>(o_parts), lse_parts,
-                                                                 n_parts, part_stride, m, n_q_heads, head_dim, out,
-                                                                 ldo, out_dtype);
+  cudaStream_t st = as_stream(stream);
+  ProfScope ps(st, OP_MERGE, 0.0);
+#define CC_MERGE(P, D)                                                                                             \
+  lse_merge_kernel<P, D><<<grid, 256, 0, st>>>(static_cast<const P*>(o_parts), lse_parts, n_parts, part_stride, m, \
+                                               n_q_heads, out, ldo, out_dtype)
+  if (part_dtype == CC_BF16) {
+    if (head_dim == 128) CC_MERGE(__nv_bfloat16, 128); else CC_MERGE(__nv_bfloat16, 64);
+  } else {
+    if (head_dim == 128) CC_MERGE(float, 128); else CC_MERGE(float, 64);
+  }
+#undef CC_MERGE
   CC_LAUNCH_CHECK("lse_merge");
   return CC_OK;
 }

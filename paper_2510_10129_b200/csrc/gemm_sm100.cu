@@ -460,10 +460,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+#ifdef CC_DBG_GEMM_NO_LOADS  // perf experiments only: after the first ring, stages are released without data
+      int issued = 0;
+#endif
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int mb = t % num_m, nb = t / num_m;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+#ifdef CC_DBG_GEMM_NO_LOADS
+          if (issued++ >= Cfg::STAGES) {
+            mbar_arrive(&full[stage]);
+            if (++stage == Cfg::STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+#endif
           mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           uint8_t* sa = smem_a + stage * Cfg::A_BYTES;
           uint8_t* sb = smem_b + stage * Cfg::B_BYTES;
@@ -518,8 +531,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               // lo*hi into the correction accumulator
               tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC2,
                             (kp | k) != 0 ? 1u : 0u);
+#ifndef CC_DBG_TF32_NO_LOHI  // perf experiments only: drop the lo*hi MMA
               tc_mma<kTF32>(d_tmem + BN, umma_desc_sw128(a0 + Cfg::A_SUB + k * 32), umma_desc_sw128(b0 + k * 32),
                             Cfg::IDESC, 1u);
+#endif
             } else {
               tc_mma<kTF32>(d_tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
                             (kp | k) != 0 ? 1u : 0u);

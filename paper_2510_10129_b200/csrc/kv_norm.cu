@@ -655,6 +655,7 @@ int cc_upload(void* dst_dev, const void* src_pinned, int64_t bytes, void* stream
                CC_ERR_UNSUPPORTED, "upload buffers must be 16-byte aligned");
   const int64_t n16 = bytes >> 4;
   const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>((n16 + 255) / 256, 1), 64);
+  ProfScope ps(as_stream(stream), OP_OTHER, 0);
   upload_kernel<<<grid, 256, 0, as_stream(stream)>>>(static_cast<uint8_t*>(dst_dev),
                                                      static_cast<const uint8_t*>(src_pinned), bytes);
   CC_LAUNCH_CHECK("upload");
@@ -773,6 +774,7 @@ int cc_norm_prep(const float* h, int64_t rows, int32_t d, int64_t ld_h, const fl
   CC_CHECK_ARG(d > 0 && d % 32 == 0 && ld_h % 4 == 0 && ld_ssq >= rows, CC_ERR_UNSUPPORTED,
                "norm_prep needs d %% 32 == 0 (d=%d), ld_h %% 4 == 0 and ld_ssq >= rows", d);
   if (rows <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_NORM, 0);
   norm_prep_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, as_stream(stream)>>>(
       h, rows, d, ld_h, gain, reinterpret_cast<__nv_bfloat16*>(xn_out), ssq_out, ld_ssq);
   CC_LAUNCH_CHECK("norm_prep");
@@ -784,6 +786,7 @@ int cc_norm_finalize(const float* ssq, int64_t rows, int32_t d, int64_t ld_ssq, 
   CC_CHECK_ARG(ssq && inv_rms, CC_ERR_VALUE, "null norm_finalize argument");
   CC_CHECK_ARG(d > 0 && d % 32 == 0 && ld_ssq >= rows, CC_ERR_UNSUPPORTED, "norm_finalize needs d %% 32 == 0");
   if (rows <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_NORM, 0);
   norm_finalize_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, as_stream(stream)>>>(ssq, rows, d / 32, ld_ssq,
                                                                                       1.0f / (float)d, eps, inv_rms);
   CC_LAUNCH_CHECK("norm_finalize");
@@ -804,6 +807,7 @@ int cc_convert_matrix(const float* src, int64_t rows, int64_t cols, void* dst, i
                       int32_t split_weight, void* stream) {
   const int64_t n = rows * cols;
   if (n <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_OTHER, 0);
   convert_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(src, rows, cols, dst, dst_mode, split_weight);
   CC_LAUNCH_CHECK("convert_matrix");
   return CC_OK;
@@ -813,6 +817,7 @@ int cc_build_rows(const int64_t* sel, int64_t m, const int64_t* token_ids, const
                   int64_t base, int64_t* ids_out, int64_t* pos_out, void* stream) {
   const int64_t n = m + nq;
   if (n <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_OTHER, 0);
   build_rows_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(sel, m, token_ids, query_ids, nq, base, ids_out,
                                                                      pos_out);
   CC_LAUNCH_CHECK("build_rows");
@@ -821,6 +826,7 @@ int cc_build_rows(const int64_t* sel, int64_t m, const int64_t* token_ids, const
 
 int cc_gather_i64(const int64_t* src, const int64_t* idx, int64_t n, int64_t* dst, void* stream) {
   if (n <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_OTHER, 0);
   gather_i64_kernel<<<(n + 255) / 256, 256, 0, as_stream(stream)>>>(src, idx, n, dst);
   CC_LAUNCH_CHECK("gather_i64");
   return CC_OK;

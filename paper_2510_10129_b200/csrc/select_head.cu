@@ -319,6 +319,7 @@ int cc_row_l2_diff(const void* a, int32_t a_dtype, int64_t lda, const void* b, i
   CC_CHECK_ARG((a_dtype == CC_BF16 || a_dtype == CC_F32) && (b_dtype == CC_BF16 || b_dtype == CC_F32),
                CC_ERR_UNSUPPORTED, "dtypes %d / %d", a_dtype, b_dtype);
   if (n <= 0) return CC_OK;
+  ProfScope ps(as_stream(stream), OP_OTHER, 0);
   row_l2_diff_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, as_stream(stream)>>>(a, a_dtype, lda, b, b_dtype,
                                                                                        ldb, n, width, out);
   CC_LAUNCH_CHECK("row_l2_diff");
