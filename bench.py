@@ -575,6 +575,20 @@ def run_ours(args, rank: int, world: int):
         e2e = {"value": world * m_sel / (e2e_ms * 1e-3), "unit": "tok/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(4 * primary.config.vocab_size + 8 +
                                                                           8 * (work.n_tokens + 1))}
+        # e2e across the sweep's ratios (exact-budget rule): the same H2D per
+        # request, so at low ratios the PCIe stream, not the recompute, bounds it
+        if sweep:
+            for r in (0.05, 0.1, 0.2, 0.4):
+                cfg_r = cc.SelectionConfig(r, 8, args.window_threshold)
+                cc.cacheclip_prefill(primary, aux, pc, ac, list(query), cfg_r)
+                torch.cuda.synchronize()
+                tr = []
+                for _ in range(3):
+                    t1 = time.perf_counter()
+                    cc.cacheclip_prefill(primary, aux, pc, ac, list(query), cfg_r)
+                    tr.append(time.perf_counter() - t1)
+                sweep[f"{r:.2f}"]["e2e_ms"] = float(np.median(tr)) * 1e3
+                sweep[f"{r:.2f}"]["e2e_h2d_gbs"] = h2d / (float(np.median(tr)) * 1e9)
 
     cpu = None
     if rank == 0 and world == 1 and not args.skip_cpu:

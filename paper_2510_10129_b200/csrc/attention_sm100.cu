@@ -50,7 +50,7 @@ __device__ long long g_fa_trace[16 * 128];
 constexpr int kFaTileRows = 128;
 constexpr int kFaKeys = 128;
 constexpr int kFaThreads = 384;  // 3 warpgroups: producer/MMA, softmax A, softmax B
-constexpr int kFaCtlRegs = 56;    // setmaxnreg budgets: 128*56 + 256*224 <= 64K
+constexpr int kFaCtlRegs = 56;    // setmaxnreg budgets: 128*56 + 256*224 = 384*168 (the launch allocation)
 constexpr int kFaSoftmaxRegs = 224;
 constexpr float kFaRescaleThreshold = 8.0f;  // log2 domain
 constexpr int kMaxAttnSplits = 32;
@@ -97,6 +97,18 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+// warp-wide form (see tc_mma_warp in cc_common.cuh): the whole warp calls
+// with uniform operands, one elected lane issues
+__device__ __forceinline__ void tc_mma_ts_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
@@ -359,32 +371,31 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       }
     } else if (warp == 1) {
       // ---------------- MMA issuer (ping-pong over the two query tiles) ----------------
+      // the whole warp issues (one elected lane per tcgen05 op) from
+      // warp-uniform descriptors formed once
+      const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint64_t qdesc0 = umma_desc_sw128(smem_u32(sQ));
+      const uint64_t kdesc0 = umma_desc_sw128(smem_u32(sK));
+      const uint64_t vdesc0 = umma_desc_mn_sw128(smem_u32(sV), kFaKeys * 128, 1024);
       auto issue_s = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
-        if (lane == 0) {
-          const uint32_t q0 = smem_u32(sQ + t * Cfg::QT_BYTES), k0 = smem_u32(sK + (j & 1) * Cfg::KT_BYTES);
-  #pragma unroll
-          for (int k = 0; k < D / 16; ++k) {
-            const uint32_t qo = (k >> 2) * (kFaTileRows * 128) + (k & 3) * 32;
-            const uint32_t ko = (k >> 2) * (kFaKeys * 128) + (k & 3) * 32;
-            tc_mma<false>(tmem + Cfg::s_col(t), umma_desc_sw128(q0 + qo), umma_desc_sw128(k0 + ko), Cfg::IDESC_S,
-                          k > 0 ? 1u : 0u);
-          }
-          tc_commit(&s_full[t]);
+        const uint64_t qd = qdesc0 + (uint64_t)((t * Cfg::QT_BYTES) >> 4);
+        const uint64_t kd = kdesc0 + (uint64_t)(((j & 1) * Cfg::KT_BYTES) >> 4);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t qo = (k >> 2) * (kFaTileRows * 128) + (k & 3) * 32;
+          const uint32_t ko = (k >> 2) * (kFaKeys * 128) + (k & 3) * 32;
+          tc_mma_warp<false>(tmem_u + Cfg::s_col(t), qd + (qo >> 4), kd + (ko >> 4), Cfg::IDESC_S, k > 0 ? 1u : 0u);
         }
-        __syncwarp();
+        tc_commit_warp(&s_full[t]);
       };
       auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P read from TMEM (over S_t)
         mbar_wait(&p_full[t], j & 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t v0 = smem_u32(sV + (j & 1) * Cfg::KT_BYTES);
-  #pragma unroll
-          for (int k = 0; k < kFaKeys / 16; ++k)
-            tc_mma_ts(tmem + Cfg::o_col(t), tmem + Cfg::s_col(t) + k * 8,
-                      umma_desc_mn_sw128(v0 + k * 16 * 128, kFaKeys * 128, 1024), Cfg::IDESC_PV,
-                      (j > 0 || k > 0) ? 1u : 0u);
-        }
-        __syncwarp();
+        const uint64_t vd = vdesc0 + (uint64_t)(((j & 1) * Cfg::KT_BYTES) >> 4);
+#pragma unroll
+        for (int k = 0; k < kFaKeys / 16; ++k)
+          tc_mma_ts_warp(tmem_u + Cfg::o_col(t), tmem_u + Cfg::s_col(t) + k * 8, vd + ((k * 16 * 128) >> 4),
+                         Cfg::IDESC_PV, (j > 0 || k > 0) ? 1u : 0u);
       };
       if (n_tiles > 0) {
         mbar_wait(&k_full[0], 0);
@@ -404,13 +415,11 @@ __global__ void __launch_bounds__(kFaThreads, 1)
           }
           issue_pv(1, j);
           FA_T(6, j);
-          if (lane == 0) tc_commit(&kv_empty[j & 1]);
-          __syncwarp();
+          tc_commit_warp(&kv_empty[j & 1]);
           if (more) issue_s(1, j + 1);
           FA_T(7, j);
         }
-        if (lane == 0) tc_commit(pv_done);
-        __syncwarp();
+        tc_commit_warp(pv_done);
       }
     }
   } else {
