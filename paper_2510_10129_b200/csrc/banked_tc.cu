@@ -82,6 +82,17 @@ __device__ __forceinline__ void tc_mma_ts_tf32(uint32_t d_tmem, uint32_t a_tmem,
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
+// warp-wide form (see tc_mma_warp in cc_common.cuh)
+__device__ __forceinline__ void tc_mma_ts_tf32_warp(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                    uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void tmem_st32_f(uint32_t taddr, const float* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
@@ -236,6 +247,11 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // warp-uniform MMA operands for warp 0's issue (descriptors formed once)
+  const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem, 0);
+  const uint64_t dq_h = umma_desc_sw128(smem_u32(sQh)), dq_l = umma_desc_sw128(smem_u32(sQl));
+  const uint64_t dk_h = umma_desc_sw128(smem_u32(sKh)), dk_l = umma_desc_sw128(smem_u32(sKl));
+  const uint64_t dv_h = umma_desc_sw128(smem_u32(sVh)), dv_l = umma_desc_sw128(smem_u32(sVl));
   const uint32_t tl = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // this warp's TMEM lane quarter
   const uint32_t t_s = tl + Cfg::T_S + half * HC;
 
@@ -253,18 +269,16 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
       tc_fence_before();
       __syncthreads();  // also: every thread has read S(j-1) before S(j) overwrites it
       tc_fence_after();
-      if (tid == 0) {
-        const uint32_t q0h = smem_u32(sQh), q0l = smem_u32(sQl), k0h = smem_u32(sKh), k0l = smem_u32(sKl);
+      if (warp == 0) {  // warp-wide issue from uniform descriptors (one elected lane per op)
 #pragma unroll
         for (int k = 0; k < HD / 8; ++k) {
-          const uint32_t qo = (k >> 2) * (kBtRows * 128) + (k & 3) * 32;
-          const uint32_t ko = (k >> 2) * (kBtKeys * 128) + (k & 3) * 32;
-          tc_mma<true>(tmem + Cfg::T_S, umma_desc_sw128(q0h + qo), umma_desc_sw128(k0h + ko), Cfg::IDESC_S,
-                       k > 0 ? 1u : 0u);
-          tc_mma<true>(tmem + Cfg::T_S, umma_desc_sw128(q0h + qo), umma_desc_sw128(k0l + ko), Cfg::IDESC_S, 1u);
-          tc_mma<true>(tmem + Cfg::T_S, umma_desc_sw128(q0l + qo), umma_desc_sw128(k0h + ko), Cfg::IDESC_S, 1u);
+          const uint32_t qo = ((k >> 2) * (kBtRows * 128) + (k & 3) * 32) >> 4;
+          const uint32_t ko = ((k >> 2) * (kBtKeys * 128) + (k & 3) * 32) >> 4;
+          tc_mma_warp<true>(tmem_u + Cfg::T_S, dq_h + qo, dk_h + ko, Cfg::IDESC_S, k > 0 ? 1u : 0u);
+          tc_mma_warp<true>(tmem_u + Cfg::T_S, dq_h + qo, dk_l + ko, Cfg::IDESC_S, 1u);
+          tc_mma_warp<true>(tmem_u + Cfg::T_S, dq_l + qo, dk_h + ko, Cfg::IDESC_S, 1u);
         }
-        tc_commit(s_bar);
+        tc_commit_warp(s_bar);
       }
       if (j + 1 < n_tiles) fetch(j + 1, with_v);  // in flight during the MMA and the softmax
       mbar_wait(s_bar, s_phase);
@@ -379,16 +393,16 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
       tc_fence_before();
       __syncthreads();
       tc_fence_after();
-      if (tid == 0) {
-        const uint32_t v0h = smem_u32(sVh), v0l = smem_u32(sVl);
+      if (warp == 0) {
 #pragma unroll
         for (int k = 0; k < kBtKeys / 8; ++k) {
-          const uint64_t bh = umma_desc_sw128(v0h + k * 32), bl = umma_desc_sw128(v0l + k * 32);
-          tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PH + k * 8, bh, Cfg::IDESC_PV, (j > 0 || k > 0) ? 1u : 0u);
-          tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PH + k * 8, bl, Cfg::IDESC_PV, 1u);
-          tc_mma_ts_tf32(tmem + Cfg::T_O, tmem + Cfg::T_PL + k * 8, bh, Cfg::IDESC_PV, 1u);
+          const uint64_t bh = dv_h + 2 * k, bl = dv_l + 2 * k;
+          tc_mma_ts_tf32_warp(tmem_u + Cfg::T_O, tmem_u + Cfg::T_PH + k * 8, bh, Cfg::IDESC_PV,
+                              (j > 0 || k > 0) ? 1u : 0u);
+          tc_mma_ts_tf32_warp(tmem_u + Cfg::T_O, tmem_u + Cfg::T_PH + k * 8, bl, Cfg::IDESC_PV, 1u);
+          tc_mma_ts_tf32_warp(tmem_u + Cfg::T_O, tmem_u + Cfg::T_PL + k * 8, bh, Cfg::IDESC_PV, 1u);
         }
-        tc_commit(pv_bar);
+        tc_commit_warp(pv_bar);
       }
     });
     float l_other, unused;
