@@ -62,6 +62,10 @@ int cc_abi_version(void);
 const char* cc_last_error(void);
 /* Returns CC_OK when device `dev` is sm_100 (B200) and the kernels load. */
 int cc_device_check(int dev);
+/* Self-check of the batched SiLU the GLU epilogues use (silu_n, cc_common.cuh)
+ * against the per-element x / (1 + exp(-x)) with IEEE division: writes the
+ * number of bitwise mismatches over x[0..n) to *mismatches (device int64). */
+int cc_check_silu(const float* x, int64_t n, int64_t* mismatches, void* stream);
 
 /* ------------------------------------------------------------------------
  * (1) KV assembly — replaces the per-layer concatenate + rope_apply in

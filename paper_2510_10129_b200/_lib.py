@@ -90,6 +90,7 @@ _SIGS = {
     "cc_abi_version": ([], i32),
     "cc_last_error": ([], ctypes.c_char_p),
     "cc_device_check": ([i32], i32),
+    "cc_check_silu": ([vp, i64, vp, vp], i32),
     "cc_assemble_kv": ([vp, i32, i64, i32, i32, i32, i32, vp, i64, vp, vp, i64, vp], i32),
     "cc_upload": ([vp, vp, i64, vp], i32),
     "cc_h2d_uniform": ([vp, vp, i64, i64, vp, vp, i64, i64, i64, i32, i32, i32, vp], i32),

@@ -208,15 +208,23 @@ __device__ __forceinline__ void acc_ld16(uint32_t taddr, float* v) {
 template <int BN, int kEpi = -1>
 __device__ __forceinline__ void glu16(const EpiParams& ep, int nb, int c, float* g16, const float* u16) {
   const int64_t gcol = b_row<BN, kEpi>(ep, nb, 0) + c;  // interleaved gate row of column c
+  float up[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    float g = g16[j], up = u16[j];
+    up[j] = u16[j];
     if (ep.bias) {
-      g += ep.bias[gcol + j];
-      up += ep.bias[gcol + ep.glu_block + j];
+      g16[j] += ep.bias[gcol + j];
+      up[j] += ep.bias[gcol + ep.glu_block + j];
     }
-    g16[j] = __fmul_rn(act_apply(ep.act, g), up);
   }
+  if (ep.act == CC_ACT_SILU) {
+    silu_n<16>(g16);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) g16[j] = gelu_tanh_f(g16[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) g16[j] = __fmul_rn(g16[j], up[j]);
 }
 
 template <int BN, int kEpi = -1>
@@ -644,7 +652,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             acc_phase ^= 1;
           }
         }
-        if (ew == 0) GT(4, 2 * tile_i);
+        if (ew == 0) GT(4, 3 * tile_i);
 #if defined(CC_DBG_GEMM_NO_EPI) || defined(CC_DBG_GEMM_NO_FINAL)
         if (false)
 #endif
@@ -654,13 +662,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           for (int cc = 0; cc < NV / 2; cc += 32) {
             glu16<BN, kEpi>(ep, nb, c_begin + cc, run + cc, run + NV / 2 + cc);
             glu16<BN, kEpi>(ep, nb, c_begin + cc + 16, run + cc + 16, run + NV / 2 + cc + 16);
+            if (ew == 0) GT(4, 3 * tile_i + 1);
             epilogue_tail<BN, kEpi>(ep, run + cc, c_begin + cc, row0, nb, stg, lane);
           }
         } else {
 #pragma unroll
           for (int cc = 0; cc < NV; cc += 32) epilogue_tail<BN, kEpi>(ep, run + cc, c_begin + cc, row0, nb, stg, lane);
         }
-        if (ew == 0) GT(4, 2 * tile_i + 1);
+        if (ew == 0) GT(4, 3 * tile_i + 2);
         ++tile_i;
       } else {
         mbar_wait(&tfull[acc], acc_phase);

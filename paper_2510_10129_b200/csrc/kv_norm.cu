@@ -564,6 +564,25 @@ __global__ void __launch_bounds__(256) norm_prep_kernel(const float* __restrict_
   }
 }
 
+// one thread per 16 values: silu_n<16> (the GLU epilogues' batched form)
+// against silu_f element by element, bitwise
+__global__ void silu_check_kernel(const float* __restrict__ x, int64_t n, int64_t* __restrict__ mismatches) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g * 16 >= n) return;
+  float v[16], w[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int64_t i = g * 16 + j;
+    v[j] = i < n ? x[i] : 0.f;
+    w[j] = silu_f(v[j]);
+  }
+  silu_n<16>(v);
+  int bad = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) bad += (g * 16 + j < n) && (__float_as_uint(v[j]) != __float_as_uint(w[j]));
+  if (bad) atomicAdd(reinterpret_cast<unsigned long long*>(mismatches), (unsigned long long)bad);
+}
+
 extern "C" {
 
 int cc_abi_version(void) { return CC_ABI_VERSION; }
@@ -600,6 +619,14 @@ void cc_profile_fill_work(int32_t op, double work) {
 }
 
 const char* cc_last_error(void) { return g_err; }
+
+int cc_check_silu(const float* x, int64_t n, int64_t* mismatches, void* stream) {
+  if (n <= 0) return CC_OK;
+  const int64_t groups = (n + 15) / 16;
+  silu_check_kernel<<<(unsigned)((groups + 255) / 256), 256, 0, as_stream(stream)>>>(x, n, mismatches);
+  CC_LAUNCH_CHECK("check_silu");
+  return CC_OK;
+}
 
 int cc_device_check(int dev) {
   cudaDeviceProp prop;

@@ -61,9 +61,10 @@ ne = int(np.count_nonzero(t[3])) // 2
 e = t[3, :2 * ne].reshape(ne, 2) - t0
 fold = e[1:, 0] - e[:-1, 1]  # from tfull seen to the next phase's wait start: fold (+ tile epilogue)
 print(f"  epilogue phases {ne}: fold+epilogue per phase median {np.median(fold):.0f}, max {fold.max():.0f} clk")
-nt = int(np.count_nonzero(t[4])) // 2
+nt = int(np.count_nonzero(t[4])) // 3
 if nt:
-    fe = t[4, :2 * nt].reshape(nt, 2)
-    print(f"  final epilogue per tile ({nt} tiles): median {np.median(fe[:, 1] - fe[:, 0]):.0f} clk")
+    fe = t[4, :3 * nt].reshape(nt, 3)
+    print(f"  final epilogue per tile ({nt} tiles): median {np.median(fe[:, 2] - fe[:, 0]):.0f} clk "
+          f"(GLU math {np.median(fe[:, 1] - fe[:, 0]):.0f}, store tail {np.median(fe[:, 2] - fe[:, 1]):.0f})")
 for i in range(min(n, 40)):
     print(f"    kb {i:3d}: start {start[i]:9.0f}  tempty {w_tempty[i]:6.0f}  full {w_full[i]:6.0f}")

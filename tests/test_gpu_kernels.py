@@ -558,3 +558,23 @@ def test_streamed_merge_from_pinned_host_matches_device_merge():
     r2 = cc.cacheclip_prefill(primary, aux, host, host_aux, query, cfg)
     assert r1.plan.indices == r2.plan.indices
     np.testing.assert_array_equal(r1.logits, r2.logits)
+
+
+def test_batched_silu_is_bitwise_the_ieee_formula():
+    """The GLU epilogues' batched SiLU (div.rn fast path for the whole chunk,
+    exact fallback outside its range) equals x / (1 + exp(-x)) with IEEE
+    division bit for bit, over normal, tiny, huge, subnormal and special inputs."""
+    from paper_2510_10129_b200 import _lib as L
+    g = torch.Generator(device=DEV).manual_seed(7)
+    parts = [torch.randn(1 << 20, device=DEV, generator=g) * s for s in (0.01, 1.0, 10.0, 60.0)]
+    bits = torch.randint(0, 2 ** 31 - 1, (1 << 20,), device=DEV, generator=g, dtype=torch.int64).to(torch.int32)
+    parts.append(bits.view(torch.float32))           # every exponent, both signs via the next line
+    parts.append(-bits.view(torch.float32))
+    parts.append(torch.tensor([0.0, -0.0, 1e-45, -1e-45, 1e-38, -1e-38, 88.0, -88.0, 89.0, -89.0, 104.0,
+                               -104.0, 3e38, -3e38, float("inf"), float("-inf")], device=DEV))
+    x = torch.cat(parts).contiguous()
+    x = x[torch.isfinite(x) | torch.isinf(x)]   # NaN payloads excluded (NaN != NaN bitwise is not a defect)
+    bad = torch.zeros(1, dtype=torch.int64, device=DEV)
+    L.call("cc_check_silu", x.data_ptr(), x.numel(), bad.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
