@@ -422,6 +422,11 @@ def run_ours(args, rank: int, world: int):
     roof.update(kernel=top, frac=roof["achieved"] / roof["peak"], traffic=ncu_traffic(top),
                 share_of_step=tv["ms"] / n_prof / ttft,
                 peak_source=f"{pk['source']} ({'HBM copy' if roof['bound'] == 'hbm' else 'bf16 sustained'})")
+    if roof["bound"] == "tensor" and pk.get("bf16"):
+        # the sustained figure is cuBLAS 8192^3 back to back for 4 s on this pod;
+        # the kernel runs inside a power-capped step too, and may beat it: the
+        # burst figure bounds it from above
+        roof.update(peak_burst=pk["bf16"], frac_of_burst=roof["achieved"] / pk["bf16"])
     stages = None
 
     # ---- full-attention prefill of the same primary on the same GPU -------
@@ -694,6 +699,11 @@ def run_sharded(args, rank: int, world: int):
     full_ms = None
     if world == 1 and not args.skip_full:
         ids = cc.reuse_context_ids(chunks, query)
+        # the chunk caches (tens of GB at C4) are not needed by the dense prefill
+        del chunks, aux_chunks
+        out_indices, out_first = out.indices, out.first_token
+        out = None
+        torch.cuda.empty_cache()
         cc.full_attention_prefill(primary, ids)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -702,9 +712,11 @@ def run_sharded(args, rank: int, world: int):
         b.record()
         torch.cuda.synchronize()
         full_ms = float(a.elapsed_time(b))
+    else:
+        out_indices, out_first = out.indices, out.first_token
     if rank != 0:
         return
-    m_sel = len(out.indices)
+    m_sel = len(out_indices)
     line = {
         "metric": f"recomputed tok/s at recomp {args.ratio:.0%}, {work.name} RAG prefill (TTFT in ms_per_step)",
         "value": m_sel / (ttft * 1e-3), "unit": "tok/s", "n_gpus": world, "steps": args.steps,
@@ -714,7 +726,7 @@ def run_sharded(args, rank: int, world: int):
                    "recomputed_rows": m_sel, "parallelism": f"sequence-sharded x{world} (chunk round-robin, "
                    "split-KV + LSE merge over NCCL)",
                    "window_rule": f"window_len=8, threshold={args.window_threshold}"},
-        "ttft_ms": ttft, "first_token": out.first_token, "clocks": clocks.summary(), "setup_s": setup_s,
+        "ttft_ms": ttft, "first_token": out_first, "clocks": clocks.summary(), "setup_s": setup_s,
         "full_prefill_ms": full_ms, "speedup_vs_full": (full_ms / ttft) if full_ms else None,
     }
     print(json.dumps(line), flush=True)

@@ -251,7 +251,7 @@ int cc_sparse_row_attention_split(const void* q, int64_t ldq, const int64_t* pos
                                   const float* row_factor, int32_t n_splits, float* o_parts, float* lse_parts,
                                   void* out, int64_t ldo, void* stream);
 /* The split count cc_forward_rows uses: > 1 only when the launch's
- * ceil(m * (Hq / Hkv) / 256) * Hkv CTAs are under two waves of the SMs and
+ * ceil(m * (Hq / Hkv) / 256) * Hkv CTAs are under one wave of the SMs and
  * the keys are >= 4096 (up to 32 parts, at least 1024 keys each); 1
  * otherwise. Inside the kernel a CTA uses one part per 8 key tiles of its
  * own range at most (unused parts report LSE = -inf). */

@@ -519,13 +519,24 @@ using namespace cc;
 // lane l covers 4 columns, 8-lane groups = one 32-column chunk.
 // thread per row: the partials in a fixed order (deterministic), then
 // 1 / sqrt(mean + eps) with correctly rounded sqrt and division
-__global__ void __launch_bounds__(256) norm_finalize_kernel(const float* __restrict__ ssq, int64_t rows, int parts,
-                                                            int64_t ld, float inv_d, float eps,
-                                                            float* __restrict__ inv_rms) {
-  const int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x;
+// One thread per row, the partial sums added in part order (deterministic);
+// 32 loads in flight per thread and 64-thread blocks (a few thousand rows
+// would otherwise occupy a few dozen SMs, each waiting out ~14 round trips).
+constexpr int kFinThreads = 64;
+__global__ void __launch_bounds__(kFinThreads) norm_finalize_kernel(const float* __restrict__ ssq, int64_t rows,
+                                                                    int parts, int64_t ld, float inv_d, float eps,
+                                                                    float* __restrict__ inv_rms) {
+  const int64_t r = (int64_t)blockIdx.x * kFinThreads + threadIdx.x;
   if (r >= rows) return;
   float s = 0.f;
   int i = 0;
+  for (; i + 32 <= parts; i += 32) {
+    float t[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) t[j] = __ldg(ssq + (int64_t)(i + j) * ld + r);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s = __fadd_rn(s, t[j]);
+  }
   for (; i + 8 <= parts; i += 8) {
     float t[8];
 #pragma unroll
@@ -814,8 +825,8 @@ int cc_norm_finalize(const float* ssq, int64_t rows, int32_t d, int64_t ld_ssq, 
   CC_CHECK_ARG(d > 0 && d % 32 == 0 && ld_ssq >= rows, CC_ERR_UNSUPPORTED, "norm_finalize needs d %% 32 == 0");
   if (rows <= 0) return CC_OK;
   ProfScope ps(as_stream(stream), OP_NORM, 0);
-  norm_finalize_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, as_stream(stream)>>>(ssq, rows, d / 32, ld_ssq,
-                                                                                      1.0f / (float)d, eps, inv_rms);
+  norm_finalize_kernel<<<(unsigned)((rows + kFinThreads - 1) / kFinThreads), kFinThreads, 0, as_stream(stream)>>>(
+      ssq, rows, d / 32, ld_ssq, 1.0f / (float)d, eps, inv_rms);
   CC_LAUNCH_CHECK("norm_finalize");
   return CC_OK;
 }

@@ -362,7 +362,7 @@ def test_split_kv_attention_few_rows(m, S):
     assert lib.cc_attention_splits(6586, Hq, Hkv, 32800) == 1   # full grids: never split
 
 
-@pytest.mark.parametrize("m,n,spread", [(43, 32800, "tail32"), (300, 9000, "sorted"), (557, 32800, "sorted")])
+@pytest.mark.parametrize("m,n,spread", [(43, 32800, "tail32"), (300, 9000, "sorted"), (557, 32800, "sorted"), (1000, 20000, "sorted")])
 def test_split_kv_attention_small_grids(m, n, spread):
     """Low-ratio / default-rule launches (a few hundred rows over a long key
     bank) take the library's split count; the work-aware parts (long ranges
