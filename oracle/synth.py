@@ -134,5 +134,10 @@ P2_PRIMARY = OracleConfig(n_layers=2, n_heads=28, n_kv_heads=4, d_model=3584, d_
                           activation="silu", mlp_gated=True, attn_bias=True)
 P2 = Workload("p2", P2_PRIMARY, QWEN05B, prefix_len=32, n_chunks=16, chunk_len=512, query_len=32,
               window_threshold=1)
+# the same request under the paper's default 8/5 window rule: a few hundred
+# recomputed rows, the launches that take the small-grid split-KV attention
+# and the split-K GEMMs
+P2D = Workload("p2d", P2_PRIMARY, QWEN05B, prefix_len=32, n_chunks=16, chunk_len=512, query_len=32,
+               window_threshold=5)
 SCALE_RATIOS = (0.05, 0.2, 0.4)
 SCALE_THRESHOLDS = (5, 1)   # the paper's default 8/5 rule and the exact-budget rule (H2)

@@ -3,7 +3,7 @@ missing" #1): the benchmarked scoring model and a depth-truncated 7B primary.
 
 Run in the build container only (the reference is not on the GPU box):
 
-    python tests/golden/make_golden_scale.py            # c2, c3, p2
+    python tests/golden/make_golden_scale.py            # c2, c3, p2, p2d
     python tests/golden/make_golden_scale.py c3         # one of them
 
 * ``c2_scoring.npz`` / ``c3_scoring.npz`` — the 24-layer Qwen2.5-0.5B-shape
@@ -43,7 +43,7 @@ sys.path.insert(0, REF_SRC)
 import cacheclip as ref  # noqa: E402  (the reference, read-only)
 
 from oracle import cacheclip_oracle as orc  # noqa: E402
-from oracle.synth import C2, C3, P2, SCALE_RATIOS, SCALE_THRESHOLDS  # noqa: E402
+from oracle.synth import C2, C3, P2, P2D, SCALE_RATIOS, SCALE_THRESHOLDS  # noqa: E402
 
 sys.path.insert(0, HERE)
 from make_golden import char_vocab, ref_config  # noqa: E402
@@ -91,13 +91,17 @@ def scoring(w, aux=None):
     return out, aux, aux_chunks
 
 
-def primary(w, aux, aux_chunks):
+def primary(w, aux, aux_chunks, full_prefill: bool = True, prim_chunks=None):
     t0 = time.perf_counter()
-    p_params = _bf16_2d(orc.seeded_params(w.primary, w.primary_seed, w.bias_std, fast=True))
-    prim = ref.Model(ref_config(w.primary, "chars"), orc.mha_expand(w.primary, p_params))
-    del p_params
-    prefix, chunk_ids, query = w.token_ids(0)
-    chunks = [ref.prefill_chunk(prim, prefix, c) for c in chunk_ids]
+    if prim_chunks is None:
+        p_params = _bf16_2d(orc.seeded_params(w.primary, w.primary_seed, w.bias_std, fast=True))
+        prim = ref.Model(ref_config(w.primary, "chars"), orc.mha_expand(w.primary, p_params))
+        del p_params
+        prefix, chunk_ids, query = w.token_ids(0)
+        chunks = [ref.prefill_chunk(prim, prefix, c) for c in chunk_ids]
+    else:
+        prim, chunks = prim_chunks
+        prefix, chunk_ids, query = w.token_ids(0)
     t1 = time.perf_counter()
     tok = ref.GreedyTokenizer(char_vocab(max(w.primary.vocab_size, w.aux.vocab_size)), "chars")
     cfg = ref.SelectionConfig(recomp_ratio=w.ratio, window_len=w.window_len, window_threshold=w.window_threshold)
@@ -116,21 +120,28 @@ def primary(w, aux, aux_chunks):
                q_k=np.stack([k[qrows][:, head_sel] for k in clip.cache.keys]),
                q_v=np.stack([v[qrows][:, head_sel] for v in clip.cache.values]))
     del clip
-    full = ref.full_attention_prefill(prim, ref.reuse_context_ids(chunks, query))
+    if full_prefill:
+        full = ref.full_attention_prefill(prim, ref.reuse_context_ids(chunks, query))
+        out["full_logits"] = full.logits
     t3 = time.perf_counter()
-    out["full_logits"] = full.logits
-    print(f"p2: chunk precompute {t1 - t0:.1f} s, cacheclip_prefill {t2 - t1:.1f} s, full prefill {t3 - t2:.1f} s; "
-          f"{len(sel)} rows, top1 clip={int(np.argmax(out['clip_logits']))} full={int(np.argmax(full.logits))}")
-    return out
+    print(f"{w.name}: chunk precompute {t1 - t0:.1f} s, cacheclip_prefill {t2 - t1:.1f} s, full prefill "
+          f"{t3 - t2:.1f} s; {len(sel)} rows, top1 clip={int(np.argmax(out['clip_logits']))}")
+    return out, (prim, chunks)
 
 
 def main(names) -> None:
     aux = aux_c2 = None
-    if "c2" in names or "p2" in names:
+    if "c2" in names or "p2" in names or "p2d" in names:
         out, aux, aux_c2 = scoring(C2)
         np.savez_compressed(os.path.join(HERE, "c2_scoring.npz"), **out)
+    pc = None
     if "p2" in names:
-        np.savez_compressed(os.path.join(HERE, "p2_primary.npz"), **primary(P2, aux, aux_c2))
+        out, pc = primary(P2, aux, aux_c2)
+        np.savez_compressed(os.path.join(HERE, "p2_primary.npz"), **out)
+    if "p2d" in names:  # same model and chunks, default 8/5 rule (no full prefill: p2 holds it)
+        out, pc = primary(P2D, aux, aux_c2, full_prefill=False, prim_chunks=pc)
+        np.savez_compressed(os.path.join(HERE, "p2d_primary.npz"), **out)
+    del pc
     del aux_c2
     if "c3" in names:
         out, _, _ = scoring(C3, aux)
@@ -138,4 +149,4 @@ def main(names) -> None:
 
 
 if __name__ == "__main__":
-    main(sys.argv[1:] or ["c2", "p2", "c3"])
+    main(sys.argv[1:] or ["c2", "p2", "p2d", "c3"])
