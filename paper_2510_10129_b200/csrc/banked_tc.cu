@@ -34,19 +34,25 @@
 namespace cc {
 
 constexpr int kBtRows = 128;   // packed rows per CTA = TMEM lanes
-constexpr int kBtKeys = 32;    // keys per tile
 constexpr int kBtThreads = 256;  // 4 lane quarters x 2 column halves
 
 template <int HD>
 struct BtCfg {
+  // keys per tile. 64-key tiles for head_dim 64 (half the serial tile steps)
+  // were measured slower (C3 step 2.7 -> 3.4 ms): 128 KB of shared memory and
+  // 201 registers leave one CTA per SM where 32-key tiles fit two, and the
+  // second CTA hides more of the per-tile barrier chain than halving it saves.
+  static constexpr int KEYS = 32;
+  static constexpr int HC = KEYS / 2;               // columns of a key tile per thread (two halves)
   static constexpr int Q_BYTES = kBtRows * HD * 4;  // one of Q_hi / Q_lo
-  static constexpr int K_BYTES = kBtKeys * HD * 4;  // one of K_hi / K_lo / V_hi / V_lo
+  static constexpr int K_BYTES = KEYS * HD * 4;     // one of K_hi / K_lo / V_hi / V_lo
   static constexpr int SMEM = 2 * Q_BYTES + 4 * K_BYTES + 4 * kBtRows * 4 + 1024 + 64;
-  static constexpr int T_S = 0, T_PH = kBtKeys, T_PL = 2 * kBtKeys, T_O = 3 * kBtKeys;
-  static constexpr int TMEM_COLS = (3 * kBtKeys + HD) <= 256 ? 256 : 512;
-  static constexpr int F4 = kBtKeys * HD / 4 / kBtThreads;  // float4 per thread per K (or V) tile
-  static constexpr uint32_t IDESC_S = umma_idesc(128, kBtKeys, true);
+  static constexpr int T_S = 0, T_PH = KEYS, T_PL = 2 * KEYS, T_O = 3 * KEYS;
+  static constexpr int TMEM_COLS = (3 * KEYS + HD) <= 256 ? 256 : 512;
+  static constexpr int F4 = KEYS * HD / 4 / kBtThreads;  // float4 per thread per K (or V) tile
+  static constexpr uint32_t IDESC_S = umma_idesc(128, KEYS, true);
   static constexpr uint32_t IDESC_PV = umma_idesc(128, HD, true);  // B = V^T, K-major
+  static_assert(SMEM <= 232448, "banked tile over the shared-memory limit");
 };
 
 // byte offset of fp32 element (row, col) in a [R rows] x [cols] 128B-swizzled
@@ -144,7 +150,8 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
     const float* __restrict__ v_new, int n_q_heads, int n_kv_heads, float factor, int qpb, void* __restrict__ out,
     int out_mode, float* __restrict__ weights_out, int64_t w_col0, int64_t w_ld) {
   using Cfg = BtCfg<HD>;
-  constexpr int HC = kBtKeys / 2;  // columns of a key tile per thread (two column halves)
+  constexpr int HC = Cfg::HC;
+  constexpr int kBtKeys = Cfg::KEYS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sQh = smem;
@@ -230,7 +237,7 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
       *reinterpret_cast<float4*>(sKl + off) = lo;
       if (with_v) {
         split4(vreg[e], hi, lo);
-        // V^T [HD dims][32 keys], K-major (one 128-byte block of keys per dim)
+        // V^T [HD dims][keys], K-major (128-byte blocks of 32 keys per dim)
         const float hv[4] = {hi.x, hi.y, hi.z, hi.w}, lv[4] = {lo.x, lo.y, lo.z, lo.w};
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -285,7 +292,8 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
       s_phase ^= 1;
       tc_fence_after();
       float s[HC];
-      tmem_ld16(t_s, s);
+#pragma unroll
+      for (int c = 0; c < HC; c += 16) tmem_ld16(t_s + c, s + c);
       body(j, j * kBtKeys + half * HC, s);
     }
   };
@@ -387,8 +395,11 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
         split_tf32_finite(lo, s[t], l2);
       }
       l_half = l_half * alpha + ls;
-      tmem_st16_f(tl + Cfg::T_PH + half * HC, ph);
-      tmem_st16_f(tl + Cfg::T_PL + half * HC, s);
+#pragma unroll
+      for (int c = 0; c < HC; c += 16) {
+        tmem_st16_f(tl + Cfg::T_PH + half * HC + c, ph + c);
+        tmem_st16_f(tl + Cfg::T_PL + half * HC + c, s + c);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncthreads();
@@ -396,7 +407,9 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
       if (warp == 0) {
 #pragma unroll
         for (int k = 0; k < kBtKeys / 8; ++k) {
-          const uint64_t bh = dv_h + 2 * k, bl = dv_l + 2 * k;
+          // V^T [HD dims][keys]: 32-key (128-byte) K-blocks HD rows apart
+          const uint32_t vo = ((k >> 2) * (HD * 128) + (k & 3) * 32) >> 4;
+          const uint64_t bh = dv_h + vo, bl = dv_l + vo;
           tc_mma_ts_tf32_warp(tmem_u + Cfg::T_O, tmem_u + Cfg::T_PH + k * 8, bh, Cfg::IDESC_PV,
                               (j > 0 || k > 0) ? 1u : 0u);
           tc_mma_ts_tf32_warp(tmem_u + Cfg::T_O, tmem_u + Cfg::T_PH + k * 8, bl, Cfg::IDESC_PV, 1u);
