@@ -762,23 +762,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1) {  // warp-wide issue from uniform descriptors (tc_mma_warp)
     int stage = 0;
     uint32_t phase = 0;
+    const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
+    const uint64_t adesc0 = umma_desc_sw128(smem_u32(smem_a));
+    const uint64_t bdesc0 = umma_desc_sw128(smem_u32(smem_b));
     for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(&full[stage], phase);
       tc_fence_after();
-      if (lane == 0) {
-        const uint32_t a0 = smem_u32(smem_a + stage * Cfg::A_BYTES);
-        const uint32_t b0 = smem_u32(smem_b + stage * Cfg::B_BYTES);
+      const uint64_t ad = adesc0 + (uint64_t)((stage * Cfg::A_BYTES) >> 4);
+      const uint64_t bd = bdesc0 + (uint64_t)((stage * Cfg::B_BYTES) >> 4);
 #pragma unroll
-        for (int k = 0; k < Cfg::KSTEPS; ++k)
-          tc_mma<false>(tmem_base, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), Cfg::IDESC,
-                        (kb > kb0 || k > 0) ? 1u : 0u);
-        tc_commit(&empty[stage]);
-        if (kb == kb1 - 1) tc_commit(tfull);
-      }
-      __syncwarp();
+      for (int k = 0; k < Cfg::KSTEPS; ++k)
+        tc_mma_warp<false>(tmem_u, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (kb > kb0 || k > 0) ? 1u : 0u);
+      tc_commit_warp(&empty[stage]);
+      if (kb == kb1 - 1) tc_commit_warp(tfull);
       if (++stage == Cfg::STAGES) {
         stage = 0;
         phase ^= 1;
@@ -1383,5 +1382,16 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
         return launch_pair<256, false>(a, ep, kop, st);
     }
   }
-  return wide ? launch<256, false>(a, ep, kop, st) : launch<128, false>(a, ep, kop, st);
+  switch (a->epilogue) {  // specialised on the recompute layer's epilogues (few-row GEMMs land here)
+    case CC_EPI_QKV_ROPE:
+      return wide ? launch<256, false, CC_EPI_QKV_ROPE>(a, ep, kop, st)
+                  : launch<128, false, CC_EPI_QKV_ROPE>(a, ep, kop, st);
+    case CC_EPI_RESIDUAL:
+      return wide ? launch<256, false, CC_EPI_RESIDUAL>(a, ep, kop, st)
+                  : launch<128, false, CC_EPI_RESIDUAL>(a, ep, kop, st);
+    case CC_EPI_GLU:
+      return launch<256, false, CC_EPI_GLU>(a, ep, kop, st);
+    default:
+      return wide ? launch<256, false>(a, ep, kop, st) : launch<128, false>(a, ep, kop, st);
+  }
 }
