@@ -38,7 +38,7 @@ namespace cc {
 __device__ long long g_fa_trace[16 * 128];
 #define FA_T(slot, j)                                                                        \
   do {                                                                                       \
-    if (blockIdx.x == 0 && blockIdx.y == 0 && lane == 0 && (j) < 128)                         \
+    if (blockIdx.x == 0 && lane == 0 && (j) < 128)                                              \
       g_fa_trace[(slot) * 128 + (j)] = clock64();                                            \
   } while (0)
 #else
@@ -243,8 +243,11 @@ __global__ void __launch_bounds__(kFaThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = n_q_heads / n_kv_heads;
-  const int kvh = blockIdx.y;
-  const int cta = n_ctas - 1 - (int)blockIdx.x;  // heavy (late-position) tiles first
+  // heavy (late-position) tiles first ACROSS all KV heads: block b takes tile
+  // n_ctas-1 - b / Hkv of head b % Hkv, so the launch order is the
+  // longest-first schedule of the whole grid, not per head
+  const int kvh = (int)blockIdx.x % n_kv_heads;
+  const int cta = n_ctas - 1 - (int)blockIdx.x / n_kv_heads;
   const int64_t packed_total = m * G;
   const int64_t p0 = (int64_t)cta * 2 * kFaTileRows;
 
@@ -600,7 +603,7 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const
   set_smem_once<fa_sparse_row_kernel<D>>(FaCfg<D>::SMEM);
   const int G = hq / hkv;
   const int n_ctas = (int)((m * G + 2 * kFaTileRows - 1) / (2 * kFaTileRows));
-  dim3 grid(n_ctas, hkv, n_splits);
+  dim3 grid(n_ctas * hkv, 1, n_splits);
   ProfScope ps(st, OP_ATTENTION, flops);
   fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
       tk, tv, (const __nv_bfloat16*)q, ldq, positions, kstart, m, n_keys, hq, hkv, factor, row_factor,
