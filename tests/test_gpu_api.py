@@ -182,3 +182,63 @@ def test_fused_rmsnorm_matches_standalone(tmp_path):
     print(f"fused vs standalone RMSNorm: max|dlogits| {d:.3e} (std {std:.3f})")
     assert d < 2e-2 * std
     assert not np.array_equal(fused, plain)  # the fused path really ran
+
+
+_SMALL_GRID_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2510_10129_b200 as cc
+from oracle import cacheclip_oracle as orc
+# d_model 1024 (16 K-blocks: the few-row GEMMs split along K), 8K-key bank
+# (the few-row attention launches split along keys), fused RMSNorm on
+oc = orc.OracleConfig(n_layers=2, n_heads=16, n_kv_heads=2, d_model=1024, d_head=128, d_ff=2048,
+                      vocab_size=512, rope_base=1e6, norm_eps=1e-6, activation="silu", mlp_gated=True,
+                      attn_bias=True)
+ac = orc.OracleConfig(n_layers=2, n_heads=4, n_kv_heads=2, d_model=256, d_head=64, d_ff=512, vocab_size=512,
+                      rope_base=1e6, norm_eps=1e-6, activation="silu", mlp_gated=True, attn_bias=True)
+def cfg(o, dt):
+    return cc.ModelConfig(n_layers=o.n_layers, n_heads=o.n_heads, d_model=o.d_model, d_head=o.d_head, d_ff=o.d_ff,
+                          vocab_size=o.vocab_size, rope_base=o.rope_base, norm_eps=o.norm_eps, activation=o.activation,
+                          mlp_gated=o.mlp_gated, attn_bias=o.attn_bias, n_kv_heads=o.kv_heads, dtype=dt,
+                          tokenizer_id="chars")
+primary = cc.from_params(cfg(oc, "bf16"), orc.seeded_params(oc, 0, 0.05))
+aux = cc.from_params(cfg(ac, "fp32"), orc.seeded_params(ac, 1, 0.05))
+rng = np.random.default_rng(5)
+prefix = rng.integers(0, 512, 32).tolist()
+chunk_ids = [rng.integers(0, 512, 512).tolist() for _ in range(16)]
+query = rng.integers(0, 512, 32).tolist()
+chunks = cc.prefill_chunks(primary, prefix, chunk_ids)
+aux_chunks = cc.prefill_chunks(aux, prefix, chunk_ids)
+out = cc.cacheclip_prefill(primary, aux, chunks, aux_chunks, query, cc.SelectionConfig(0.2))  # default 8/5 rule
+tok = out.first_token
+dec, _ = cc.decode_step(primary, out.cache, tok)
+np.savez(sys.argv[2], logits=out.logits, decode=np.asarray(dec), rows=len(out.plan.indices))
+"""
+
+
+def test_small_grid_paths_match_whole_grid_paths(tmp_path):
+    """Few-row launches (the default 8/5 rule's recompute, a decode step) take
+    the split-K bf16 GEMMs and the split-KV attention; against the same
+    request with both disabled (CC_GEMM_SPLITK=0, CC_ATTN_SPLIT=0: the
+    whole-grid kernels) the logits agree within bf16 rounding, and the split
+    run really differs (it ran)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for flag in ("1", "0"):
+        f = tmp_path / f"out_{flag}.npz"
+        env = dict(os.environ, CC_GEMM_SPLITK=flag, CC_ATTN_SPLIT=flag)
+        r = subprocess.run([sys.executable, "-c", _SMALL_GRID_SCRIPT, root, str(f)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[flag] = dict(np.load(f))
+    on, off = outs["1"], outs["0"]
+    assert int(on["rows"]) == int(off["rows"]) and int(on["rows"]) < 400
+    for key in ("logits", "decode"):
+        std = off[key].std()
+        d = np.abs(on[key] - off[key]).max()
+        print(f"{key}: split vs whole-grid max|d| {d:.3e} (std {std:.3f}), rows {int(on['rows'])}")
+        assert d < 2e-2 * std
+    assert not np.array_equal(on["logits"], off["logits"])
