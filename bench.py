@@ -282,6 +282,13 @@ def run_reference(args, rank: int, world: int):
     work = WORKLOADS[args.config]
     if rank != 0:
         return
+    # all the host threads: torchrun exports OMP_NUM_THREADS=1 to every rank,
+    # which would leave the reference's BLAS on one core
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=os.cpu_count(), user_api="blas")
+    except Exception:  # pragma: no cover
+        pass
     est = ref_estimator(work, args.ratio, args.window_threshold)
     if est is None:   # port fallback: recompute-only sample
         for _ in range(args.warmup):
@@ -861,7 +868,8 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        if args.impl == "ours":  # the reference arm is CPU-only
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
     if args.impl == "reference":
         run_reference(args, rank, world)
