@@ -199,6 +199,14 @@ typedef struct {
   float* ssq_out;
   const float* inv_rms;
   int64_t ld_ssq;
+  /* The consumer may instead take the producer's partial sums directly:
+   * ssq_in[p * ld_ssq_in + m] for p < n_ssq (d = 32 * n_ssq); its epilogue
+   * then forms 1/rms per row itself, with cc_norm_finalize's arithmetic and
+   * summation order (bitwise the same scaling, one launch fewer). */
+  const float* ssq_in;
+  int32_t n_ssq;
+  int64_t ld_ssq_in;
+  float norm_eps;
 } cc_gemm_args;
 
 int cc_gemm(const cc_gemm_args* args, void* stream);

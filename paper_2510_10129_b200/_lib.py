@@ -57,6 +57,7 @@ class GemmArgs(ctypes.Structure):
         ("ssq_out", vp),
         ("inv_rms", vp),
         ("ld_ssq", i64),
+        ("ssq_in", vp), ("n_ssq", i32), ("ld_ssq_in", i64), ("norm_eps", ctypes.c_float),
     ]
 
 

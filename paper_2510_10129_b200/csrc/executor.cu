@@ -131,11 +131,15 @@ static void norm_produce(cc_gemm_args& a, const NormFuse& nf, int64_t r0, const 
   a.ld_ssq = nf.ld;
 }
 
-// reduce the partials of rows [r0, r0 + n) to 1/rms, then point the
-// consumer GEMM at them
+// point the consumer GEMM at the partials of rows [r0, r0 + n): its epilogue
+// forms 1/rms per row (cc_norm_finalize's arithmetic, no separate launch)
 static int norm_consume(cc_gemm_args& a, const NormFuse& nf, int64_t r0, int64_t n, void* stream) {
-  CC_TRY(cc_norm_finalize(nf.ssq + r0, n, nf.d, nf.ld, nf.eps, nf.inv + r0, stream));
-  a.inv_rms = nf.inv + r0;
+  (void)n;
+  (void)stream;
+  a.ssq_in = nf.ssq + r0;
+  a.n_ssq = nf.parts;
+  a.ld_ssq_in = nf.ld;
+  a.norm_eps = nf.eps;
   return CC_OK;
 }
 

@@ -111,6 +111,12 @@ struct EpiParams {
   float* ssq_out;
   const float* ssq_in;  // inv_rms [M]
   int64_t ld_ssq;
+  // or the producer's partial sums (1/rms formed in the epilogue)
+  const float* ssq_parts;
+  int n_parts;
+  int64_t ld_parts;
+  float eps;
+  float inv_d;
 };
 
 // The epilogue mode: a compile-time constant when the kernel is specialised
@@ -118,9 +124,32 @@ struct EpiParams {
 // under the full shared-memory carve-out), else the runtime field.
 __device__ __forceinline__ int epi_of(const EpiParams& ep, int kEpi) { return kEpi >= 0 ? kEpi : ep.epilogue; }
 
-// 1 / rms of GEMM row m (cc_norm_finalize reduced the producer's partial sums)
+// 1 / rms of GEMM row m: given (cc_norm_finalize reduced the producer's
+// partial sums), or formed here from the partials with the same arithmetic
+// and summation order (32 loads in flight)
+__device__ __forceinline__ bool row_scaled(const EpiParams& ep) { return ep.ssq_in || ep.ssq_parts; }
 __device__ __forceinline__ float row_inv_rms(const EpiParams& ep, int64_t m) {
-  return m < ep.M ? __ldg(ep.ssq_in + m) : 0.f;
+  if (m >= ep.M) return 0.f;
+  if (ep.ssq_in) return __ldg(ep.ssq_in + m);
+  const float* p = ep.ssq_parts + m;
+  float s = 0.f;
+  int i = 0;
+  for (; i + 32 <= ep.n_parts; i += 32) {
+    float t[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) t[j] = __ldg(p + (int64_t)(i + j) * ep.ld_parts);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) s = __fadd_rn(s, t[j]);
+  }
+  for (; i + 8 <= ep.n_parts; i += 8) {
+    float t[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t[j] = __ldg(p + (int64_t)(i + j) * ep.ld_parts);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) s = __fadd_rn(s, t[j]);
+  }
+  for (; i < ep.n_parts; ++i) s = __fadd_rn(s, __ldg(p + (int64_t)i * ep.ld_parts));
+  return __frcp_rn(__fsqrt_rn(__fadd_rn(__fmul_rn(s, ep.inv_d), ep.eps)));
 }
 
 __device__ __forceinline__ float act_apply(int act, float x) {
@@ -254,12 +283,13 @@ __device__ __forceinline__ void add_parts16(const SplitParts& sp, int col, float
   }
 }
 
+// rs: this lane's row 1/rms (row_inv_rms, formed once per tile by the caller)
 template <int BN, bool kTF32, int kEpi = -1>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, uint32_t tbase, int c0, int64_t row0, int nb,
-                                               float* stg, int lane, const SplitParts& sp = SplitParts{nullptr, 0, 0}) {
+                                               float* stg, int lane, float rs,
+                                               const SplitParts& sp = SplitParts{nullptr, 0, 0}) {
   float v[32];
-  const bool scaled = ep.ssq_in != nullptr;
-  const float rs = scaled ? row_inv_rms(ep, row0 + lane) : 1.f;
+  const bool scaled = row_scaled(ep);
   if (epi_of(ep, kEpi) == CC_EPI_GLU) {
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {  // 16 columns at a time (register budget)
@@ -672,11 +702,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (ew == 0) GT(4, 3 * tile_i + 2);
         ++tile_i;
       } else {
+        // 1/rms of this lane's row, formed while the tile's MMAs run
+        const float rs = row_scaled(ep) ? row_inv_rms(ep, row0 + lane) : 1.f;
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         const uint32_t tbase = tmem_base + acc * Cfg::ACC_STRIDE + lane_off;
         for (int c0 = c_begin; c0 < c_end; c0 += 32)
-          epilogue_chunk<BN, kTF32, kEpi>(ep, tbase, c0, row0, nb, stg, lane);
+          epilogue_chunk<BN, kTF32, kEpi>(ep, tbase, c0, row0, nb, stg, lane, rs);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -828,7 +860,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const int cols = glu ? BN / 2 : BN;
         const int c_begin = chalf * (cols / 2), c_end = c_begin + cols / 2;
         const SplitParts sp{tile_parts, S - 1, lrow};
-        for (int c0 = c_begin; c0 < c_end; c0 += 32) epilogue_chunk<BN, false>(ep, tbase, c0, row0, nb, stg, lane, sp);
+        const float rs = row_scaled(ep) ? row_inv_rms(ep, row0 + lane) : 1.f;
+        for (int c0 = c_begin; c0 < c_end; c0 += 32)
+          epilogue_chunk<BN, false>(ep, tbase, c0, row0, nb, stg, lane, rs, sp);
       }
       asm volatile("bar.sync 2, %0;" ::"n"(32 * kEpiWarps) : "memory");
       if (ew == 0 && lane == 0) counters[tile] = 0;  // re-armed for the next launch on this stream
@@ -1081,11 +1115,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int c_begin = chalf * (cols / 2), c_end = c_begin + cols / 2;
     for (int t = cluster_id; t < tiles; t += n_clusters) {
       const int mb = t % num_m2, nb = t / num_m2;
+      const int64_t row0 = (int64_t)mb * 256 + (int64_t)rank * 128 + quarter * 32;
+      // 1/rms of this lane's row, formed while the tile's MMAs run
+      const float rs = row_scaled(ep) ? row_inv_rms(ep, row0 + lane) : 1.f;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + acc * Cfg::ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
-      const int64_t row0 = (int64_t)mb * 256 + (int64_t)rank * 128 + quarter * 32;
-      for (int c0 = c_begin; c0 < c_end; c0 += 32) epilogue_chunk<BN, kTF32, kEpi>(ep, tbase, c0, row0, nb, stg, lane);
+      for (int c0 = c_begin; c0 < c_end; c0 += 32)
+        epilogue_chunk<BN, kTF32, kEpi>(ep, tbase, c0, row0, nb, stg, lane, rs);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(map_to_rank(&tempty[acc], 0));
@@ -1315,7 +1352,14 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
   ep.ssq_out = a->ssq_out;
   ep.ssq_in = a->inv_rms;
   ep.ld_ssq = a->ld_ssq;
-  if (a->ssq_out || a->inv_rms) CC_CHECK_ARG(!tf32, CC_ERR_UNSUPPORTED, "fused RMSNorm runs on bf16 GEMMs");
+  ep.ssq_parts = a->inv_rms ? nullptr : a->ssq_in;
+  ep.n_parts = a->n_ssq;
+  ep.ld_parts = a->ld_ssq_in;
+  ep.eps = a->norm_eps;
+  ep.inv_d = a->n_ssq > 0 ? 1.0f / (float)(32 * a->n_ssq) : 0.f;
+  if (a->ssq_out || a->inv_rms || a->ssq_in) CC_CHECK_ARG(!tf32, CC_ERR_UNSUPPORTED, "fused RMSNorm runs on bf16 GEMMs");
+  if (a->ssq_in && !a->inv_rms)
+    CC_CHECK_ARG(a->n_ssq > 0 && a->ld_ssq_in >= a->M, CC_ERR_DIMENSION, "ssq_in needs n_ssq > 0 and ld_ssq_in >= M");
   if (a->ssq_out)
     CC_CHECK_ARG(a->ld_ssq >= a->M, CC_ERR_DIMENSION, "ld_ssq %lld < M %lld", (long long)a->ld_ssq, (long long)a->M);
   if (a->ssq_out) {
@@ -1323,7 +1367,7 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
                      a->ldxn % 4 == 0 && ((uintptr_t)a->xn_out % 16) == 0 && ((uintptr_t)a->norm_gain % 16) == 0,
                  CC_ERR_UNSUPPORTED, "RMSNorm partials come from a RESIDUAL epilogue with N %% 32 == 0, xn and gain");
   }
-  if (a->inv_rms)
+  if (a->inv_rms || a->ssq_in)
     CC_CHECK_ARG(a->epilogue != CC_EPI_RESIDUAL, CC_ERR_UNSUPPORTED,
                  "row RMS scaling applies to QKV / GLU / STORE / ACT epilogues");
   bool wide;
