@@ -295,3 +295,39 @@ def test_chunk_spans_identity_needs_equal_vocab_contents():
     assert n is None
     p, a = spans
     assert [s.token_id for s in p] == [2] and [s.token_id for s in a] == [0, 1]
+
+
+def test_gemm_argument_checks_before_any_device_work():
+    """cc_gemm validates its arguments (status codes, no CUDA call) before it
+    touches the device: the fused-RMSNorm partial-sum input is bf16-only,
+    needs its part count and row pitch, and is refused on a RESIDUAL
+    epilogue; shapes and alignment as before. Runs without a GPU."""
+    import ctypes
+
+    from paper_2510_10129_b200 import _lib as L
+    lib = L.load()
+
+    def args(**kw):
+        a = L.GemmArgs()
+        a.kind, a.epilogue = L.CC_GEMM_BF16, L.CC_EPI_STORE
+        a.M, a.N, a.K = 4, 128, 64
+        a.A = a.B = a.C = ctypes.c_void_p(1 << 20)   # aligned, never dereferenced
+        a.lda = a.ldb = 64
+        a.ldc = 128
+        a.c_mode = L.CC_F32
+        for k, v in kw.items():
+            setattr(a, k, v)
+        return a
+
+    def rc(a):
+        return lib.cc_gemm(ctypes.byref(a), None)
+
+    ssq = ctypes.c_void_p(1 << 21)
+    assert rc(args(M=-1)) == L.CC_ERR_DIMENSION
+    assert rc(args(N=100)) == L.CC_ERR_UNSUPPORTED                      # N % 16
+    assert rc(args(kind=L.CC_GEMM_TF32X3, lda=192, ldb=192, ssq_in=ssq, n_ssq=2, ld_ssq_in=4)) == \
+        L.CC_ERR_UNSUPPORTED                                              # fused norm is bf16-only
+    assert rc(args(ssq_in=ssq, n_ssq=0, ld_ssq_in=4)) == L.CC_ERR_DIMENSION
+    assert rc(args(ssq_in=ssq, n_ssq=2, ld_ssq_in=2)) == L.CC_ERR_DIMENSION   # ld < M
+    assert rc(args(epilogue=L.CC_EPI_RESIDUAL, ssq_in=ssq, n_ssq=2, ld_ssq_in=4)) == L.CC_ERR_UNSUPPORTED
+    assert b"ssq" in lib.cc_last_error() or b"RMS" in lib.cc_last_error()
