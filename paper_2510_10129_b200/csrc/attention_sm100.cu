@@ -22,8 +22,10 @@
 //               writes P (bf16 pairs) back over its S row with tcgen05.st.
 //               Lazy rescale: the running max moves (and O is rescaled in TMEM)
 //               only when a tile raises it by > 2^8. One FFMA per element
-//               folds scale and max; a quarter of the exp2s run as a
-//               polynomial on the FMA pipe to offload MUFU.
+//               folds scale and max; 3 of 16 exp2 pairs run as a degree-3
+//               polynomial on the FMA pipe to offload MUFU. P goes back in
+//               four 32-key parts, each released to the PV MMA as soon as it
+//               is in TMEM.
 #include "cc_common.cuh"
 
 #include <algorithm>
@@ -176,25 +178,15 @@ __device__ __forceinline__ float ex2_mufu(float x) {
   return y;
 }
 
-// 2^x on the FMA pipe: round-to-nearest split x = n + f, |f| <= 1/2, degree-4
-// polynomial for 2^f (|rel err| < 5e-5, far below bf16 P rounding), 2^n via
-// the exponent field.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.0f);
-  const float magic = 12582912.0f;  // 1.5 * 2^23
-  const float t = x + magic;
-  const float f = x - (t - magic);
-  float p = fmaf(f, 9.6181291e-3f, 5.5504109e-2f);
-  p = fmaf(p, f, 2.4022651e-1f);
-  p = fmaf(p, f, 6.9314718e-1f);
-  p = fmaf(p, f, 1.0f);
-  const int n = __float_as_int(t) - __float_as_int(magic);
-  return __int_as_float(__float_as_int(p) + (n << 23));
-}
+#ifndef CC_FA_POLY_DEG
+#define CC_FA_POLY_DEG 3
+#endif
 
-// The same on a pair with the sm_100 paired-FP32 instructions (FADD2/FFMA2):
-// half the issue slots. t = x + 1.5*2^23 holds n in its low mantissa bits and
-// the magic's own bits vanish under << 23, so 2^n scaling is one IMAD.
+// 2^x for a pair on the FMA pipe, with the sm_100 paired-FP32 instructions
+// (FADD2/FFMA2, half the issue slots): round-to-nearest split x = n + f,
+// |f| <= 1/2, a polynomial for 2^f, 2^n via the exponent field.
+// t = x + 1.5*2^23 holds n in its low mantissa bits and the magic's own bits
+// vanish under << 23, so 2^n scaling is one IMAD.
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   x.x = fmaxf(x.x, -126.0f);
   x.y = fmaxf(x.y, -126.0f);
@@ -202,9 +194,16 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
   const float2 t = __fadd2_rn(x, magic);
   const float2 n = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
   const float2 f = __ffma2_rn(n, make_float2(-1.0f, -1.0f), x);
+#if CC_FA_POLY_DEG == 3
+  // degree-3 minimax for 2^f on [-1/2, 1/2]: |rel err| < 1.1e-4, still 20x
+  // below the bf16 rounding of P
+  float2 p = __ffma2_rn(f, make_float2(5.5008930e-2f, 5.5008930e-2f), make_float2(2.4221098e-1f, 2.4221098e-1f));
+  p = __ffma2_rn(p, f, make_float2(6.9328293e-1f, 6.9328293e-1f));
+#else
   float2 p = __ffma2_rn(f, make_float2(9.6181291e-3f, 9.6181291e-3f), make_float2(5.5504109e-2f, 5.5504109e-2f));
   p = __ffma2_rn(p, f, make_float2(2.4022651e-1f, 2.4022651e-1f));
   p = __ffma2_rn(p, f, make_float2(6.9314718e-1f, 6.9314718e-1f));
+#endif
   p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
   return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
@@ -212,9 +211,18 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 
 // pairs (of 16 per 32-key chunk) whose exponentials run on the FMA pipe
 #ifndef CC_FA_POLY
-#define CC_FA_POLY 4
+#define CC_FA_POLY 3
 #endif
 constexpr int kFaPolyPairs = CC_FA_POLY;
+
+// P is handed to the PV MMA in this many key parts: the MMA warp starts
+// O += P V on the first part while the softmax warps still exponentiate the
+// rest, so part of the softmax leaves the S -> softmax -> PV -> S chain
+#ifndef CC_FA_PV_PARTS
+#define CC_FA_PV_PARTS 4
+#endif
+constexpr int kFaPvParts = CC_FA_PV_PARTS;
+static_assert(kFaPvParts == 1 || kFaPvParts == 2 || kFaPvParts == 4, "P parts: 1, 2 or 4 (32-key chunks per part)");
 
 template <int D>
 __global__ void __launch_bounds__(kFaThreads, 1)
@@ -235,10 +243,10 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   uint64_t* v_full = bars + 2;    // [2]
   uint64_t* kv_empty = bars + 4;  // [2]
   uint64_t* s_full = bars + 6;    // [2 tiles]
-  uint64_t* p_full = bars + 8;    // [2 tiles]
-  uint64_t* pv_done = bars + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 11);
-  int* s_kmax = reinterpret_cast<int*>(bars + 12);
+  uint64_t* p_full = bars + 8;    // [2 tiles][kFaPvParts]
+  uint64_t* pv_done = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  int* s_kmax = reinterpret_cast<int*>(bars + 18);
   int* s_kmin = s_kmax + 1;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -257,8 +265,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
       mbar_init(&v_full[s], 1);
       mbar_init(&kv_empty[s], 1);
       mbar_init(&s_full[s], 1);
-      mbar_init(&p_full[s], 4);
     }
+    for (int b = 0; b < 2 * kFaPvParts; ++b) mbar_init(&p_full[b], 4);
     mbar_init(pv_done, 1);
     *s_kmax = 0;
     *s_kmin = 0x7fffffff;
@@ -391,14 +399,20 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         }
         tc_commit_warp(&s_full[t]);
       };
-      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P read from TMEM (over S_t)
-        mbar_wait(&p_full[t], j & 1);
-        tc_fence_after();
+      auto issue_pv = [&](int t, int j) {  // O_t += P_t(j) V_j, P read from TMEM (over S_t), part by part
         const uint64_t vd = vdesc0 + (uint64_t)(((j & 1) * Cfg::KT_BYTES) >> 4);
+        constexpr int kPer = kFaKeys / 16 / kFaPvParts;  // K=16 MMAs per part
 #pragma unroll
-        for (int k = 0; k < kFaKeys / 16; ++k)
-          tc_mma_ts_warp(tmem_u + Cfg::o_col(t), tmem_u + Cfg::s_col(t) + k * 8, vd + ((k * 16 * 128) >> 4),
-                         Cfg::IDESC_PV, (j > 0 || k > 0) ? 1u : 0u);
+        for (int part = 0; part < kFaPvParts; ++part) {
+          mbar_wait(&p_full[t * kFaPvParts + part], j & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < kPer; ++kk) {
+            const int k = part * kPer + kk;
+            tc_mma_ts_warp(tmem_u + Cfg::o_col(t), tmem_u + Cfg::s_col(t) + k * 8, vd + ((k * 16 * 128) >> 4),
+                           Cfg::IDESC_PV, (j > 0 || k > 0) ? 1u : 0u);
+          }
+        }
       };
       if (n_tiles > 0) {
         mbar_wait(&k_full[0], 0);
@@ -469,9 +483,23 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         m_run = m_tile;
         resc = true;
       }
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+        // O is stable here: PV_t(j-1) completed before S_t(j) (in-order
+        // tcgen05 pipe); rescaled before the first part of P is handed over
+        const float a = resc ? alpha : 1.f;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          float ov[32];
+          tmem_ld32(o_addr + c * 32, ov);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) ov[e] *= a;
+          tmem_st32(o_addr + c * 32, ov);
+        }
+      }
       const float nbase = (m_run == -INFINITY) ? 0.f : -m_run;
       const float2 sc2 = make_float2(scale2, scale2), nb2 = make_float2(nbase, nbase);
       float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      constexpr int kChunksPerPart = kFaKeys / 32 / kFaPvParts;
 #pragma unroll
       for (int c = 0; c < kFaKeys / 32; ++c) {
         uint32_t pk[16];
@@ -489,26 +517,16 @@ __global__ void __launch_bounds__(kFaThreads, 1)
           pk[e] = pack2_bf16(p.x, p.y);
         }
         tmem_st16u(s_addr + c * 16, pk);  // P over the S row: column c*16+e holds keys (2e, 2e+1) of chunk c
+        if ((c + 1) % kChunksPerPart == 0) {  // a part of P is in TMEM: hand it to the PV MMA
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[tq * kFaPvParts + c / kChunksPerPart]);
+        }
       }
       const float2 s01 = __fadd2_rn(acc[0], acc[1]), s23 = __fadd2_rn(acc[2], acc[3]);
       const float lsum = (s01.x + s01.y) + (s23.x + s23.y);
       l_run = l_run * alpha + lsum;
-      if (j > 0 && __any_sync(0xffffffffu, resc)) {
-        // O is stable here: PV_t(j-1) completed before S_t(j) (in-order tcgen05 pipe)
-        const float a = resc ? alpha : 1.f;
-#pragma unroll
-        for (int c = 0; c < D / 32; ++c) {
-          float ov[32];
-          tmem_ld32(o_addr + c * 32, ov);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) ov[e] *= a;
-          tmem_st32(o_addr + c * 32, ov);
-        }
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[tq]);
       if (quarter == 0) FA_T(tq * 2 + 1, j);
     }
     if (n_tiles > 0) {
