@@ -989,10 +989,28 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `b
       : "memory");
 }
 
+// Tile t of the persistent schedule -> (m pair, n tile). group_m = 0: m
+// fastest over all m (a wave of clusters shares the B columns of ~2-3 n tiles
+// and re-reads all of A per wave, right when A stays in L2). group_m = g:
+// m fastest inside bands of g m-pairs, so a wave covers ~g x (clusters / g)
+// tiles and reads both A and B once per band (both operands larger than L2).
+__device__ __forceinline__ void tile_mn(int t, int num_m2, int num_n, int group_m, int& mb, int& nb) {
+  if (group_m <= 0 || group_m >= num_m2) {
+    mb = t % num_m2;
+    nb = t / num_m2;
+    return;
+  }
+  const int per = group_m * num_n;  // tiles per full band (every band but the last is full)
+  const int g = t / per, local = t - g * per;
+  const int m0 = g * group_m, gm = min(group_m, num_m2 - m0);
+  mb = m0 + local % gm;
+  nb = local / gm;
+}
+
 template <int BN, bool kTF32, int kEpi = -1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
-                 int num_m2, int num_n, int num_kb, int k_orig) {
+                 int num_m2, int num_n, int num_kb, int k_orig, int group_m) {
   using Cfg = Gemm2Cfg<BN, kTF32>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -1041,7 +1059,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int t = cluster_id; t < tiles; t += n_clusters) {
-        const int mb = t % num_m2, nb = t / num_m2;
+        int mb, nb;
+        tile_mn(t, num_m2, num_n, group_m, mb, nb);
         const int arow = mb * 256 + (int)rank * 128;
         const int brow = b_row<BN, kEpi>(ep, nb, (int)rank);
         for (int kb = 0; kb < num_kb; ++kb) {
@@ -1114,7 +1133,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int cols = (epi_of(ep, kEpi) == CC_EPI_GLU) ? BN / 2 : BN;
     const int c_begin = chalf * (cols / 2), c_end = c_begin + cols / 2;
     for (int t = cluster_id; t < tiles; t += n_clusters) {
-      const int mb = t % num_m2, nb = t / num_m2;
+      int mb, nb;
+      tile_mn(t, num_m2, num_n, group_m, mb, nb);
       const int64_t row0 = (int64_t)mb * 256 + (int64_t)rank * 128 + quarter * 32;
       // 1/rms of this lane's row, formed while the tile's MMAs run
       const float rs = row_scaled(ep) ? row_inv_rms(ep, row0 + lane) : 1.f;
@@ -1209,9 +1229,23 @@ static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, 
   const int num_kb = (int)(((kTF32 ? a->K : kop) + Cfg::BK - 1) / Cfg::BK);
   const int tiles = num_m2 * num_n;
   const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
+  // Schedule: a wave of ~74 clusters over an a x b block of tiles reads ~(a + b)
+  // operand panels from DRAM. m fastest over all m (b ~ 3) is right only when
+  // A is small enough to stay in L2 and B is not (gate/up: A 47 MB, B 271 MB:
+  // B is read once); otherwise band the m-pairs by 8 (measured, ncu DRAM
+  // read: down 1.79 -> 1.20 GB, qkv 189 -> 143 MB, o 292 -> 213 MB; the
+  // chunk precompute's M = 34,816 would otherwise re-read all of A for every
+  // n tile). CC_GEMM_GROUP=g in the environment forces a band (0: m fastest).
+  static const int group_env = [] {
+    const char* e = getenv("CC_GEMM_GROUP");
+    return e ? atoi(e) : -1;
+  }();
+  const double elem = kTF32 ? 4.0 : 2.0, l2_half = 60e6;
+  const bool a_small = (double)a->M * a->K * elem <= l2_half, b_small = (double)a->N * a->K * elem <= l2_half;
+  const int group_m = group_env >= 0 ? group_env : ((a_small && !b_small) ? 0 : 8);
   ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
   gemm2_kernel<BN, kTF32, kEpi><<<2 * clusters, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m2, num_n, num_kb,
-                                                                               (int)a->K);
+                                                                               (int)a->K, group_m);
   CC_LAUNCH_CHECK("gemm (CTA pair)");
   return CC_OK;
 }

@@ -578,3 +578,54 @@ def test_batched_silu_is_bitwise_the_ieee_formula():
     L.call("cc_check_silu", x.data_ptr(), x.numel(), bad.data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     assert int(bad.item()) == 0
+
+
+_BAND_SCRIPT = r"""
+import sys, math
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from paper_2510_10129_b200 import _lib as L, runtime
+L.load()
+DEV = "cuda:0"
+g = torch.Generator(device=DEV).manual_seed(5)
+# both operands > 60 MB: banded by default
+M, N, K = 2600, 3584, 12288
+A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+B = (torch.randn(N, K, device=DEV, generator=g) * 0.05).to(torch.bfloat16)
+bias = torch.randn(N, device=DEV, generator=g)
+C = torch.empty(M, N, device=DEV, dtype=torch.float32)
+runtime.gemm(L.CC_GEMM_BF16, L.CC_EPI_STORE, M, N, K, A, B, bias=bias, C=C, ldc=N, c_mode=L.CC_F32)
+h = torch.randn(M, N, device=DEV, generator=g)
+runtime.gemm(L.CC_GEMM_BF16, L.CC_EPI_RESIDUAL, M, N, K, A, B, C=h, ldc=N, c_mode=L.CC_F32)
+torch.cuda.synchronize()
+ref = (A[:64].double() @ B.double().t() + bias.double())
+err = (C[:64].double() - ref).abs().max().item()
+assert err < 1e-4 * math.sqrt(K), err
+np.savez(sys.argv[2], store=C.cpu().numpy(), residual=h.cpu().numpy())
+"""
+
+
+def test_gemm_banded_schedule_is_bitwise_the_same(tmp_path):
+    """The CTA-pair GEMM bands its persistent tile schedule (m fastest inside
+    bands of 8 m-pairs) unless A fits in L2 and B does not — e.g. the
+    recompute's down projection, both operands > 60 MB. Every tile runs the same arithmetic whichever wave it
+    lands in, so the banded run (default; and a band of 3 with a ragged last
+    band) is bitwise the m-fastest run (CC_GEMM_GROUP=0)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for flag in ("", "0", "3"):
+        f = tmp_path / f"band_{flag or 'default'}.npz"
+        env = dict(os.environ)
+        env.pop("CC_GEMM_GROUP", None)
+        if flag:
+            env["CC_GEMM_GROUP"] = flag
+        r = subprocess.run([sys.executable, "-c", _BAND_SCRIPT, root, str(f)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[flag] = dict(np.load(f))
+    for flag in ("", "3"):
+        for key in ("store", "residual"):
+            assert np.array_equal(outs[flag][key], outs["0"][key]), (flag, key)
