@@ -473,10 +473,48 @@ __device__ __forceinline__ void epilogue_tail(const EpiParams& ep, float* v, int
   __syncwarp();  // the staging tile is reused by the next chunk
 }
 
+// Tile t of a persistent schedule -> (m tile, n tile). group_m = 0: m fastest
+// over all m (a wave shares the B panels of a few n tiles and re-reads all of
+// A per wave: right when A stays in L2 and B does not). group_m = g: m fastest
+// inside bands of g m tiles, so a wave covers ~g x (wave / g) tiles and reads
+// each A and B panel about once per band.
+__device__ __forceinline__ void tile_mn(int t, int num_m, int num_n, int group_m, int& mb, int& nb) {
+  if (group_m <= 0 || group_m >= num_m) {
+    mb = t % num_m;
+    nb = t / num_m;
+    return;
+  }
+  const int per = group_m * num_n;  // tiles per full band (every band but the last is full)
+  const int g = t / per, local = t - g * per;
+  const int m0 = g * group_m, gm = min(group_m, num_m - m0);
+  mb = m0 + local % gm;
+  nb = local / gm;
+}
+
+
+// Band size for a persistent GEMM schedule (tile_mn): a wave of the grid over
+// an a x b block of tiles reads ~(a + b) operand panels from DRAM. m fastest
+// over all m is right only when A is small enough to stay in L2 and B is not
+// (the recompute's gate/up: A 47 MB, B 271 MB, B read once); otherwise band
+// (measured on the CTA-pair kernel, ncu DRAM read: down 1.79 -> 1.20 GB, qkv
+// 189 -> 143 MB, o 292 -> 213 MB; at M = 34,816 rows (chunk precompute, full
+// prefill) m fastest re-reads all of A for every n tile). CC_GEMM_GROUP=g in
+// the environment forces a band of g (0: m fastest).
+static int schedule_band(const cc_gemm_args* a, double elem, int band) {
+  static const int group_env = [] {
+    const char* e = getenv("CC_GEMM_GROUP");
+    return e ? atoi(e) : -1;
+  }();
+  if (group_env >= 0) return group_env;
+  const double l2_half = 60e6;
+  const bool a_small = (double)a->M * a->K * elem <= l2_half, b_small = (double)a->N * a->K * elem <= l2_half;
+  return (a_small && !b_small) ? 0 : band;
+}
+
 template <int BN, bool kTF32, int kEpi = -1>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
-                int num_m, int num_n, int num_kb, int k_orig, int kb_per_phase) {
+                int num_m, int num_n, int num_kb, int k_orig, int kb_per_phase, int group_m) {
   using Cfg = GemmCfg<BN, kTF32>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
@@ -520,7 +558,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int issued = 0;
 #endif
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int mb = t % num_m, nb = t / num_m;
+        int mb, nb;
+        tile_mn(t, num_m, num_n, group_m, mb, nb);
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
 #ifdef CC_DBG_GEMM_NO_LOADS
@@ -645,7 +684,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     (void)epi_i;
     (void)tile_i;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-      const int mb = t % num_m, nb = t / num_m;
+      int mb, nb;
+      tile_mn(t, num_m, num_n, group_m, mb, nb);
       const int64_t row0 = (int64_t)mb * kBM + quarter * 32;
       if constexpr (kTF32) {
         // this warp's accumulator columns, BN/2 per row (GLU: its gate columns
@@ -989,24 +1029,6 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `b
       : "memory");
 }
 
-// Tile t of the persistent schedule -> (m pair, n tile). group_m = 0: m
-// fastest over all m (a wave of clusters shares the B columns of ~2-3 n tiles
-// and re-reads all of A per wave, right when A stays in L2). group_m = g:
-// m fastest inside bands of g m-pairs, so a wave covers ~g x (clusters / g)
-// tiles and reads both A and B once per band (both operands larger than L2).
-__device__ __forceinline__ void tile_mn(int t, int num_m2, int num_n, int group_m, int& mb, int& nb) {
-  if (group_m <= 0 || group_m >= num_m2) {
-    mb = t % num_m2;
-    nb = t / num_m2;
-    return;
-  }
-  const int per = group_m * num_n;  // tiles per full band (every band but the last is full)
-  const int g = t / per, local = t - g * per;
-  const int m0 = g * group_m, gm = min(group_m, num_m2 - m0);
-  mb = m0 + local % gm;
-  nb = local / gm;
-}
-
 template <int BN, bool kTF32, int kEpi = -1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
@@ -1208,8 +1230,10 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   const int tiles = num_m * num_n;
   const int grid = tiles < num_sms() ? tiles : num_sms();
   ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
+  // 3xTF32 operands are split planes: 3 x 4 bytes per element in A's and B's panels
+  const int group_m = schedule_band(a, kTF32 ? 12.0 : 2.0, 16);
   gemm_kernel<BN, kTF32, kEpi><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb, (int)a->K,
-                                                                      kTF32 ? kTf32KbPerPhase : num_kb);
+                                                                      kTF32 ? kTf32KbPerPhase : num_kb, group_m);
   CC_LAUNCH_CHECK("gemm");
   return CC_OK;
 }
@@ -1229,20 +1253,7 @@ static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, 
   const int num_kb = (int)(((kTF32 ? a->K : kop) + Cfg::BK - 1) / Cfg::BK);
   const int tiles = num_m2 * num_n;
   const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
-  // Schedule: a wave of ~74 clusters over an a x b block of tiles reads ~(a + b)
-  // operand panels from DRAM. m fastest over all m (b ~ 3) is right only when
-  // A is small enough to stay in L2 and B is not (gate/up: A 47 MB, B 271 MB:
-  // B is read once); otherwise band the m-pairs by 8 (measured, ncu DRAM
-  // read: down 1.79 -> 1.20 GB, qkv 189 -> 143 MB, o 292 -> 213 MB; the
-  // chunk precompute's M = 34,816 would otherwise re-read all of A for every
-  // n tile). CC_GEMM_GROUP=g in the environment forces a band (0: m fastest).
-  static const int group_env = [] {
-    const char* e = getenv("CC_GEMM_GROUP");
-    return e ? atoi(e) : -1;
-  }();
-  const double elem = kTF32 ? 4.0 : 2.0, l2_half = 60e6;
-  const bool a_small = (double)a->M * a->K * elem <= l2_half, b_small = (double)a->N * a->K * elem <= l2_half;
-  const int group_m = group_env >= 0 ? group_env : ((a_small && !b_small) ? 0 : 8);
+  const int group_m = schedule_band(a, kTF32 ? 12.0 : 2.0, 8);  // bands of 8 m-pairs
   ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
   gemm2_kernel<BN, kTF32, kEpi><<<2 * clusters, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m2, num_n, num_kb,
                                                                                (int)a->K, group_m);

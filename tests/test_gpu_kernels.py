@@ -601,14 +601,28 @@ torch.cuda.synchronize()
 ref = (A[:64].double() @ B.double().t() + bias.double())
 err = (C[:64].double() - ref).abs().max().item()
 assert err < 1e-4 * math.sqrt(K), err
-np.savez(sys.argv[2], store=C.cpu().numpy(), residual=h.cpu().numpy())
+# 3xTF32 on single-CTA tiles (split-plane operands, 12 bytes per element):
+# A 80 MB, B 63 MB -> banded by 16 m tiles (21 m tiles: a ragged last band)
+M2, N2, K2 = 2600, 2048, 2560
+a = torch.randn(M2, K2, device=DEV, generator=g)
+b = torch.randn(N2, K2, device=DEV, generator=g)
+A2 = torch.empty(M2, 3 * K2, device=DEV)
+B2 = torch.empty(N2, 3 * K2, device=DEV)
+s = torch.cuda.current_stream().cuda_stream
+L.call("cc_convert_matrix", a.data_ptr(), M2, K2, A2.data_ptr(), L.CC_F32_SPLIT3, 0, s)
+L.call("cc_convert_matrix", b.data_ptr(), N2, K2, B2.data_ptr(), L.CC_F32_SPLIT3, 1, s)
+C2 = torch.empty(M2, N2, device=DEV)
+runtime.gemm(L.CC_GEMM_TF32X3, L.CC_EPI_STORE, M2, N2, K2, A2, B2, C=C2, ldc=N2, c_mode=L.CC_F32)
+torch.cuda.synchronize()
+np.savez(sys.argv[2], store=C.cpu().numpy(), residual=h.cpu().numpy(), tf32=C2.cpu().numpy())
 """
 
 
 def test_gemm_banded_schedule_is_bitwise_the_same(tmp_path):
     """The CTA-pair GEMM bands its persistent tile schedule (m fastest inside
     bands of 8 m-pairs) unless A fits in L2 and B does not — e.g. the
-    recompute's down projection, both operands > 60 MB. Every tile runs the same arithmetic whichever wave it
+    recompute's down projection, both operands > 60 MB; the single-CTA
+    kernel (3xTF32 here) bands by 16 m tiles under the same rule. Every tile runs the same arithmetic whichever wave it
     lands in, so the banded run (default; and a band of 3 with a ragged last
     band) is bitwise the m-fastest run (CC_GEMM_GROUP=0)."""
     import os
@@ -627,5 +641,5 @@ def test_gemm_banded_schedule_is_bitwise_the_same(tmp_path):
         assert r.returncode == 0, r.stderr[-2000:]
         outs[flag] = dict(np.load(f))
     for flag in ("", "3"):
-        for key in ("store", "residual"):
+        for key in ("store", "residual", "tf32"):
             assert np.array_equal(outs[flag][key], outs["0"][key]), (flag, key)
