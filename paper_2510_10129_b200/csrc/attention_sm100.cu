@@ -22,7 +22,8 @@
 //               writes P (bf16 pairs) back over its S row with tcgen05.st.
 //               Lazy rescale: the running max moves (and O is rescaled in TMEM)
 //               only when a tile raises it by > 2^8. One FFMA per element
-//               folds scale and max; 3 of 16 exp2 pairs run as a degree-3
+//               folds scale and max; 4 of 16 exp2 pairs (the first of each
+//               32-key chunk) run as a degree-3
 //               polynomial on the FMA pipe to offload MUFU. P goes back in
 //               four 32-key parts, each released to the PV MMA as soon as it
 //               is in TMEM.
@@ -211,9 +212,18 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 
 // pairs (of 16 per 32-key chunk) whose exponentials run on the FMA pipe
 #ifndef CC_FA_POLY
-#define CC_FA_POLY 3
+#define CC_FA_POLY 4
 #endif
 constexpr int kFaPolyPairs = CC_FA_POLY;
+// where in a chunk's 16 pairs the polynomial ones sit: 0 spread evenly, 1 first, 2 last
+#ifndef CC_FA_POLY_POS
+#define CC_FA_POLY_POS 1
+#endif
+__host__ __device__ constexpr bool fa_poly_pair(int e) {
+  return CC_FA_POLY_POS == 1   ? e < kFaPolyPairs
+         : CC_FA_POLY_POS == 2 ? e >= 16 - kFaPolyPairs
+                               : (e & 15) * kFaPolyPairs % 16 >= 16 - kFaPolyPairs;
+}
 
 // P is handed to the PV MMA in this many key parts: the MMA warp starts
 // O += P V on the first part while the softmax warps still exponentiate the
@@ -507,7 +517,7 @@ __global__ void __launch_bounds__(kFaThreads, 1)
         for (int e = 0; e < 16; ++e) {
           const float2 x = __ffma2_rn(make_float2(sv[c * 32 + 2 * e], sv[c * 32 + 2 * e + 1]), sc2, nb2);
           float2 p;
-          if ((e & 15) * kFaPolyPairs % 16 >= 16 - kFaPolyPairs) {  // kFaPolyPairs of 16 pairs on the FMA pipe
+          if (fa_poly_pair(e)) {  // kFaPolyPairs of 16 pairs on the FMA pipe
             p = ex2_poly2(x);
           } else {
             p.x = ex2_mufu(x.x);
