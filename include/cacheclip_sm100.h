@@ -438,6 +438,10 @@ int cc_forward_banked(const cc_model_desc* md, const int64_t* ids, const int64_t
  * reduction, 9 lm_head, 10 rope table. */
 void cc_profile_enable(int32_t on);
 int64_t cc_profile_collect(int32_t* ops, double* work, float* ms, int64_t cap);
+/* The same records as a timeline: start and end of each launch in ms after
+ * the first record's start (idle gaps between launches, stream overlap).
+ * Does not clear; call before cc_profile_collect. */
+int64_t cc_profile_timeline(int32_t* ops, float* t0_ms, float* t1_ms, int64_t cap);
 /* Set the algorithmic work of pending records of `op` launched with an
  * unknown (negative) work: cc_forward_rows with attn_pairs < 0, i.e. launched
  * before the host has read the selected positions. */

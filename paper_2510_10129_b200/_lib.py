@@ -135,6 +135,7 @@ _SIGS = {
     "cc_profile_enable": ([i32], None),
     "cc_profile_collect": ([vp, vp, vp, i64], i64),
     "cc_profile_fill_work": ([i32, ctypes.c_double], None),
+    "cc_profile_timeline": ([vp, vp, vp, i64], i64),
 }
 
 PROFILE_OPS = ("gemm_bf16", "gemm_3xtf32", "attention_tcgen05", "attention_mma", "banked_attention_f32",
@@ -158,6 +159,20 @@ def profile_collect():
     n = min(n, cap)
     return [(PROFILE_OPS[o] if 0 <= o < len(PROFILE_OPS) else f"op{o}", float(w), float(t))
             for o, w, t in zip(ops[:n], work[:n], ms[:n])]
+
+def profile_timeline():
+    """[(op name, start ms, end ms)] of every launch recorded since enable,
+    relative to the first start; does not clear (profile_collect does)."""
+    import numpy as np
+    lib = load()
+    cap = 1 << 16
+    ops = np.zeros(cap, np.int32)
+    t0 = np.zeros(cap, np.float32)
+    t1 = np.zeros(cap, np.float32)
+    n = min(int(lib.cc_profile_timeline(ops.ctypes.data, t0.ctypes.data, t1.ctypes.data, cap)), cap)
+    return [(PROFILE_OPS[o] if 0 <= o < len(PROFILE_OPS) else f"op{o}", float(a), float(b))
+            for o, a, b in zip(ops[:n], t0[:n], t1[:n])]
+
 
 EXPORTED_SYMBOLS = tuple(_SIGS)
 

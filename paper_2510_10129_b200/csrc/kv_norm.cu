@@ -623,6 +623,22 @@ int64_t cc_profile_collect(int32_t* ops, double* work, float* ms, int64_t cap) {
   g_prof.clear();
   return n;
 }
+int64_t cc_profile_timeline(int32_t* ops, float* t0_ms, float* t1_ms, int64_t cap) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  const int64_t n = (int64_t)g_prof.size();
+  if (!n) return 0;
+  cudaEventSynchronize(g_prof.back().e1);
+  const cudaEvent_t origin = g_prof.front().e0;
+  for (int64_t k = 0; k < n && k < cap; ++k) {
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, origin, g_prof[k].e0);
+    cudaEventElapsedTime(&b, origin, g_prof[k].e1);
+    ops[k] = g_prof[k].op;
+    t0_ms[k] = a;
+    t1_ms[k] = b;
+  }
+  return n;
+}
 void cc_profile_fill_work(int32_t op, double work) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   for (auto& r : g_prof)

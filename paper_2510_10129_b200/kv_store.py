@@ -181,6 +181,25 @@ class ChunkCache:
     def chunk_ids(self) -> list[int]:
         return self.token_ids[self.prefix_len:]
 
+    def token_ids_array(self) -> np.ndarray:
+        """token_ids as int64, formed once (a chunk cache is immutable): the
+        merge concatenates these instead of converting ~10^4 Python ints per
+        request on the host's critical path."""
+        arr = getattr(self, "_ids_np", None)
+        if arr is None or arr.size != len(self.token_ids):
+            arr = np.asarray(self.token_ids, dtype=np.int64)
+            self._ids_np = arr
+        return arr
+
+    def chunk_key(self) -> bytes:
+        """The chunk's token ids (after the prefix) as int64 bytes, formed
+        once: equal chunk texts compare as one memcmp per request."""
+        key = getattr(self, "_chunk_key", None)
+        if key is None or len(key) != 8 * self.chunk_len:
+            key = self.token_ids_array()[self.prefix_len:].tobytes()
+            self._chunk_key = key
+        return key
+
     @property
     def chunk_len(self) -> int:
         return self.n_rows - self.prefix_len
@@ -263,6 +282,7 @@ class MergedCache:
         self.model_fingerprint = model_fingerprint
         self.recomputed_rows = tuple(recomputed_rows)
         self._ids_dev = None
+        self._ids_np = None  # int64 copy of token_ids when the merge formed one
         self.layer_ready = None  # per-layer events while a streamed merge is in flight
         if self._n_rows != len(self.token_ids) or (self._source is not None and self._n_rows != len(self._source)):
             raise CacheConsistencyError("rows, token ids, and source map disagree")
@@ -287,7 +307,9 @@ class MergedCache:
         """Device copy of token_ids (uploaded once, extended in place on append)."""
         if self._ids_dev is None or self._ids_dev.numel() < self._n_rows:
             buf = torch.empty(max(self.capacity, self._n_rows), dtype=torch.int64, device=self.k_store.device)
-            buf[: self._n_rows].copy_(host_to_device(np.asarray(self.token_ids, dtype=np.int64), buf.device))
+            ids = self._ids_np if self._ids_np is not None and self._ids_np.size == self._n_rows \
+                else np.asarray(self.token_ids, dtype=np.int64)
+            buf[: self._n_rows].copy_(host_to_device(ids, buf.device))
             self._ids_dev = buf
         return self._ids_dev
 
@@ -621,4 +643,6 @@ def merge_caches(chunks: Sequence[ChunkCache], rope: RopeParams, trace: Pipeline
                          tokenizer_id=first.tokenizer_id, model_fingerprint=first.model_fingerprint,
                          k_store=k_store, v_store=v_store, n_rows=total)
     merged.layer_ready = layer_ready
+    merged._ids_np = np.concatenate([first.token_ids_array()[:sink]] +
+                                    [c.token_ids_array()[sink:] for c in chunks])
     return merged

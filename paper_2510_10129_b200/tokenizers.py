@@ -12,6 +12,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from typing import Iterable, Sequence
 
+import numpy as np
+
 from .errors import SpanCoverageError, UnknownCharacterError, VocabFormatError
 
 
@@ -42,7 +44,7 @@ class GreedyTokenizer:
         self._lengths = sorted({len(t) for t in vocab}, reverse=True)
         self.tokenizer_id = tokenizer_id
         self._digest: str | None = None
-        self._canonical: set[tuple[int, ...]] = set()  # id sequences known to re-encode to themselves
+        self._canonical: set[bytes] = set()  # id sequences (int64 bytes) known to re-encode to themselves
 
     @property
     def vocab_digest(self) -> str:
@@ -57,13 +59,17 @@ class GreedyTokenizer:
             self._digest = h.hexdigest()
         return self._digest
 
-    def is_canonical(self, ids: Sequence[int]) -> bool:
+    def is_canonical(self, ids: Sequence[int], key: bytes | None = None) -> bool:
         """True when decode(ids) re-encodes to exactly ids (memoised: a
-        cached chunk's ids are checked once per tokenizer, not per request)."""
-        key = tuple(int(i) for i in ids)
+        cached chunk's ids are checked once per tokenizer, not per request).
+        ``key``: the ids as int64 bytes when the caller has them
+        (``ChunkCache.chunk_key``), so a repeat check is one hash lookup."""
+        if key is None:
+            key = np.asarray([int(i) for i in ids], dtype=np.int64).tobytes()
         if key in self._canonical:
             return True
-        ok = self.encode(self.decode(key)) == list(key)
+        seq = [int(i) for i in ids]
+        ok = self.encode(self.decode(seq)) == seq
         if ok:
             self._canonical.add(key)
         return ok

@@ -1,5 +1,7 @@
 """Host-side cProfile of one C3 cacheclip_prefill (device-resident caches):
-which Python work precedes the first kernel launch."""
+which Python work precedes the first kernel launch, and (argv[1] = 5: the
+default 8/5 window rule) what runs between the selection read-back and the
+recompute launch."""
 import cProfile
 import os
 import pstats
@@ -18,7 +20,8 @@ aux = cc.init_model(w.aux, 1, device=dev, source="torch")
 prefix, chunk_ids, query = w.token_ids(1000)
 chunks = cc.prefill_chunks(primary, prefix, chunk_ids)
 aux_chunks = cc.prefill_chunks(aux, prefix, chunk_ids)
-cfg = cc.SelectionConfig(0.2, 8, 1)
+thr = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+cfg = cc.SelectionConfig(0.2, 8, thr)
 for _ in range(3):
     cc.cacheclip_prefill(primary, aux, chunks, aux_chunks, query, cfg)
 torch.cuda.synchronize()
@@ -27,4 +30,5 @@ pr.enable()
 cc.cacheclip_prefill(primary, aux, chunks, aux_chunks, query, cfg)
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("cumulative").print_stats(25)
+st.sort_stats("cumulative").print_stats(30)
+st.sort_stats("tottime").print_stats(20)

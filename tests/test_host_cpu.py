@@ -282,7 +282,8 @@ def test_chunk_spans_identity_needs_equal_vocab_contents():
     ta, tb = GreedyTokenizer(va, "tok"), GreedyTokenizer(vb, "tok")
     assert ta.vocab_digest != tb.vocab_digest
     assert GreedyTokenizer(list(va), "other").vocab_digest == ta.vocab_digest
-    mk = lambda ids: SimpleNamespace(chunk_ids=list(ids), chunk_len=len(ids))  # noqa: E731
+    mk = lambda ids: SimpleNamespace(chunk_ids=list(ids), chunk_len=len(ids),  # noqa: E731
+                                     chunk_key=lambda: np.asarray(ids, dtype=np.int64).tobytes())
     # equal contents: identity alignment
     spans, n = chunk_spans([mk([2, 3])], [mk([2, 3])], ta, GreedyTokenizer(list(va), "x"))
     assert spans is None and n == 2
