@@ -287,6 +287,8 @@ __global__ void __launch_bounds__(kFaThreads, 1)
   // some warps' atomicMax/atomicMin and reset them)
   __syncthreads();
   if (warp == 1) tmem_alloc(tmem_slot, 512);
+  pdl_wait();  // nothing above touched global memory
+  pdl_trigger();
 
   // ---- prologue: row ranges -> the CTA's key tiles; then the Q gather ----
   const int tq = warp >= 4 ? (warp - 4) >> 2 : 0;  // query tile of this softmax warp
@@ -633,10 +635,10 @@ static int fa_launch(const void* q, int64_t ldq, const int64_t* positions, const
   const int n_ctas = (int)((m * G + 2 * kFaTileRows - 1) / (2 * kFaTileRows));
   dim3 grid(n_ctas * hkv, 1, n_splits);
   ProfScope ps(st, OP_ATTENTION, flops);
-  fa_sparse_row_kernel<D><<<grid, kFaThreads, FaCfg<D>::SMEM, st>>>(
+  const cudaError_t e = launch_pdl(fa_sparse_row_kernel<D>, grid, dim3(kFaThreads), FaCfg<D>::SMEM, st,
       tk, tv, (const __nv_bfloat16*)q, ldq, positions, kstart, m, n_keys, hq, hkv, factor, row_factor,
       (__nv_bfloat16*)out, ldo, n_ctas, o_part, lse_part, part_bf16);
-  CC_LAUNCH_CHECK("fa_sparse_row");
+  if (e != cudaSuccess) return fail(CC_ERR_CUDA, "fa_sparse_row launch failed: %s", cudaGetErrorString(e));
   return CC_OK;
 }
 
@@ -650,6 +652,8 @@ __global__ void lse_merge_kernel(const P* __restrict__ o_parts, const float* __r
                                  int64_t part_stride, int64_t m, int hq, void* __restrict__ out, int64_t ldo,
                                  int out_dtype) {
   constexpr int C = D / 32;  // columns per lane
+  pdl_wait();
+  pdl_trigger();
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (gw >= m * hq) return;
@@ -872,8 +876,8 @@ extern "C" int cc_lse_merge(const void* o_parts, int32_t part_dtype, const float
   cudaStream_t st = as_stream(stream);
   ProfScope ps(st, OP_MERGE, 0.0);
 #define CC_MERGE(P, D)                                                                                             \
-  lse_merge_kernel<P, D><<<grid, 256, 0, st>>>(static_cast<const P*>(o_parts), lse_parts, n_parts, part_stride, m, \
-                                               n_q_heads, out, ldo, out_dtype)
+  launch_pdl(lse_merge_kernel<P, D>, dim3(grid), dim3(256), 0, st, static_cast<const P*>(o_parts), lse_parts, n_parts, \
+             part_stride, m, n_q_heads, out, ldo, out_dtype)
   if (part_dtype == CC_BF16) {
     if (head_dim == 128) CC_MERGE(__nv_bfloat16, 128); else CC_MERGE(__nv_bfloat16, 64);
   } else {

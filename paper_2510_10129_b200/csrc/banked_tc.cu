@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(kBtThreads) banked_tc_kernel(
   uint64_t* pv_bar = s_bar + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_bar + 2);
 
+  pdl_wait();  // first global access below (the bank table)
+  pdl_trigger();
   const cc_bank_seq sq = seqs[blockIdx.z];
   const int kvh = blockIdx.y;
   const int G = n_q_heads / n_kv_heads;
@@ -481,14 +483,12 @@ extern "C" int cc_banked_attention_f32(const cc_bank_seq* seqs_dev, int32_t n_se
   ProfScope ps(st, OP_BANKED, 0);
   if (head_dim == 64) {
     set_smem_once<banked_tc_kernel<64>>(BtCfg<64>::SMEM);
-    banked_tc_kernel<64><<<grid, kBtThreads, BtCfg<64>::SMEM, st>>>(seqs_dev, q, k_new, v_new, n_q_heads,
-                                                                      n_kv_heads, factor, qpb, out, out_mode,
-                                                                      weights_out, w_col0, w_ld);
+    launch_pdl(banked_tc_kernel<64>, grid, dim3(kBtThreads), BtCfg<64>::SMEM, st, seqs_dev, q, k_new, v_new,
+               n_q_heads, n_kv_heads, factor, qpb, out, out_mode, weights_out, w_col0, w_ld);
   } else {
     set_smem_once<banked_tc_kernel<128>>(BtCfg<128>::SMEM);
-    banked_tc_kernel<128><<<grid, kBtThreads, BtCfg<128>::SMEM, st>>>(seqs_dev, q, k_new, v_new, n_q_heads,
-                                                                        n_kv_heads, factor, qpb, out, out_mode,
-                                                                        weights_out, w_col0, w_ld);
+    launch_pdl(banked_tc_kernel<128>, grid, dim3(kBtThreads), BtCfg<128>::SMEM, st, seqs_dev, q, k_new, v_new,
+               n_q_heads, n_kv_heads, factor, qpb, out, out_mode, weights_out, w_col0, w_ld);
   }
   CC_LAUNCH_CHECK("banked_attention_tc");
   return CC_OK;

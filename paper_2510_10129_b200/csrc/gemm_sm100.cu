@@ -549,6 +549,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the prologue above touched no global memory
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -815,6 +817,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the prologue above touched no global memory
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1075,6 +1079,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   __syncthreads();  // also a CTA barrier for tools that do not model barrier.cluster (racecheck)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the prologue above touched no global memory
+  pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {  // both CTAs: own A rows and own B half, completion counted on the leader's barrier
@@ -1232,9 +1238,10 @@ static int launch(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, cudaS
   ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
   // 3xTF32 operands are split planes: 3 x 4 bytes per element in A's and B's panels
   const int group_m = schedule_band(a, kTF32 ? 12.0 : 2.0, 16);
-  gemm_kernel<BN, kTF32, kEpi><<<grid, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_n, num_kb, (int)a->K,
-                                                                      kTF32 ? kTf32KbPerPhase : num_kb, group_m);
-  CC_LAUNCH_CHECK("gemm");
+  const cudaError_t e = launch_pdl(gemm_kernel<BN, kTF32, kEpi>, dim3(grid), dim3(kGemmThreads), Cfg::SMEM_BYTES, st,
+                                   ta, tb, ep, num_m, num_n, num_kb, (int)a->K,
+                                   kTF32 ? kTf32KbPerPhase : num_kb, group_m);
+  if (e != cudaSuccess) return fail(CC_ERR_CUDA, "gemm launch failed: %s", cudaGetErrorString(e));
   return CC_OK;
 }
 
@@ -1255,9 +1262,9 @@ static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, 
   const int clusters = tiles < num_sms() / 2 ? tiles : num_sms() / 2;
   const int group_m = schedule_band(a, kTF32 ? 12.0 : 2.0, 8);  // bands of 8 m-pairs
   ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
-  gemm2_kernel<BN, kTF32, kEpi><<<2 * clusters, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m2, num_n, num_kb,
-                                                                               (int)a->K, group_m);
-  CC_LAUNCH_CHECK("gemm (CTA pair)");
+  const cudaError_t e = launch_pdl(gemm2_kernel<BN, kTF32, kEpi>, dim3(2 * clusters), dim3(kGemmThreads),
+                                   Cfg::SMEM_BYTES, st, ta, tb, ep, num_m2, num_n, num_kb, (int)a->K, group_m);
+  if (e != cudaSuccess) return fail(CC_ERR_CUDA, "gemm (CTA pair) launch failed: %s", cudaGetErrorString(e));
   return CC_OK;
 }
 
@@ -1319,9 +1326,9 @@ static int launch_splitk(const cc_gemm_args* a, const EpiParams& ep, int64_t kop
   const int num_n = (int)((a->N + BN - 1) / BN);
   const int num_kb = (int)((kop + Cfg::BK - 1) / Cfg::BK);
   ProfScope ps(st, OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
-  gemm_splitk_kernel<BN><<<num_m * num_n * S, kGemmThreads, Cfg::SMEM_BYTES, st>>>(ta, tb, ep, num_m, num_kb, S,
-                                                                                 ws.parts, ws.counters);
-  CC_LAUNCH_CHECK("gemm (split-K)");
+  const cudaError_t e = launch_pdl(gemm_splitk_kernel<BN>, dim3(num_m * num_n * S), dim3(kGemmThreads),
+                                   Cfg::SMEM_BYTES, st, ta, tb, ep, num_m, num_kb, S, ws.parts, ws.counters);
+  if (e != cudaSuccess) return fail(CC_ERR_CUDA, "gemm (split-K) launch failed: %s", cudaGetErrorString(e));
   return CC_OK;
 }
 

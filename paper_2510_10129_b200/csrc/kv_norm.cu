@@ -52,6 +52,14 @@ static cudaEvent_t pool_event() {
 
 bool prof_enabled() { return g_prof_on; }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CC_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void prof_record(cudaStream_t st, int op, double work, cudaEvent_t* e0, bool begin) {
   std::lock_guard<std::mutex> lk(g_prof_mu);
   if (begin) {
@@ -340,6 +348,8 @@ __global__ void __launch_bounds__(256) rmsnorm_warp_kernel(
     float* __restrict__ h_out, const float* __restrict__ gain, float eps, void* __restrict__ x_out, int x_mode,
     const float* __restrict__ h_in, int64_t ld_h, int64_t rows) {
   __shared__ float red[8];
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x;  // "lane" strides the row by 256 float4s
   const int64_t row = blockIdx.x;
   const int n4 = d >> 2;
@@ -401,8 +411,8 @@ static void launch_rmsnorm(const int64_t* ids, const void* embed, int embed_dtyp
   const unsigned grid = (unsigned)rows;
 #define CC_NORM_CASE(V)                                                                                        \
   if (per_lane <= V) {                                                                                         \
-    rmsnorm_warp_kernel<V><<<grid, 256, 0, st>>>(ids, embed, embed_dtype, d, h_out, gain, eps, x_out, x_mode, \
-                                                 h_in, ld_h, rows);                                            \
+    launch_pdl(rmsnorm_warp_kernel<V>, dim3(grid), dim3(256), 0, st, ids, embed, embed_dtype, d, h_out, gain, eps, \
+               x_out, x_mode, h_in, ld_h, rows);                                                                  \
     return;                                                                                                    \
   }
   CC_NORM_CASE(1)
