@@ -37,3 +37,26 @@ for i in range(25):
     if i >= 5:
         ts.append(a.elapsed_time(b))
 print(f"decode at {cache.n_rows} rows: {np.median(ts):.2f} ms/token (lib {os.path.basename(_lib.LIB_PATH)})")
+# one token under the launch profiler: where the step goes
+_lib.profile_collect()
+_lib.profile_enable(True)
+a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+a.record()
+logits, cache = cc.decode_step(primary, cache, tok)
+b.record()
+torch.cuda.synchronize()
+_lib.profile_enable(False)
+tl = _lib.profile_timeline()
+recs = _lib.profile_collect()
+ops = {}
+for op, _, ms in recs:
+    n, t = ops.get(op, (0, 0.0))
+    ops[op] = (n + 1, t + ms)
+span = max(t1 for _, _, t1 in tl) - min(t0 for _, t0, _ in tl)
+print(f"profiled token: wall {a.elapsed_time(b):.2f} ms, first..last launch {span:.2f} ms, "
+      f"kernel sum {sum(t for _, t in ops.values()):.2f} ms over {len(recs)} launches")
+for op, (n, t) in sorted(ops.items(), key=lambda kv: -kv[1][1]):
+    print(f"   {op:24s} {n:4d} launches {t:7.3f} ms")
+print("first layer, per launch (op, work, us; GEMM work 2*M*N*K):")
+for (op, wk, ms), (_, t0, t1) in list(zip(recs, tl))[:12]:
+    print(f"   {op:20s} work {wk:12.4g}  {ms * 1e3:7.1f} us  start {t0 * 1e3:8.1f} us")
