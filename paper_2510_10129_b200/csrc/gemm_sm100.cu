@@ -1295,6 +1295,204 @@ static int splitk_ws(cudaStream_t st, SplitKWs* out) {
   return CC_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Weight-streaming GEMV for bf16 GEMMs of M <= 4 rows (a decode step, the
+// query row of a tiny request). A tcgen05 tile of 128 rows would hold one
+// live row; the launch is bound by how fast the weights stream from HBM, so
+// the CUDA cores do the dot products and every load is a contiguous 16-byte
+// segment of a K-major weight row. One CTA per 32-column output chunk (64
+// weight rows for GLU: 32 gate + 32 up), 8 warps x 4 weight rows each (16
+// x 4 for GLU: every warp takes 4 rows of the chunk per pass), lanes striding
+// K with four 16-byte loads per row in flight; each warp butterfly-reduces
+// its (row, weight row) sums into smem; warp 0 then holds the chunk as the
+// tensor-core kernels' epilogue expects it (lane = row, 32 columns) and runs
+// the same fused epilogue code (bias, RoPE + K/V scatter, residual + RMSNorm
+// partials, GLU, 1/rms scaling).
+// ---------------------------------------------------------------------------
+constexpr int kGemvMaxRows = 4;
+constexpr int kGemvWarps = 8;
+constexpr int kGemvRowsPerWarp = 4;  // weight rows a warp reduces per pass
+constexpr int kGemvUnroll = 4;       // 16-byte K segments per weight row in flight per lane
+#ifndef CC_GEMV_PREFETCH
+#define CC_GEMV_PREFETCH 4096
+#endif
+constexpr int64_t kGemvPrefetchBytes = CC_GEMV_PREFETCH;  // L2 prefetch per weight row (bounded: L2 holds it)
+
+template <int MR, int kEpi>
+__global__ void __launch_bounds__(32 * kGemvWarps) gemv_kernel(const __nv_bfloat16* __restrict__ A, int64_t lda,
+                                                               const __nv_bfloat16* __restrict__ B, int64_t ldb,
+                                                               int K, EpiParams ep) {
+  constexpr bool kGlu = kEpi == CC_EPI_GLU;
+  constexpr int kRows = kGlu ? 64 : 32;  // weight rows of the chunk
+  __shared__ float res[MR][kRows];
+  __shared__ __align__(16) float stg[32 * 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q = blockIdx.x;  // output chunk of 32 columns
+  int nb, c0;
+  int64_t wrow0, wrow1;  // first weight row of the chunk's (gate,) up half
+  if constexpr (kGlu) {
+    nb = q >> 1;
+    c0 = (q & 1) * 32;
+    wrow0 = b_row<128, kEpi>(ep, nb, 0) + c0;
+    wrow1 = b_row<128, kEpi>(ep, nb, 1) + c0;
+  } else {
+    nb = q >> 2;
+    c0 = (q & 3) * 32;
+    wrow0 = (int64_t)q * 32;
+    wrow1 = 0;
+  }
+  // The weights are constant (no predecessor writes them): one thread per
+  // weight row starts an L2 bulk prefetch of its head before the dependency
+  // wait, so the stream from HBM overlaps the previous kernel's tail and the
+  // K loop below mostly hits L2.
+  if (kGemvPrefetchBytes > 0 && threadIdx.x < kRows) {
+    const int j = threadIdx.x;
+    const int64_t row = (kGlu && j >= 32) ? wrow1 + (j - 32) : wrow0 + j;
+    const int64_t row_bytes = (int64_t)K * 2;
+    const uint32_t bytes = (uint32_t)(row_bytes < kGemvPrefetchBytes ? row_bytes : kGemvPrefetchBytes);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(B + row * ldb), "r"(bytes) : "memory");
+  }
+  pdl_wait();
+  pdl_trigger();
+  const int k8 = K >> 3;
+  for (int j0 = warp * kGemvRowsPerWarp; j0 < kRows; j0 += kGemvWarps * kGemvRowsPerWarp) {
+    const uint4* w[kGemvRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kGemvRowsPerWarp; ++r) {
+      const int j = j0 + r;
+      const int64_t row = (kGlu && j >= 32) ? wrow1 + (j - 32) : wrow0 + j;
+      w[r] = reinterpret_cast<const uint4*>(B + row * ldb);
+    }
+    float acc[kGemvRowsPerWarp][MR];
+#pragma unroll
+    for (int r = 0; r < kGemvRowsPerWarp; ++r)
+#pragma unroll
+      for (int m = 0; m < MR; ++m) acc[r][m] = 0.f;
+    for (int base = lane; base < k8; base += 32 * kGemvUnroll) {
+      uint4 wv[kGemvUnroll][kGemvRowsPerWarp];
+      uint4 av[kGemvUnroll][MR];
+#pragma unroll
+      for (int u = 0; u < kGemvUnroll; ++u) {
+        const int c = base + 32 * u;
+        const bool ok = c < k8;
+#pragma unroll
+        for (int r = 0; r < kGemvRowsPerWarp; ++r) wv[u][r] = ok ? __ldcs(w[r] + c) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int m = 0; m < MR; ++m)
+          av[u][m] = ok && m < ep.M ? __ldg(reinterpret_cast<const uint4*>(A + m * lda) + c) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kGemvUnroll; ++u) {
+        float af[MR][8];
+#pragma unroll
+        for (int m = 0; m < MR; ++m) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&av[u][m]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            af[m][2 * e] = f.x;
+            af[m][2 * e + 1] = f.y;
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kGemvRowsPerWarp; ++r) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&wv[u][r]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+#pragma unroll
+            for (int m = 0; m < MR; ++m)
+              acc[r][m] = fmaf(f.y, af[m][2 * e + 1], fmaf(f.x, af[m][2 * e], acc[r][m]));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kGemvRowsPerWarp; ++r)
+#pragma unroll
+      for (int m = 0; m < MR; ++m) {
+        float x = acc[r][m];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+        if (lane == 0) res[m][j0 + r] = x;
+      }
+  }
+  __syncthreads();
+  if (warp != 0) return;
+  // lane = output row (rows >= M carry zeros and are never stored)
+  const int m = lane < MR ? lane : 0;
+  const bool live = lane < MR && lane < ep.M;
+  const float rs = row_scaled(ep) ? row_inv_rms(ep, lane) : 1.f;
+  float v[32];
+  if constexpr (kGlu) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      float u[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        v[16 * hh + j] = live ? res[m][16 * hh + j] : 0.f;
+        u[j] = live ? res[m][32 + 16 * hh + j] : 0.f;
+        if (row_scaled(ep)) {
+          v[16 * hh + j] = __fmul_rn(v[16 * hh + j], rs);
+          u[j] = __fmul_rn(u[j], rs);
+        }
+      }
+      glu16<128, kEpi>(ep, nb, c0 + 16 * hh, v + 16 * hh, u);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      v[j] = live ? res[m][j] : 0.f;
+      if (row_scaled(ep)) v[j] = __fmul_rn(v[j], rs);
+    }
+  }
+  epilogue_tail<128, kEpi>(ep, v, c0, 0, nb, stg, lane);
+}
+
+// CC_GEMM_GEMV=0 in the environment keeps few-row GEMMs on the tensor-core kernels (A/B runs)
+static bool gemv_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("CC_GEMM_GEMV");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <int MR>
+static int launch_gemv_rows(const cc_gemm_args* a, const EpiParams& ep, cudaStream_t st) {
+  const bool glu = a->epilogue == CC_EPI_GLU;
+  const int chunks = (int)(glu ? a->N / 64 : a->N / 32);
+  const auto* A = static_cast<const __nv_bfloat16*>(a->A);
+  const auto* B = static_cast<const __nv_bfloat16*>(a->B);
+  const int K = (int)a->K;
+  cudaError_t e;
+  switch (a->epilogue) {
+    case CC_EPI_GLU:
+      e = launch_pdl(gemv_kernel<MR, CC_EPI_GLU>, dim3(chunks), dim3(32 * kGemvWarps), 0, st, A, a->lda, B, a->ldb, K, ep);
+      break;
+    case CC_EPI_RESIDUAL:
+      e = launch_pdl(gemv_kernel<MR, CC_EPI_RESIDUAL>, dim3(chunks), dim3(32 * kGemvWarps), 0, st, A, a->lda, B, a->ldb,
+                     K, ep);
+      break;
+    case CC_EPI_QKV_ROPE:
+      e = launch_pdl(gemv_kernel<MR, CC_EPI_QKV_ROPE>, dim3(chunks), dim3(32 * kGemvWarps), 0, st, A, a->lda, B, a->ldb,
+                     K, ep);
+      break;
+    default:
+      e = launch_pdl(gemv_kernel<MR, -1>, dim3(chunks), dim3(32 * kGemvWarps), 0, st, A, a->lda, B, a->ldb, K, ep);
+      break;
+  }
+  if (e != cudaSuccess) return fail(CC_ERR_CUDA, "gemv launch failed: %s", cudaGetErrorString(e));
+  return CC_OK;
+}
+
+static int launch_gemv(const cc_gemm_args* a, const EpiParams& ep, cudaStream_t st) {
+  ProfScope ps(st, OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
+  if (a->M == 1) return launch_gemv_rows<1>(a, ep, st);
+  if (a->M == 2) return launch_gemv_rows<2>(a, ep, st);
+  return launch_gemv_rows<4>(a, ep, st);
+}
+
 // K-slices for a bf16 GEMM of `tiles` output tiles over num_kb K-blocks: > 1
 // only when the tiles fill under half the SMs and each slice keeps >= 8
 // K-blocks (CC_GEMM_SPLITK=0 in the environment: never, for A/B runs)
@@ -1459,6 +1657,9 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
         return narrow ? launch<64, true>(a, ep, kop, st) : launch<128, true>(a, ep, kop, st);
     }
   }
+  // at most 4 rows: stream the weights through the CUDA cores (GEMV)
+  if (a->M <= kGemvMaxRows && a->N % 32 == 0 && a->K % 8 == 0 && gemv_enabled())
+    return launch_gemv(a, ep, st);
   // bf16 GEMMs of few tiles (few rows): 128-wide tiles cut along K
   if (a->N % 128 == 0) {
     const int64_t t128 = ((a->M + kBM - 1) / kBM) * (a->N / 128);

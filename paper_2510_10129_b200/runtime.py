@@ -46,8 +46,11 @@ def gemm(kind: int, epilogue: int, M: int, N: int, K: int, A: torch.Tensor, B: t
          lda: int | None = None, rope=None, q_out=None, ldq: int = 0, q_mode: int = _lib.CC_BF16,
          k_cache=None, v_cache=None, cache_dtype: int = _lib.CC_BF16, dst_rows=None, k_raw=None,
          raw_rows=None, heads=(0, 0, 0), inv_rms=None, ld_ssq: int = 0, xn_out=None, ldxn: int = 0,
-         norm_gain=None, ssq_out=None) -> None:
-    """Direct cc_gemm call (kernel tests and one-off GEMMs)."""
+         norm_gain=None, ssq_out=None, ssq_in=None, n_ssq: int = 0, ld_ssq_in: int = 0,
+         norm_eps: float = 0.0) -> None:
+    """Direct cc_gemm call (kernel tests and one-off GEMMs). ``ssq_in`` /
+    ``n_ssq`` / ``ld_ssq_in`` / ``norm_eps``: a fused-norm consumer forming
+    1/rms per row from a producer's per-32-column partial sums."""
     a = _lib.GemmArgs()
     a.kind, a.epilogue = kind, epilogue
     a.M, a.N, a.K = M, N, K
@@ -64,6 +67,7 @@ def gemm(kind: int, epilogue: int, M: int, N: int, K: int, A: torch.Tensor, B: t
     a.dst_rows, a.k_raw, a.raw_rows = _p(dst_rows), _p(k_raw), _p(raw_rows)
     a.xn_out, a.ldxn, a.norm_gain, a.ssq_out = _p(xn_out), ldxn, _p(norm_gain), _p(ssq_out)
     a.inv_rms, a.ld_ssq = _p(inv_rms), ld_ssq
+    a.ssq_in, a.n_ssq, a.ld_ssq_in, a.norm_eps = _p(ssq_in), n_ssq, ld_ssq_in, norm_eps
     _lib.call("cc_gemm", ctypes.byref(a), _s())
 
 

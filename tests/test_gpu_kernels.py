@@ -204,7 +204,8 @@ def test_gemm_bf16_split_k(M, N, K):
         assert (out.double() - glu).abs().max().item() < 2e-4 * math.sqrt(K) * (1 + glu.abs().max().item())
 
 
-@pytest.mark.parametrize("M,d,Hq,Hkv,dh", [(77, 256, 4, 2, 64), (43, 2048, 16, 2, 128)])  # the second splits K
+@pytest.mark.parametrize("M,d,Hq,Hkv,dh", [(77, 256, 4, 2, 64), (43, 2048, 16, 2, 128),  # the second splits K
+                                             (1, 3584, 28, 4, 128), (3, 256, 4, 2, 64)])  # GEMV (M <= 4)
 def test_gemm_qkv_rope_scatter(M, d, Hq, Hkv, dh):
     from paper_2510_10129_b200 import _lib as L
     from paper_2510_10129_b200.config import RopeParams
@@ -643,3 +644,73 @@ def test_gemm_banded_schedule_is_bitwise_the_same(tmp_path):
     for flag in ("", "3"):
         for key in ("store", "residual", "tf32"):
             assert np.array_equal(outs[flag][key], outs["0"][key]), (flag, key)
+
+
+_GEMV_SCRIPT = r"""
+import sys, math
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from paper_2510_10129_b200 import _lib as L, runtime
+from paper_2510_10129_b200.weights import _interleave_bias, _interleave_glu
+L.load()
+DEV = "cuda:0"
+out = {}
+for M in (1, 2, 3, 4):
+    g = torch.Generator(device=DEV).manual_seed(40 + M)
+    K, N = 3584, 4608
+    A = torch.randn(M, K, device=DEV, generator=g).to(torch.bfloat16)
+    B = (torch.randn(N, K, device=DEV, generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(N, device=DEV, generator=g)
+    C = torch.empty(M, N, device=DEV)
+    runtime.gemm(L.CC_GEMM_BF16, L.CC_EPI_STORE, M, N, K, A, B, bias=bias, C=C, ldc=N, c_mode=L.CC_F32)
+    # residual + the next RMSNorm's fused outputs (bf16 h x gain, per-32-column partial sums)
+    Wr = (torch.randn(K, K, device=DEV, generator=g) * 0.05).to(torch.bfloat16)
+    h = torch.randn(M, K, device=DEV, generator=g)
+    gain = torch.rand(K, device=DEV, generator=g) + 0.5
+    xn = torch.empty(M, K, device=DEV, dtype=torch.bfloat16)
+    ssq = torch.empty(K // 32, M, device=DEV)
+    runtime.gemm(L.CC_GEMM_BF16, L.CC_EPI_RESIDUAL, M, K, K, A, Wr, C=h, ldc=K, c_mode=L.CC_F32,
+                 xn_out=xn, ldxn=K, norm_gain=gain, ssq_out=ssq, ld_ssq=M)
+    # GLU consuming the fused norm (1/rms from the partial sums)
+    FF = 1024
+    wg = torch.randn(FF, K, device=DEV, generator=g) * 0.05
+    wu = torch.randn(FF, K, device=DEV, generator=g) * 0.05
+    W = _interleave_glu(wg, wu).to(torch.bfloat16)
+    b = _interleave_bias(bias[:FF], bias[FF:2 * FF])
+    glu = torch.empty(M, FF, device=DEV)
+    runtime.gemm(L.CC_GEMM_BF16, L.CC_EPI_GLU, M, 2 * FF, K, xn, W, bias=b, C=glu, ldc=FF, c_mode=L.CC_F32,
+                 act=L.CC_ACT_SILU, n_out=FF, ssq_in=ssq, n_ssq=K // 32, ld_ssq_in=M, norm_eps=1e-6)
+    torch.cuda.synchronize()
+    for k, t in (("store", C), ("res", h), ("xn", xn.float()), ("ssq", ssq), ("glu", glu)):
+        out[f"{k}{M}"] = t.cpu().numpy()
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_gemv_matches_tensor_core_path(tmp_path):
+    """GEMMs of at most 4 rows run as a weight-streaming GEMV on the CUDA cores
+    with the tensor-core kernels' epilogue code. Against the tensor-core path
+    (CC_GEMM_GEMV=0: split-K / whole-tile kernels) on the same inputs: STORE,
+    RESIDUAL with the fused RMSNorm outputs (bf16 h x gain, partial sums) and a
+    GLU consuming them agree to fp32 summation-order rounding, M = 1..4."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for flag in ("1", "0"):
+        f = tmp_path / f"gemv_{flag}.npz"
+        env = dict(os.environ, CC_GEMM_GEMV=flag)
+        r = subprocess.run([sys.executable, "-c", _GEMV_SCRIPT, root, str(f)], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[flag] = dict(np.load(f))
+    for key in outs["0"]:
+        a, b = outs["1"][key], outs["0"][key]
+        scale = max(1.0, float(np.abs(b).max()))
+        # xn is bf16 (one rounding step apart at most where h differs in its
+        # last fp32 bit); the GLU consumes xn, so it inherits such a step
+        tol = 1e-2 if key.startswith("xn") else (1e-3 if key.startswith("glu") else 1e-4)
+        d = float(np.abs(a - b).max()) / scale
+        print(f"{key}: max |gemv - tc| / max|tc| = {d:.2e}")
+        assert d < tol, (key, d)
