@@ -34,9 +34,13 @@ constexpr int kEpiWarps = 8;  // two per TMEM lane quarter (column halves)
 constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
 constexpr int kEpiStageBytes = 32 * 32 * 4;
 // 3xTF32: K-blocks (32 K each) accumulated in TMEM before the epilogue folds
-// the partial into fp32 registers (see the MMA loop)
+// the partial into fp32 registers (see the MMA loop). 8 (256 K): the CTA-pair
+// kernel's per-phase handshake (commit, fold, remote arrive) stalls the MMA
+// warp at 4 (C3 scoring GEMMs 6.95 ms per pass at 4, 6.54 at 8, 6.46 with no
+// phases); scoring error vs fp64 median 6.4e-7 -> 6.9e-7, p99 2.79e-6 ->
+// 2.84e-6, selections still exact at C2/C3 (profiles/r2_tf32_phases.md)
 #ifndef CC_TF32_KB_PER_PHASE
-#define CC_TF32_KB_PER_PHASE 4
+#define CC_TF32_KB_PER_PHASE 8
 #endif
 constexpr int kTf32KbPerPhase = CC_TF32_KB_PER_PHASE;
 
@@ -1036,7 +1040,7 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {  // arrive on `b
 template <int BN, bool kTF32, int kEpi = -1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, EpiParams ep,
-                 int num_m2, int num_n, int num_kb, int k_orig, int group_m) {
+                 int num_m2, int num_n, int num_kb, int k_orig, int kb_per_phase, int group_m) {
   using Cfg = Gemm2Cfg<BN, kTF32>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
@@ -1119,35 +1123,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t tmem_u = __shfl_sync(0xffffffffu, tmem_base, 0);
       const uint64_t adesc0 = umma_desc_sw128(smem_u32(smem_a));
       const uint64_t bdesc0 = umma_desc_sw128(smem_u32(smem_b));
+      // 3xTF32: the accumulator buffer rotates every kb_per_phase K-blocks, as
+      // in gemm_kernel (the epilogue folds each phase into fp32 registers);
+      // bf16: one phase per tile
+      const int per_phase = kTF32 ? kb_per_phase : num_kb;
       for (int t = cluster_id; t < tiles; t += n_clusters) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_u + acc * Cfg::ACC_STRIDE;
+        uint32_t d_tmem = 0;
         for (int kb = 0; kb < num_kb; ++kb) {
+          const int kp = kb % per_phase;
+          if (kp == 0) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            d_tmem = tmem_u + acc * Cfg::ACC_STRIDE;
+          }
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           const uint64_t ad = adesc0 + (uint64_t)((stage * Cfg::A_BYTES) >> 4);
           const uint64_t bd = bdesc0 + (uint64_t)((stage * Cfg::B_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < Cfg::KSTEPS; ++k) {
-            tc_mma_pair_warp<kTF32>(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (kb | k) != 0 ? 1u : 0u);
+            tc_mma_pair_warp<kTF32>(d_tmem, ad + 2 * k, bd + 2 * k, Cfg::IDESC, (kp | k) != 0 ? 1u : 0u);
             if constexpr (kTF32) {  // corrections hi*lo + lo*hi into the second accumulator (each CTA holds
                                     // half of B_hi and of B_lo, so hi*[hi;lo] cannot be one N=2*BN MMA here)
               tc_mma_pair_warp<kTF32>(d_tmem + BN, ad + 2 * k, bd + (Cfg::B_SUB >> 4) + 2 * k, Cfg::IDESC,
-                                      (kb | k) != 0 ? 1u : 0u);
+                                      (kp | k) != 0 ? 1u : 0u);
               tc_mma_pair_warp<kTF32>(d_tmem + BN, ad + (Cfg::A_SUB >> 4) + 2 * k, bd + 2 * k, Cfg::IDESC, 1u);
             }
           }
           tc_commit_pair_warp(&empty[stage]);
-          if (kb == num_kb - 1) tc_commit_pair_warp(&tfull[acc]);
+          const bool phase_end = kp == per_phase - 1 || kb == num_kb - 1;
+          if (phase_end) tc_commit_pair_warp(&tfull[acc]);
           if (++stage == Cfg::STAGES) {
             stage = 0;
             phase ^= 1;
           }
-        }
-        if (++acc == 2) {
-          acc = 0;
-          acc_phase ^= 1;
+          if (phase_end && ++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
         }
       }
     }
@@ -1164,6 +1177,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int mb, nb;
       tile_mn(t, num_m2, num_n, group_m, mb, nb);
       const int64_t row0 = (int64_t)mb * 256 + (int64_t)rank * 128 + quarter * 32;
+      if constexpr (kTF32) {
+        // phases folded in registers exactly as gemm_kernel does (bitwise the
+        // same sums), then the same register epilogue
+        const bool glu = epi_of(ep, kEpi) == CC_EPI_GLU;
+        constexpr int NV = BN / 2;
+        float run[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) run[j] = 0.f;
+        const int n_phases = (num_kb + kb_per_phase - 1) / kb_per_phase;
+        for (int ph = 0; ph < n_phases; ++ph) {
+          mbar_wait(&tfull[acc], acc_phase);
+          tc_fence_after();
+          const uint32_t tb = tmem_base + acc * Cfg::ACC_STRIDE + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll
+          for (int j = 0; j < NV; j += 16) {
+            const int col = (glu && j >= NV / 2) ? c_begin + BN / 2 + (j - NV / 2) : c_begin + j;
+            float m16[16], c16[16];
+            tmem_ld16(tb + col, m16);
+            tmem_ld16(tb + BN + col, c16);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) run[j + i] = __fadd_rn(run[j + i], __fadd_rn(m16[i], c16[i]));
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(map_to_rank(&tempty[acc], 0));
+          if (++acc == 2) {
+            acc = 0;
+            acc_phase ^= 1;
+          }
+        }
+        if (glu) {
+#pragma unroll
+          for (int cc = 0; cc < NV / 2; cc += 32) {
+            glu16<BN, kEpi>(ep, nb, c_begin + cc, run + cc, run + NV / 2 + cc);
+            glu16<BN, kEpi>(ep, nb, c_begin + cc + 16, run + cc + 16, run + NV / 2 + cc + 16);
+            epilogue_tail<BN, kEpi>(ep, run + cc, c_begin + cc, row0, nb, stg, lane);
+          }
+        } else {
+#pragma unroll
+          for (int cc = 0; cc < NV; cc += 32) epilogue_tail<BN, kEpi>(ep, run + cc, c_begin + cc, row0, nb, stg, lane);
+        }
+        continue;
+      }
       // 1/rms of this lane's row, formed while the tile's MMAs run
       const float rs = row_scaled(ep) ? row_inv_rms(ep, row0 + lane) : 1.f;
       mbar_wait(&tfull[acc], acc_phase);
@@ -1263,7 +1319,8 @@ static int launch_pair(const cc_gemm_args* a, const EpiParams& ep, int64_t kop, 
   const int group_m = schedule_band(a, kTF32 ? 12.0 : 2.0, 8);  // bands of 8 m-pairs
   ProfScope ps(st, kTF32 ? OP_GEMM_TF32X3 : OP_GEMM_BF16, 2.0 * (double)a->M * (double)a->N * (double)a->K);
   const cudaError_t e = launch_pdl(gemm2_kernel<BN, kTF32, kEpi>, dim3(2 * clusters), dim3(kGemmThreads),
-                                   Cfg::SMEM_BYTES, st, ta, tb, ep, num_m2, num_n, num_kb, (int)a->K, group_m);
+                                   Cfg::SMEM_BYTES, st, ta, tb, ep, num_m2, num_n, num_kb, (int)a->K,
+                                   kTF32 ? kTf32KbPerPhase : num_kb, group_m);
   if (e != cudaSuccess) return fail(CC_ERR_CUDA, "gemm (CTA pair) launch failed: %s", cudaGetErrorString(e));
   return CC_OK;
 }
@@ -1540,6 +1597,16 @@ static bool pair_enabled() {
   return on == 1;
 }
 
+// CC_TF32_PAIR=0 keeps every 3xTF32 GEMM on single-CTA tiles (A/B runs)
+static bool tf32_pair_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("CC_TF32_PAIR");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 }  // namespace cc
 
 using namespace cc;
@@ -1643,6 +1710,22 @@ extern "C" int cc_gemm(const cc_gemm_args* a, void* stream) {
     // 128-wide tiles would leave over half the SMs idle (GLU tiles need >= 128)
     const int64_t t128 = ((a->M + kBM - 1) / kBM) * ((a->N + 127) / 128);
     const bool narrow = a->epilogue != CC_EPI_GLU && 2 * t128 <= num_sms();
+    // large M (the C3 scoring pass, M = 2048): 256-row CTA-pair tiles, each
+    // CTA loading half of B (48 instead of 64 KB of operands per K-block per
+    // SM; the split operands make these GEMMs operand-bandwidth bound):
+    // 7.10 -> 6.5 ms per 24-layer pass on the C3 shapes (scripts/bench_gemm.py)
+    if (tf32_pair_enabled() && a->M >= 1024 && a->N % 128 == 0) {
+      switch (a->epilogue) {
+        case CC_EPI_GLU:
+          return launch_pair<128, true, CC_EPI_GLU>(a, ep, kop, st);
+        case CC_EPI_RESIDUAL:
+          return launch_pair<128, true, CC_EPI_RESIDUAL>(a, ep, kop, st);
+        case CC_EPI_QKV_ROPE:
+          return launch_pair<128, true, CC_EPI_QKV_ROPE>(a, ep, kop, st);
+        default:
+          return launch_pair<128, true>(a, ep, kop, st);
+      }
+    }
     // specialised on the epilogue (the scoring model's four), generic otherwise
     switch (a->epilogue) {
       case CC_EPI_GLU:

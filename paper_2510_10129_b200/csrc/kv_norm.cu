@@ -678,7 +678,13 @@ int cc_device_check(int dev) {
 int cc_assemble_kv(const cc_kv_segment* segs_dev, int32_t n_segs, int64_t n_dst_rows, int32_t n_layers,
                    int32_t kv_heads, int32_t head_dim, int32_t dtype, const double* inv_freq_host,
                    int64_t pos_offset, void* dst_k, void* dst_v, int64_t dst_rows_cap, void* stream) {
-  const int32_t max_ctas = 0;  // full grid (the kernel is grid-stride)
+  // CC_ASSEMBLE_CTAS=n caps the (grid-stride) grid: a capped assembly leaves
+  // thread slots free, so the scoring pass's CTAs co-reside with it on the
+  // side stream instead of queueing behind a full grid. 0: full grid.
+  static const int32_t max_ctas = [] {
+    const char* e = getenv("CC_ASSEMBLE_CTAS");
+    return e ? atoi(e) : 0;
+  }();
   CC_CHECK_ARG(segs_dev && n_segs > 0, CC_ERR_CONSISTENCY, "nothing to merge");
   CC_CHECK_ARG(n_layers > 0 && kv_heads > 0, CC_ERR_DIMENSION, "bad geometry");
   CC_CHECK_ARG(n_dst_rows <= dst_rows_cap, CC_ERR_DIMENSION, "destination capacity %lld < rows %lld",
