@@ -45,7 +45,9 @@ def test_gemm_bf16_store(M, N, K):
     assert err < 1e-3 * math.sqrt(K), err
 
 
-@pytest.mark.parametrize("M,N,K", [(64, 128, 128), (2048, 1152, 896), (33, 4864 * 2 // 2, 896)])
+# (1100, 1152, 2080): CTA-pair tiles with a ragged last pair (rows 1024..1099 in
+# one CTA, none in its peer) and a last phase of 1 K-block (65 = 8 x 8 + 1)
+@pytest.mark.parametrize("M,N,K", [(64, 128, 128), (2048, 1152, 896), (33, 4864 * 2 // 2, 896), (1100, 1152, 2080)])
 def test_gemm_tf32x3_is_fp32_faithful(M, N, K):
     from paper_2510_10129_b200 import _lib as L
     g = torch.Generator(device=DEV).manual_seed(7 + M)
@@ -111,6 +113,32 @@ def test_gemm_tf32x3_row_blocks_bitwise_equal(epi):
         want = torch.nn.functional.silu(gt) * up
         err = ((whole.double() - want).abs() / want.abs().clamp_min(1.0)).max().item()
         assert err < 1e-5, err
+
+
+def test_gemm_tf32x3_pair_ragged_rows_bitwise_equal():
+    """A CTA-pair 3xTF32 GEMM whose last 256-row pair is ragged (M = 1100:
+    rows 1024..1099 in one CTA, none in its peer) equals single-CTA GEMMs
+    over the same rows bitwise (residual epilogue, QKV-width N)."""
+    from paper_2510_10129_b200 import _lib as L
+    M, N, K = 1100, 1152, 896
+    g = torch.Generator(device=DEV).manual_seed(23)
+    a = torch.randn(M, K, device=DEV, generator=g)
+    b = torch.randn(N, K, device=DEV, generator=g) / math.sqrt(K)
+    A = torch.empty(M, 3 * K, device=DEV)
+    B = torch.empty(N, 3 * K, device=DEV)
+    s = torch.cuda.current_stream().cuda_stream
+    L.call("cc_convert_matrix", a.data_ptr(), M, K, A.data_ptr(), L.CC_F32_SPLIT3, 0, s)
+    L.call("cc_convert_matrix", b.data_ptr(), N, K, B.data_ptr(), L.CC_F32_SPLIT3, 1, s)
+    h0 = torch.randn(M, N, device=DEV, generator=g)
+    whole = h0.clone()
+    _gemm(L.CC_GEMM_TF32X3, L.CC_EPI_RESIDUAL, A, B, C=whole, ldc=N, c_mode=L.CC_F32)
+    parts = []
+    for r0, r1 in ((0, 600), (600, M)):   # M < 1024: single-CTA tiles
+        c = h0[r0:r1].clone()
+        _gemm(L.CC_GEMM_TF32X3, L.CC_EPI_RESIDUAL, A[r0:r1], B, C=c, ldc=N, c_mode=L.CC_F32)
+        parts.append(c)
+    torch.cuda.synchronize()
+    assert torch.equal(whole, torch.cat(parts))
 
 
 @pytest.mark.parametrize("epi", ["store", "residual"])
